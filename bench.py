@@ -1,0 +1,339 @@
+#!/usr/bin/env python
+"""Benchmark of the RHOSVD canonical-to-Tucker hot path (BASELINE.json metric:
+"RHOSVD canonical terms/s and FP64 tensor-pipe % of peak at 1/2/4/8 B200").
+
+One "step" = one full rhosvd_c2t call (normalize, Gram, eigensolve, one-sided
+Rayleigh-Ritz + refinement, rank selection, projection, core, and the NCCL
+all-reduces when R-sharded) on the BASELINE.json workload (default cfg 4:
+n = 2048, R = 48 000 multi-particle Newton potential, eps = 1e-5), inputs
+resident in HBM (2.36 GB > L2, so no L2 flush is needed between steps).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config 4] [--impl ours|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...      (R-sharded, strong scaling)
+
+Prints ONE JSON line on rank 0.  `--impl reference` times the CPU oracle (the
+reference arm of this tier) on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "RHOSVD canonical terms/s"
+UNIT = "terms/s"
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", type=int, default=4)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--cpu-sample", type=int, default=0, help="terms in the oracle sample (0 = auto)")
+    ap.add_argument("--report", default="", help="write per-phase report JSON here (rank 0)")
+    return ap.parse_args()
+
+
+# ---------------------------------------------------------------- clocks
+class ClockSampler:
+    FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
+              "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
+              "clocks_event_reasons.sw_power_cap"]
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + ",".join(self.FIELDS),
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for ln in self.proc.stdout:
+            self.lines.append(ln.strip())
+
+    def stop(self):
+        if not self.proc:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=2)
+        except Exception:
+            self.proc.kill()
+        sm, mx, pw, reasons = [], [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+                pw.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        sm_sorted = sorted(sm)
+        med = sm_sorted[len(sm_sorted) // 2] if sm_sorted else None
+        return {"sm_mhz": med, "sm_max_mhz": max(mx) if mx else None, "samples": len(sm),
+                "power_w_max": max(pw) if pw else None, "reasons": sorted(reasons)}
+
+
+# ---------------------------------------------------------------- FP64 peak
+def fp64_peak():
+    """Measured DMMA (mma.sync.m8n8k4.f64) peak from tools/fp64_peak.cu."""
+    exe = os.path.join(ROOT, "build", "fp64_peak")
+    try:
+        if not os.path.exists(exe):
+            from paper_2201_12663_b200.build import build_tools
+            build_tools()
+        out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+        return json.loads(out.stdout.strip().splitlines()[-1])
+    except Exception as e:  # pragma: no cover
+        return {"error": str(e)}
+
+
+# ---------------------------------------------------------------- oracle sample (cpu_baseline / reference arm)
+def oracle_sample(cfg, sample_terms):
+    import numpy as np  # noqa: F401
+    from oracle import rhosvd as oracle_rhosvd
+    from workloads import make_config, make_params
+    p = make_params(cfg)
+    Rs = min(p.R, sample_terms)
+    U1, U2, U3, xi = make_config(p, 0, Rs)
+    t0 = time.perf_counter()
+    o = oracle_rhosvd([U1, U2, U3], xi, eps=p.eps, ranks=p.ranks)
+    dt = time.perf_counter() - t0
+    return Rs, dt, o.ranks
+
+
+def default_sample(cfg):
+    return {1: 200, 2: 2400, 3: 7260, 4: 4000, 5: 4000}[cfg]
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count()
+
+
+def run_reference(args):
+    """Reference arm of this tier: the CPU oracle as it stands, on host cores."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    from workloads import make_params
+    p = make_params(args.config)
+    Rs = args.cpu_sample or default_sample(args.config)
+    for _ in range(max(0, min(args.warmup, 1))):
+        oracle_sample(args.config, Rs)
+    times = []
+    for _ in range(args.steps):
+        Rs_, dt, ranks = oracle_sample(args.config, Rs)
+        times.append(dt)
+    tot = sum(times)
+    val = Rs_ * args.steps / tot
+    sample = f"first {Rs_} of {p.R} terms of {p.name} (n={p.n}, eps={p.eps}), oracle ranks {list(ranks)}"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": p.name, "config_index": args.config, "n": p.n,
+                                        "R": p.R, "eps": p.eps, "sample_terms": Rs_},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle", "sample": sample},
+        "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2201_12663_b200 import rhosvd
+    from workloads import make_config, make_params, shard_bounds
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    distributed = world > 1
+    if distributed:
+        dist.init_process_group("nccl", device_id=dev)
+    lib = rhosvd.lib()
+    p = make_params(args.config)
+    k0, k1 = shard_bounds(p.R, world, rank)
+    U1, U2, U3, xi = make_config(p, k0, k1, backend="torch", device=dev)
+    comm = rhosvd.Comm.nccl() if distributed else None
+    opts = rhosvd.make_opts(eps=p.eps, ranks=p.ranks)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        h = rhosvd.c2t_raw((U1, U2, U3), xi, opts, comm, stream)
+        return h
+
+    def report_of(h):
+        rep = rhosvd.Report()
+        lib.rhosvd_result_report(h, rhosvd.C.byref(rep))
+        return rhosvd._report_dict(rep)
+
+    for _ in range(args.warmup):
+        h = step()
+        last = report_of(h)
+        lib.rhosvd_result_free(h)
+    torch.cuda.synchronize(dev)
+    if distributed:
+        dist.barrier()
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    torch.cuda.synchronize(dev)
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    reps = []
+    e0.record(stream)
+    for _ in range(args.steps):
+        h = step()
+        reps.append(report_of(h))
+        lib.rhosvd_result_free(h)
+    e1.record(stream)
+    torch.cuda.synchronize(dev)
+    clk = clocks.stop()
+    ms = e0.elapsed_time(e1)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if distributed:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = p.R * args.steps / (ms_max * 1e-3)
+
+    # dominant kernel roofline (FP64 DMMA pipe): the core K7 for cfg 2/4, the Gram K1 for cfg 3/5
+    rep = reps[-1]
+    r1, r2, r3 = rep["ranks"]
+    Rl = k1 - k0
+    core_flops = 2.0 * r1 * r2 * r3 * Rl
+    gram_flops = 3.0 * p.n * (p.n + 1) * Rl  # upper-triangle Gram, 3 modes
+    core_ms = sum(r["core_ms"] for r in reps) / len(reps)
+    gram_ms = sum(r["gram_ms"] for r in reps) / len(reps)
+    if core_flops * gram_ms >= gram_flops * core_ms or args.config in (2, 4):
+        dom, fl, kms = "core_kr (K7)", core_flops, core_ms
+    else:
+        dom, fl, kms = "gram (K1)", gram_flops, gram_ms
+    peak = fp64_peak() if rank == 0 else {}
+    peak_tf = peak.get("dmma_tflops")
+    achieved = fl / (kms * 1e-3) / 1e12 if kms > 0 else None
+    roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
+            "frac": (achieved / peak_tf) if (achieved and peak_tf) else None, "traffic": None,
+            "peak_source": "measured DMMA m8n8k4.f64 microbenchmark (tools/fp64_peak.cu) on this GPU; "
+                           "MEASURED_PEAKS.json has no FP64 entry",
+            "peak_detail": peak, "algorithmic_flop_per_launch": fl, "kernel_ms": kms,
+            "other": {"gram_tflops": gram_flops / (gram_ms * 1e-3) / 1e12 if gram_ms > 0 else None,
+                      "core_tflops": core_flops / (core_ms * 1e-3) / 1e12 if core_ms > 0 else None,
+                      "gram_ms": gram_ms, "core_ms": core_ms}}
+
+    # ---- e2e: host buffers through the public API (H2D of inputs, D2H of results inside the timer)
+    e2e = None
+    if not args.no_e2e:
+        hU = [u.cpu().pin_memory() for u in (U1, U2, U3)]
+        hx = xi.cpu().pin_memory()
+        h2d = sum(u.numel() * 8 for u in hU) + hx.numel() * 8
+        d2h = 0
+
+        def e2e_step():
+            nonlocal d2h
+            dU = [u.to(dev, non_blocking=True) for u in hU]
+            dx = hx.to(dev, non_blocking=True)
+            res = rhosvd.c2t(dU, dx, eps=p.eps, ranks=p.ranks, comm=comm, keep_w=False)
+            outs = [res.beta.cpu()] + [z.cpu() for z in res.Z] + [s.cpu() for s in res.sigma]
+            d2h = sum(o.numel() * 8 for o in outs)
+            return outs
+
+        e2e_step()
+        torch.cuda.synchronize(dev)
+        if distributed:
+            dist.barrier()
+        ks = max(1, min(args.steps, 3))
+        t0 = time.perf_counter()
+        q0 = torch.cuda.Event(enable_timing=True)
+        q1 = torch.cuda.Event(enable_timing=True)
+        q0.record(stream)
+        for _ in range(ks):
+            e2e_step()
+        q1.record(stream)
+        torch.cuda.synchronize(dev)
+        ems = q0.elapsed_time(q1)
+        te = torch.tensor([ems], dtype=torch.float64, device=dev)
+        if distributed:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e = {"value": p.R * ks / (float(te.item()) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+               "d2h_bytes_per_step": d2h, "steps": ks, "wall_s": time.perf_counter() - t0}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        Rs = args.cpu_sample or default_sample(args.config)
+        Rs_, dt, oranks = oracle_sample(args.config, Rs)
+        cpu = {"value": Rs_ / dt, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+               "sample": f"first {Rs_} of {p.R} terms of {p.name} (n={p.n}, eps={p.eps}); oracle ranks "
+                         f"{list(oranks)}; {dt:.2f} s"}
+
+    if rank == 0:
+        launches = sum(r["launches"] for r in reps)
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": p.name, "config_index": args.config, "n": p.n, "R": p.R,
+                       "eps": p.eps, "ranks": p.ranks, "parallelism": f"R-sharded x{world}",
+                       "l2": "inputs (3 n R fp64 = %.2f GB) larger than L2; no flush" % (3 * p.n * p.R * 8 / 1e9)},
+            "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "clocks": clk,
+            "result": {"ranks": rep["ranks"], "block": rep["block"], "iters": rep["iters"],
+                       "tail": rep["tail"], "beta_norm": rep["beta_norm"], "phase_ms": rep["ms"],
+                       "gemm_tflop_executed": rep["gemm_flops"] / 1e12},
+        }
+        print(json.dumps(line), flush=True)
+        if args.report:
+            with open(args.report, "w") as f:
+                json.dump({"reports": reps, "line": line}, f, indent=1)
+    if comm is not None:
+        comm.close()
+    if distributed:
+        dist.barrier()
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

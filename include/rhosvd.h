@@ -1,0 +1,178 @@
+/*
+ * rhosvd.h - C ABI of the B200-native RHOSVD canonical-to-Tucker (C2T) library
+ *            (librhosvd.so, built from paper_2201_12663_b200/csrc for sm_100a).
+ *
+ * What it computes (arXiv 2201.12663, section 2.1):
+ *   Input  : a rank-R canonical tensor (Eq. can_A3)
+ *              A = sum_k xi_k u_k^(1) (x) u_k^(2) (x) u_k^(3),
+ *            given as three side matrices U_l = [u_1 ... u_R] in R^{n x R}
+ *            (Eq. can_A_Tuck) and the weights xi.
+ *   Output : the RHOSVD Tucker approximation (Def. 2.1)
+ *              A_(r)^0 = beta x_1 Z_1 x_2 Z_2 x_3 Z_3,
+ *            Z_l = the r_l dominant left singular vectors of the normalized
+ *            side matrix Uhat_l (Eq. svdr), sigma_l the
+ *            retained singular values, and the core
+ *              beta = xi' x_l (Z_l^T Uhat_l)   (Prop. 2.1),
+ *            i.e. beta[a,b,c] = sum_k xi'_k W1[a,k] W2[b,k] W3[c,k].
+ *
+ * Conventions:
+ *   - A2: columns are normalized internally (2-norm per column per mode);
+ *     xi'_k = xi_k * prod_l ||u_k^(l)||.  Inputs are never modified.
+ *   - A3: a zero column stays zero and gets xi'_k = 0.
+ *   - A1: eps mode selects r_l = min{ r >= 1 : sum_{k>r} sigma_{l,k}^2
+ *     <= eps^2 * T_l }, T_l = ||Uhat_l||_F^2.  The GPU evaluates the tail as
+ *     sum_{r<k<=b} sigma_k^2 + ||Uhat_l - Z_b W_b||_F^2 (direct residual).
+ *   - A17: fixed mode clamps r_l to min(n, R_global).
+ *   - A9: frame columns are sign-fixed (largest-|.| entry positive, lowest
+ *     row index on ties) when RHOSVD_F_SIGN_FIX is set (default).
+ *   - FP64 (IEEE binary64) throughout.
+ *
+ * Memory: every array pointer is a CUDA DEVICE pointer unless the comment
+ * says "host".  All matrices are column-major:
+ *   U_l : n x R_local, leading dimension ldu >= n (column k = u_k^(l)
+ *         contiguous) == a C-contiguous (R_local, n) row-major array.
+ *   xi  : R_local doubles.
+ *
+ * Errors: every entry point returns an rhosvd_status (0 = OK).  On error the
+ * *out handle is set to NULL and rhosvd_last_error() (thread-local) holds a
+ * message.  In multi-rank mode every rank returns the same status.
+ *
+ * Thread safety: calls on different streams/handles may run concurrently;
+ * one rhosvd_comm must not be used by two calls at once.
+ */
+#ifndef RHOSVD_H_
+#define RHOSVD_H_
+
+#include <stdint.h>
+#include <stddef.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  RHOSVD_OK = 0,
+  RHOSVD_EINVAL = -1,      /* bad argument (null pointer, n < 1, R_local < 0, ldu < n, eps not in (0,1), r < 1) */
+  RHOSVD_ENONFINITE = -2,  /* NaN/Inf in U or xi (detected by the normalisation kernel) */
+  RHOSVD_ENOCONV = -3,     /* a small dense solver (Jacobi / Cholesky) did not converge */
+  RHOSVD_ENOMEM = -4,      /* device allocation failed */
+  RHOSVD_ECUDA = -5,       /* CUDA runtime error */
+  RHOSVD_ENCCL = -6,       /* collective failed */
+  RHOSVD_EMISMATCH = -7    /* ranks disagree on n / options */
+} rhosvd_status;
+
+enum { RHOSVD_FIXED_RANK = 0, RHOSVD_EPS = 1 };
+enum { RHOSVD_F_SIGN_FIX = 1u, RHOSVD_F_KEEP_W = 2u };
+
+/* Options.  Initialise with rhosvd_opts_default(). */
+typedef struct {
+  int32_t  rank_mode;    /* RHOSVD_FIXED_RANK or RHOSVD_EPS                                  */
+  int32_t  r[3];         /* fixed mode: requested r_l >= 1 (clamped to min(n, R_global))      */
+  double   eps;          /* eps mode: 0 < eps < 1, relative Frobenius tail per mode (A1)     */
+  int32_t  oversample;   /* p: block size b = r + p (default 16)                             */
+  int32_t  block0;       /* eps mode: first block size (default 128); grows adaptively       */
+  int32_t  max_iters;    /* subspace-iteration cap per block size (default 30)               */
+  int32_t  refine_steps; /* non-squared refinement steps (default 1)                         */
+  uint64_t seed;         /* start-block seed                                                 */
+  uint32_t flags;        /* default RHOSVD_F_SIGN_FIX                                        */
+} rhosvd_opts;
+
+/* Per-call report (host struct).  ms[] holds per-phase device times:
+ *   0 normalize, 1 gram, 2 eigensolve (subspace iteration), 3 one-sided RR +
+ *   refinement, 4 residual + rank, 5 projection W_r, 6 core, 7 collectives,
+ *   8 total (all in milliseconds, CUDA events on the call's stream). */
+typedef struct {
+  double  trace[3];      /* T_l = ||Uhat_l||_F^2                                   */
+  double  tail[3];       /* (sum_{k>r_l} sigma_{l,k}^2)^{1/2} (direct residual form) */
+  double  xi_norm;       /* ||xi'||                                                */
+  double  bound_paper;   /* ||xi'|| sum_l tail_l           (Thm. 2.2) */
+  double  bound_ns;      /* ||xi'|| (sum_l tail_l^2)^{1/2} (reading A12)           */
+  double  beta_norm;     /* ||beta||_F                                             */
+  double  rho[3];        /* ||Uhat_l - Z_b W_b||_F^2 (out-of-block energy)         */
+  int32_t ranks[3];
+  int32_t block[3];      /* final block size b_l                                   */
+  int32_t iters[3];      /* subspace iterations                                    */
+  int32_t grow_events[3];
+  int64_t R_global;
+  double  ms[16];
+  double  gemm_flops;    /* executed DMMA flops (all GEMM-type kernels)            */
+  double  core_ms;       /* device time of the core kernel(s) alone                */
+  double  gram_ms;       /* device time of the Gram kernel(s) alone                */
+  int32_t launches;      /* kernels launched by this call                          */
+} rhosvd_report;
+
+typedef struct rhosvd_comm rhosvd_comm;       /* NULL => single GPU                */
+typedef struct rhosvd_result rhosvd_result;   /* opaque; owns all device outputs   */
+typedef void* rhosvd_stream;                  /* a cudaStream_t (NULL = legacy)    */
+
+/* Host-side all-reduce callback (sum, fp64) for rhosvd_comm_init_callback:
+ * must leave the element-wise sum over all ranks in `dptr` (device pointer,
+ * `count` doubles) when it returns; work queued on `stream` before the call
+ * is complete when the library invokes it.  Returns 0 on success. */
+typedef int (*rhosvd_allreduce_fn)(double* dptr, int64_t count, rhosvd_stream stream, void* user);
+
+void rhosvd_opts_default(rhosvd_opts* o);                                   /* host */
+
+/* Multi-GPU (R-sharded).  NCCL communicator from a unique id
+ * (128 host bytes) created on rank 0 and broadcast by the caller. */
+int  rhosvd_nccl_get_unique_id(uint8_t id[128]);                            /* host */
+int  rhosvd_comm_init_nccl(const uint8_t id[128], int world, int rank, rhosvd_comm** out);
+/* Host-callback communicator (e.g. torch.distributed gloo); used by tests. */
+int  rhosvd_comm_init_callback(rhosvd_allreduce_fn fn, void* user, int world, int rank,
+                               rhosvd_comm** out);
+void rhosvd_comm_destroy(rhosvd_comm* c);
+
+/* The product entry point: RHOSVD C2T of the local column block.
+ *   U1,U2,U3 : device, n x R_local column-major, leading dimension ldu >= n
+ *   xi       : device, R_local weights
+ *   comm     : NULL for one GPU; otherwise every rank calls collectively with
+ *              the same n and opts and its own contiguous column block
+ *   stream   : cudaStream_t the work is ordered on
+ *   out      : receives a result handle (free with rhosvd_result_free)
+ * Blocks the host until the result is complete (ranks size the outputs). */
+int  rhosvd_c2t(const double* U1, const double* U2, const double* U3, int64_t ldu,
+                const double* xi, int64_t n, int64_t R_local, const rhosvd_opts* opts,
+                rhosvd_comm* comm, rhosvd_stream stream, rhosvd_result** out);
+
+/* Result accessors (device pointers stay owned by the handle). */
+int  rhosvd_result_ranks   (const rhosvd_result* res, int32_t r[3]);               /* host out */
+int  rhosvd_result_frame   (const rhosvd_result* res, int mode, const double** Z, int64_t* ldz); /* n x r_l col-major */
+int  rhosvd_result_sigma   (const rhosvd_result* res, int mode, const double** s, int64_t* count); /* r_l values, descending */
+int  rhosvd_result_core    (const rhosvd_result* res, const double** beta);        /* r1 x r2 x r3, C order */
+int  rhosvd_result_cpfactor(const rhosvd_result* res, int mode, const double** W, int64_t* ldw); /* r_l x R_local row-major (KEEP_W) */
+int  rhosvd_result_report  (const rhosvd_result* res, rhosvd_report* host_out);
+void rhosvd_result_free    (rhosvd_result* res);
+const char* rhosvd_last_error(void);
+const char* rhosvd_version(void);
+
+/* ---- kernel-level entry points (used by the parity unit tests and bench) ----
+ * Each runs ONE device kernel family on `stream`, all pointers device.     */
+
+/* K1 Gram: G = Uhat Uhat^T (n x n, col-major, ldg) for Uhat n x R (ld ldu).
+ * Full symmetric output. (SVD of the side matrices.) */
+int rhosvd_gram(const double* U, int64_t ldu, int64_t n, int64_t R,
+                double* G, int64_t ldg, rhosvd_stream stream);
+
+/* Generic DMMA GEMM (col-major): C = alpha * op(A) op(B) + beta * C,
+ * op(X) = X or X^T selected by transa/transb ('N'/'T'). M x N x K. */
+int rhosvd_dgemm(char transa, char transb, int64_t M, int64_t N, int64_t K, double alpha,
+                 const double* A, int64_t lda, const double* B, int64_t ldb, double beta,
+                 double* C, int64_t ldc, rhosvd_stream stream);
+
+/* Symmetric Jacobi eigensolver (b x b, col-major lda): on return A's diagonal
+ * is overwritten, lambda (b) holds the eigenvalues in descending order and V
+ * (b x b, ldv) the eigenvectors.  High relative accuracy for scaled-diagonally
+ * dominant positive definite input (stopping rule |a_pq| <= tol sqrt(a_pp a_qq)). */
+int rhosvd_syevj(int64_t b, double* A, int64_t lda, double* lambda, double* V, int64_t ldv,
+                 double tol, int32_t* sweeps_out, rhosvd_stream stream);
+
+/* Core: beta[a,b,c] = sum_k xi[k] W1[a,k] W2[b,k] W3[c,k]; W_l row-major
+ * r_l x R with leading dimension ldw; beta C order.  (Prop. 2.1.) */
+int rhosvd_core(const double* W1, const double* W2, const double* W3, int64_t ldw,
+                const double* xi, int64_t r1, int64_t r2, int64_t r3, int64_t R,
+                double* beta, rhosvd_stream stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RHOSVD_H_ */

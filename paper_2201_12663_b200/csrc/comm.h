@@ -1,0 +1,22 @@
+// comm.h - communicator handle behind rhosvd_comm (NCCL or host callback).
+#pragma once
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+
+struct NcclUid {
+  char b[128];
+};
+
+struct rhosvd_comm {
+  enum Kind { NCCL = 0, CALLBACK = 1 } kind = NCCL;
+  void* nccl = nullptr;  // ncclComm_t
+  rhosvd_allreduce_fn fn = nullptr;
+  void* user = nullptr;
+  int world = 1, rank = 0;
+};
+
+namespace rhosvd {
+// in-place fp64 sum all-reduce over all ranks (no-op for world == 1 / null comm)
+int comm_allreduce(rhosvd_comm* c, double* p, int64_t count, cudaStream_t st);
+}  // namespace rhosvd

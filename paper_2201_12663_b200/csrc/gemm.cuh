@@ -1,0 +1,48 @@
+// gemm.cuh - FP64 DMMA GEMM engine for sm_100a (host-side descriptor + launcher).
+//
+// Every dense contraction on the RHOSVD hot path is one of
+//   C = alpha * op(A) op(B) * diag(col_scale) (row-scaled) + beta * C
+// with op(A)(m,k) = a_k ? A[m*lda + k] : A[k*lda + m] and
+//      op(B)(k,n) = b_k ? B[n*ldb + k] : B[k*ldb + n],   C(m,n) = C[n*ldc + m].
+// K1 Gram, the subspace-iteration products, the one-sided
+// Rayleigh-Ritz Grams, the projections W = Z^T Uhat and
+// the refinement are all instances; the core (Prop. 2.1) has its own kernel.
+#pragma once
+#include "common.cuh"
+
+namespace rhosvd {
+
+enum GemmEpi { EPI_STORE = 0, EPI_RESID = 1 };
+
+struct GemmArgs {
+  int64_t M = 0, N = 0, K = 0;
+  const double* A = nullptr;
+  int64_t lda = 0;
+  bool a_k = false;  // A stored k-contiguous (A[m*lda + k])
+  const double* B = nullptr;
+  int64_t ldb = 0;
+  bool b_k = false;  // B stored k-contiguous (B[n*ldb + k])
+  double* C = nullptr;
+  int64_t ldc = 0;
+  double alpha = 1.0, beta = 0.0;
+  const double* col_scale = nullptr;  // per output column n
+  const double* row_scale = nullptr;  // per output row m
+  bool upper_sym = false;             // M == N symmetric: compute upper tiles, mirror
+  int epi = EPI_STORE;
+  const double* D = nullptr;          // EPI_RESID: sum_{m,n} (D(m,n) - acc)^2
+  int64_t ldd = 0;
+  double* resid_out = nullptr;        // EPI_RESID: one double (device), overwritten
+  int splits = 0;                     // 0 = auto
+};
+
+// Scratch for split-K partials (grown on demand, stream-ordered).
+struct Scratch {
+  double* ptr = nullptr;
+  size_t cap = 0;  // doubles
+  int ensure(size_t doubles, cudaStream_t st);
+  void release(cudaStream_t st);
+};
+
+int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc = nullptr);
+
+}  // namespace rhosvd

@@ -1,0 +1,23 @@
+// kernels.h - host wrappers of the device kernels (internal).
+#pragma once
+#include "common.cuh"
+
+namespace rhosvd {
+int k_normalize(const double* U, int64_t ldu, int64_t n, int64_t R, int64_t Rp, double* Uh, int64_t ldn,
+                double* s, double* tcol, int* flag, cudaStream_t st);
+int k_xiprime(const double* xi, const double* s1, const double* s2, const double* s3, int64_t R, int64_t Rp,
+              double* xip, double* xip2, int* flag, cudaStream_t st);
+int k_fixed_sum(const double* x, int64_t n, double* out, cudaStream_t st);
+int k_sumsq(const double* x, int64_t n, double* part, double* out, cudaStream_t st);
+int k_random(double* M, int64_t ldm, int64_t n, int64_t c0, int64_t c1, uint64_t seed, cudaStream_t st);
+int k_ritz_floor(const double* th, int64_t b, double tau, double* inv, cudaStream_t st);
+int k_select_rank(const double* lam, int64_t b, const double* rho, double T, double eps, int r_fixed, int guard,
+                  double* tail2, double* out, double* sigma, cudaStream_t st);
+int k_sign_fix(double* Z, int64_t ldz, int64_t n, int64_t r, double* W, int64_t ldw, int64_t Rl, double* sgn,
+               cudaStream_t st);
+int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3, int64_t ldw, int64_t r1,
+            int64_t r2, int64_t r3, int64_t R, double* beta, double* part, size_t part_cap, cudaStream_t st,
+            double* flops_acc);
+int scale_cols(const double* W, int64_t ldw, const double* xi, int64_t r, int64_t R, double* out, int64_t ldo,
+               cudaStream_t st);
+}  // namespace rhosvd

@@ -1,0 +1,724 @@
+// rhosvd.cu - host orchestration and C ABI of the B200-native RHOSVD C2T path.
+//
+// Pipeline per call; all arithmetic runs in the kernels
+// of this library, collectives are fp64 sum all-reduces over the R shards:
+//   S1 normalize       Uhat_l = U_l diag(s_l)^-1, xi' = xi prod_l s_l, T_l
+//   S2 Gram            G_l = Uhat_l Uhat_l^T                     [all-reduce]
+//   S3 subspace iter.  Z <- CholQR(G Z V Theta^-1) with Rayleigh-Ritz alignment
+//                      (Jacobi on Z^T G Z), adaptive block b = r + p          (Eq. svdr)
+//   S4 one-sided RR    W = Z^T Uhat, W W^T = P Lambda P^T (Jacobi, high relative
+//                      accuracy)                                   [all-reduce]
+//      refinement      Z' = CholQR(Uhat W^T P Lambda^-1) (non-squared)  [all-reduce]
+//      final RR        W' = Z'^T Uhat, W' W'^T = P' Lambda' P'^T, sigma = sqrt(Lambda')
+//      rank            tail(r) = sum_{r<k<=b} Lambda'_k + ||Uhat - Z'W'||_F^2 <= eps^2 T  (A1, D2)
+//   S5 projection      Z_l = Z' P'_r, W_l = P'_r^T W' (= Z_l^T Uhat_l)
+//   S6 core            beta = (W1 (.) W2)(xi' o W3)^T                   [all-reduce]   (Prop. 2.1)
+//   S7 report          tails, ||xi'||, Thm. 2.2 bound and its orthogonal form, ||beta||
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "comm.h"
+#include "gemm.cuh"
+#include "kernels.h"
+#include "small_dense.cuh"
+
+namespace rhosvd {
+
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+
+void set_error(const std::string& msg) { g_err = msg; }
+int fail(int status, const std::string& msg) {
+  g_err = msg;
+  return status;
+}
+
+int num_sms() {
+  static int s = 0;
+  if (!s) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
+    if (s <= 0) s = 148;
+  }
+  return s;
+}
+
+struct DBuf {
+  double* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t n, cudaStream_t st) {
+    if (n <= cap && p) return RHOSVD_OK;
+    if (p) cudaFreeAsync(p, st);
+    p = nullptr;
+    cap = 0;
+    size_t want = std::max<size_t>(n, 64);
+    cudaError_t e = cudaMallocAsync((void**)&p, want * sizeof(double), st);
+    if (e != cudaSuccess) {
+      p = nullptr;
+      cudaGetLastError();
+      return fail(RHOSVD_ENOMEM, std::string("workspace alloc: ") + cudaGetErrorString(e));
+    }
+    cap = want;
+    return RHOSVD_OK;
+  }
+  // zero-initialised growth (padding must be zero)
+  int ensure_zero(size_t n, cudaStream_t st) {
+    if (n <= cap && p) return RHOSVD_OK;
+    RH_CHECK(ensure(n, st));
+    RH_CUDA(cudaMemsetAsync(p, 0, cap * sizeof(double), st));
+    return RHOSVD_OK;
+  }
+};
+
+struct Workspace {
+  DBuf Uh, s, tcol, xip, xip2, scal, part;
+  DBuf G, Z, Y, M, T1;
+  DBuf H, V, S, Bp, th, inv, tail2, sgn;
+  DBuf W, X, W1x, corepart;
+  Scratch gsc;
+  DenseWs dws;
+  int* flag = nullptr;
+};
+static Workspace& WS() {
+  static Workspace w;
+  return w;
+}
+static std::mutex g_mu;
+
+// ------------------------------------------------------------------ phase timer
+struct PhaseTimer {
+  cudaStream_t st;
+  std::vector<cudaEvent_t> ev;
+  std::vector<int> phase;
+  explicit PhaseTimer(cudaStream_t s) : st(s) {}
+  void mark(int ph) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    ev.push_back(e);
+    phase.push_back(ph);
+  }
+  // accumulate [mark i, mark i+1) into ms[phase[i]]
+  void collect(double* ms) {
+    cudaEventSynchronize(ev.back());
+    for (size_t i = 0; i + 1 < ev.size(); ++i) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, ev[i], ev[i + 1]);
+      if (phase[i] >= 0) ms[phase[i]] += t;
+    }
+    float tot = 0.f;
+    cudaEventElapsedTime(&tot, ev.front(), ev.back());
+    ms[8] = tot;
+  }
+  ~PhaseTimer() {
+    for (auto e : ev) cudaEventDestroy(e);
+  }
+};
+enum { PH_NORM = 0, PH_GRAM = 1, PH_EIG = 2, PH_RR = 3, PH_RANK = 4, PH_PROJ = 5, PH_CORE = 6, PH_COMM = 7 };
+
+struct Ctx {
+  cudaStream_t st;
+  rhosvd_comm* comm;
+  Workspace& w;
+  rhosvd_report* rep;
+  PhaseTimer* tm;
+  double flops = 0.0;
+};
+
+// ------------------------------------------------------------------ GEMM shorthands
+// all matrices column-major; "n x b" buffers use ld = LDN
+static int mm(Ctx& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t lda, bool ak, const double* B,
+              int64_t ldb, bool bk, double* C, int64_t ldc, const double* cs = nullptr, bool upper = false,
+              const double* rs = nullptr) {
+  GemmArgs g;
+  g.M = M; g.N = N; g.K = K; g.A = A; g.lda = lda; g.a_k = ak; g.B = B; g.ldb = ldb; g.b_k = bk;
+  g.C = C; g.ldc = ldc; g.col_scale = cs; g.row_scale = rs; g.upper_sym = upper;
+  return gemm(g, c.w.gsc, c.st, &c.flops);
+}
+
+static int allreduce(Ctx& c, double* p, int64_t count) {
+  if (!c.comm || c.comm->world <= 1) return RHOSVD_OK;
+  c.tm->mark(PH_COMM);
+  int r = comm_allreduce(c.comm, p, count, c.st);
+  return r;
+}
+
+// CholeskyQR pass: dst = src * D L^{-T}, L = chol(D src^T src D + shift I)
+static int cholqr_pass(Ctx& c, int64_t n, int64_t b, int64_t ldn, const double* src, double* dst, double shift,
+                       int64_t ldb_small) {
+  Workspace& w = c.w;
+  RH_CHECK(mm(c, b, b, n, src, ldn, true, src, ldn, true, w.S.p, ldb_small, nullptr, true));
+  RH_CHECK(chol_inv_scaled(b, w.S.p, ldb_small, shift, w.Bp.p, ldb_small, w.dws, c.st));
+  RH_CHECK(mm(c, n, b, b, src, ldn, false, w.Bp.p, ldb_small, true, dst, ldn));
+  return RHOSVD_OK;
+}
+// orthonormalize M (n x b) into Z: shifted CholQR (robust to rank deficiency) + CholQR2.
+// buffers: in -> out, uses tmp.
+static int orth(Ctx& c, int64_t n, int64_t b, int64_t ldn, const double* in, double* out, double* tmp,
+                int64_t ldb_small, bool shifted) {
+  const double u = 1.1102230246251565e-16;
+  if (shifted) {
+    double shift = 11.0 * ((double)n * b + (double)b * (b + 1)) * u;
+    RH_CHECK(cholqr_pass(c, n, b, ldn, in, tmp, shift, ldb_small));
+    RH_CHECK(cholqr_pass(c, n, b, ldn, tmp, out, 0.0, ldb_small));
+    RH_CHECK(cholqr_pass(c, n, b, ldn, out, tmp, 0.0, ldb_small));
+  } else {
+    RH_CHECK(cholqr_pass(c, n, b, ldn, in, tmp, 0.0, ldb_small));
+    RH_CHECK(cholqr_pass(c, n, b, ldn, tmp, out, 0.0, ldb_small));
+    return RHOSVD_OK;
+  }
+  // result in tmp -> copy to out
+  RH_CUDA(cudaMemcpyAsync(out, tmp, (size_t)ldn * b * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+  return RHOSVD_OK;
+}
+
+struct ModeOut {
+  int r = 0, b = 0, iters = 0, grows = 0;
+  double T = 0, tail2 = 0, rho = 0;
+  double* Z = nullptr;      // n x r (ld LDN), owned by result
+  double* sigma = nullptr;  // r
+  double* W = nullptr;      // r x Rp row-major, owned by result
+};
+
+// eigensolver + one-sided RR + refinement + rank + projection for one mode
+static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int64_t Rp, int64_t Rg,
+                      const double* Uh, const double* G, double T, const rhosvd_opts& o, ModeOut& mo) {
+  Workspace& w = c.w;
+  cudaStream_t st = c.st;
+  const int64_t m = std::min<int64_t>(n, Rg);
+  const bool epsmode = o.rank_mode == RHOSVD_EPS;
+  const int64_t rfix = epsmode ? 0 : std::min<int64_t>(o.r[mode], m);
+  const int p = std::max(1, o.oversample);
+  int64_t b = epsmode ? std::min<int64_t>(m, std::max(o.block0, 2 * p)) : std::min<int64_t>(m, rfix + p);
+  const double u = 1.1102230246251565e-16;
+  const double tau = 1e-13;  // Ritz-value floor relative to theta_1
+  mo.T = T;
+
+  // n x b work buffers sized for the largest possible block m = min(n, R) once, so
+  // block growth keeps their contents; the b x R buffers grow on demand.
+  RH_CHECK(w.Z.ensure((size_t)LDN * m + 64, st));
+  RH_CHECK(w.Y.ensure((size_t)LDN * m + 64, st));
+  RH_CHECK(w.M.ensure((size_t)LDN * m + 64, st));
+  RH_CHECK(w.T1.ensure((size_t)LDN * m + 64, st));
+  {
+    int64_t ldm = round_up(std::max<int64_t>(m, 2), 2);
+    for (DBuf* d : {&w.H, &w.V, &w.S, &w.Bp}) RH_CHECK(d->ensure((size_t)ldm * m + 64, st));
+    for (DBuf* d : {&w.th, &w.inv, &w.tail2, &w.sgn}) RH_CHECK(d->ensure((size_t)m + 64, st));
+  }
+  auto ensure_b = [&](int64_t bb) -> int {
+    RH_CHECK(w.W.ensure((size_t)bb * Rp, st));
+    RH_CHECK(w.X.ensure((size_t)bb * Rp, st));
+    return RHOSVD_OK;
+  };
+  auto ldbs = [&](int64_t bb) { return round_up(std::max<int64_t>(bb, 2), 2); };
+
+  RH_CHECK(ensure_b(b));
+  uint64_t seed = o.seed * 0x9E3779B97F4A7C15ull + (uint64_t)(mode + 1) * 0xD1B54A32D192ED03ull;
+  RH_CHECK(k_random(w.M.p, LDN, n, 0, b, seed, st));
+  RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldbs(b), true));
+
+  std::vector<double> th_h, th_old;
+  double dth_old = -1.0;
+  int it_total = 0, it_b = 0, guard = 0;
+  while (true) {
+    ++it_total;
+    ++it_b;
+    const int64_t ldb = ldbs(b);
+    // Y = G Z ; H = Z^T Y ; eig(H) = V Theta V^T
+    RH_CHECK(mm(c, n, b, n, G, LDN, false, w.Z.p, LDN, true, w.Y.p, LDN));
+    RH_CHECK(mm(c, b, b, n, w.Z.p, LDN, true, w.Y.p, LDN, true, w.H.p, ldb, nullptr, true));
+    int sw = 0;
+    RH_CHECK(syevj(b, w.H.p, ldb, w.th.p, w.V.p, ldb, 1e-14, 1e-16, 60, w.dws, st, &sw));
+    th_h.resize(b);
+    RH_CUDA(cudaMemcpyAsync(th_h.data(), w.th.p, b * sizeof(double), cudaMemcpyDeviceToHost, st));
+    RH_CUDA(cudaStreamSynchronize(st));
+    // rank estimate from (squared) Ritz values - growth decisions only
+    int64_t r_est = -1;
+    if (epsmode) {
+      double thr = o.eps * o.eps * T, acc = 0.0;
+      for (int64_t k = 0; k < b; ++k) {
+        acc += th_h[k];
+        if (T - acc <= thr) {
+          r_est = k + 1;
+          break;
+        }
+      }
+    } else {
+      r_est = rfix;
+    }
+    double dth = -1.0;
+    if (!th_old.empty() && (int64_t)th_old.size() == b && r_est > 0) {
+      dth = 0.0;
+      for (int64_t k = 0; k < r_est; ++k) dth = std::max(dth, std::fabs(th_h[k] - th_old[k]) / std::fabs(th_h[k]));
+    }
+    // M = Y V Theta^-1 (Ritz-aligned, well conditioned: Gram >= I)
+    RH_CHECK(k_ritz_floor(w.th.p, b, tau, w.inv.p, st));
+    RH_CHECK(mm(c, n, b, b, w.Y.p, LDN, false, w.V.p, ldb, true, w.M.p, LDN, w.inv.p));
+    if (epsmode && b < m && (r_est < 0 || r_est + p > b) && guard < 16) {
+      int64_t bn = std::min<int64_t>(m, r_est < 0 ? 2 * b : r_est + p);
+      RH_CHECK(ensure_b(bn));
+      RH_CHECK(k_random(w.M.p, LDN, n, b, bn, seed + 7919ull * (uint64_t)(it_total + 1), st));
+      b = bn;
+      RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldbs(b), true));
+      th_old.clear();
+      dth_old = -1.0;
+      it_b = 0;
+      ++mo.grows;
+      ++guard;
+      continue;
+    }
+    if (epsmode && r_est > 0 && b > r_est + p && guard < 16) {
+      b = r_est + p;  // keep the leading Ritz directions (CholQR preserves leading spans)
+      RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldbs(b), true));
+      th_old.clear();
+      dth_old = -1.0;
+      it_b = 0;
+      ++guard;
+      continue;
+    }
+    RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldb, true));
+    bool conv = dth >= 0.0 && (dth < 1e-10 || (dth_old >= 0.0 && dth > 0.25 * dth_old));
+    if (b >= m && it_b >= 1) conv = true;  // full space: the subspace is exact
+    if (conv || it_b >= std::max(2, o.max_iters)) break;
+    th_old = th_h;
+    dth_old = dth;
+  }
+  mo.iters = it_total;
+  c.tm->mark(PH_RR);
+
+  // ---------------- one-sided Rayleigh-Ritz + non-squared refinement + final RR
+  const int64_t ldb = ldbs(b);
+  auto one_sided_rr = [&](const double* Zc, double* lam, double* P) -> int {
+    // W = Z^T Uhat  (b x Rp row-major, computed as Uhat^T Z col-major Rl x b)
+    RH_CHECK(mm(c, Rl, b, n, Uh, LDN, true, Zc, LDN, true, w.W.p, Rp));
+    // S = W W^T (b x b) summed over all R shards
+    RH_CHECK(mm(c, b, b, Rl, w.W.p, Rp, true, w.W.p, Rp, true, w.S.p, ldb, nullptr, true));
+    RH_CHECK(allreduce(c, w.S.p, ldb * b));
+    c.tm->mark(PH_RR);
+    int sw = 0;
+    RH_CHECK(syevj(b, w.S.p, ldb, lam, P, ldb, 1e-15, 1e-300, 80, w.dws, st, &sw));
+    if (sw < 0) return fail(RHOSVD_ENOCONV, "Jacobi on W W^T did not converge");
+    return RHOSVD_OK;
+  };
+  RH_CHECK(one_sided_rr(w.Z.p, w.th.p, w.V.p));
+  for (int rs = 0; rs < std::max(0, o.refine_steps); ++rs) {
+    // X^T = Lambda^-1 P^T W  (stored as Rl x b col-major), M = Uhat X  (n x b)
+    RH_CHECK(k_ritz_floor(w.th.p, b, tau, w.inv.p, st));
+    RH_CHECK(mm(c, Rl, b, b, w.W.p, Rp, false, w.V.p, ldb, true, w.X.p, Rp, w.inv.p));
+    RH_CHECK(mm(c, n, b, Rl, Uh, LDN, false, w.X.p, Rp, true, w.M.p, LDN));
+    RH_CHECK(allreduce(c, w.M.p, LDN * b));
+    c.tm->mark(PH_RR);
+    RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldb, true));
+    RH_CHECK(one_sided_rr(w.Z.p, w.th.p, w.V.p));
+  }
+  c.tm->mark(PH_RANK);
+  // rho = ||Uhat - Z W||_F^2 (fused residual epilogue; E never stored)
+  {
+    GemmArgs g;
+    g.M = n; g.N = Rl; g.K = b; g.A = w.Z.p; g.lda = LDN; g.a_k = false; g.B = w.W.p; g.ldb = Rp; g.b_k = false;
+    g.epi = EPI_RESID; g.D = Uh; g.ldd = LDN; g.resid_out = w.scal.p + 16 + mode;
+    if (Rl > 0) {
+      RH_CHECK(gemm(g, w.gsc, st, &c.flops));
+    } else {
+      RH_CUDA(cudaMemsetAsync(w.scal.p + 16 + mode, 0, sizeof(double), st));
+    }
+    RH_CHECK(allreduce(c, w.scal.p + 16 + mode, 1));
+    c.tm->mark(PH_RANK);
+  }
+  double sel[4];
+  RH_CHECK(k_select_rank(w.th.p, b, w.scal.p + 16 + mode, T, epsmode ? o.eps : 0.0, (int)rfix, 8, w.tail2.p,
+                         w.scal.p + 24 + 4 * mode, w.inv.p, st));
+  RH_CUDA(cudaMemcpyAsync(sel, w.scal.p + 24 + 4 * mode, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  double rho_h = 0.0;
+  RH_CUDA(cudaMemcpyAsync(&rho_h, w.scal.p + 16 + mode, sizeof(double), cudaMemcpyDeviceToHost, st));
+  RH_CUDA(cudaStreamSynchronize(st));
+  int64_t r = (int64_t)sel[0];
+  if (r < 0) {  // the block did not reach the threshold (should not happen after growth)
+    r = b;
+  }
+  mo.r = (int)r;
+  mo.b = (int)b;
+  mo.tail2 = sel[1];
+  mo.rho = rho_h;
+  c.tm->mark(PH_PROJ);
+  // outputs: Z_l = Z' P'_r, W_l^T = W'^T P'_r (Rl x r col-major == r x Rp row-major), sigma
+  if (r > 0) {
+    RH_CUDA(cudaMallocAsync((void**)&mo.Z, (size_t)LDN * r * sizeof(double), st));
+    RH_CUDA(cudaMemsetAsync(mo.Z, 0, (size_t)LDN * r * sizeof(double), st));
+    RH_CUDA(cudaMallocAsync((void**)&mo.W, (size_t)r * Rp * sizeof(double), st));
+    RH_CUDA(cudaMemsetAsync(mo.W, 0, (size_t)r * Rp * sizeof(double), st));
+    RH_CUDA(cudaMallocAsync((void**)&mo.sigma, (size_t)r * sizeof(double), st));
+    RH_CHECK(mm(c, n, r, b, w.Z.p, LDN, false, w.V.p, ldb, true, mo.Z, LDN));
+    RH_CHECK(mm(c, Rl, r, b, w.W.p, Rp, false, w.V.p, ldb, true, mo.W, Rp));
+    RH_CUDA(cudaMemcpyAsync(mo.sigma, w.inv.p, r * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    if (o.flags & RHOSVD_F_SIGN_FIX) RH_CHECK(k_sign_fix(mo.Z, LDN, n, r, mo.W, Rp, Rl, w.sgn.p, st));
+  }
+  (void)u;
+  return RHOSVD_OK;
+}
+
+}  // namespace rhosvd
+
+// ====================================================================== C ABI
+using namespace rhosvd;
+
+struct rhosvd_result {
+  int32_t ranks[3] = {0, 0, 0};
+  int64_t n = 0, ldz = 0, Rl = 0, Rp = 0;
+  double* Z[3] = {nullptr, nullptr, nullptr};
+  double* sigma[3] = {nullptr, nullptr, nullptr};
+  double* W[3] = {nullptr, nullptr, nullptr};
+  double* beta = nullptr;
+  rhosvd_report rep{};
+};
+
+extern "C" {
+
+const char* rhosvd_last_error(void) { return g_err.c_str(); }
+const char* rhosvd_version(void) { return "rhosvd-b200 0.1 (sm_100a, FP64 DMMA)"; }
+
+void rhosvd_opts_default(rhosvd_opts* o) {
+  if (!o) return;
+  std::memset(o, 0, sizeof(*o));
+  o->rank_mode = RHOSVD_EPS;
+  o->r[0] = o->r[1] = o->r[2] = 10;
+  o->eps = 1e-6;
+  o->oversample = 16;
+  o->block0 = 128;
+  o->max_iters = 30;
+  o->refine_steps = 1;
+  o->seed = 12345;
+  o->flags = RHOSVD_F_SIGN_FIX;
+}
+
+void rhosvd_result_free(rhosvd_result* r) {
+  if (!r) return;
+  cudaDeviceSynchronize();
+  for (int l = 0; l < 3; ++l) {
+    if (r->Z[l]) cudaFree(r->Z[l]);
+    if (r->sigma[l]) cudaFree(r->sigma[l]);
+    if (r->W[l]) cudaFree(r->W[l]);
+  }
+  if (r->beta) cudaFree(r->beta);
+  delete r;
+}
+
+int rhosvd_result_ranks(const rhosvd_result* r, int32_t out[3]) {
+  if (!r || !out) return fail(RHOSVD_EINVAL, "null");
+  for (int l = 0; l < 3; ++l) out[l] = r->ranks[l];
+  return RHOSVD_OK;
+}
+int rhosvd_result_frame(const rhosvd_result* r, int mode, const double** Z, int64_t* ldz) {
+  if (!r || !Z || !ldz || mode < 0 || mode > 2) return fail(RHOSVD_EINVAL, "bad args");
+  *Z = r->Z[mode];
+  *ldz = r->ldz;
+  return RHOSVD_OK;
+}
+int rhosvd_result_sigma(const rhosvd_result* r, int mode, const double** s, int64_t* count) {
+  if (!r || !s || !count || mode < 0 || mode > 2) return fail(RHOSVD_EINVAL, "bad args");
+  *s = r->sigma[mode];
+  *count = r->ranks[mode];
+  return RHOSVD_OK;
+}
+int rhosvd_result_core(const rhosvd_result* r, const double** beta) {
+  if (!r || !beta) return fail(RHOSVD_EINVAL, "bad args");
+  *beta = r->beta;
+  return RHOSVD_OK;
+}
+int rhosvd_result_cpfactor(const rhosvd_result* r, int mode, const double** W, int64_t* ldw) {
+  if (!r || !W || !ldw || mode < 0 || mode > 2) return fail(RHOSVD_EINVAL, "bad args");
+  *W = r->W[mode];
+  *ldw = r->Rp;
+  return RHOSVD_OK;
+}
+int rhosvd_result_report(const rhosvd_result* r, rhosvd_report* out) {
+  if (!r || !out) return fail(RHOSVD_EINVAL, "bad args");
+  *out = r->rep;
+  return RHOSVD_OK;
+}
+
+static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n, int64_t Rl,
+                    const rhosvd_opts& o, rhosvd_comm* comm, cudaStream_t st, rhosvd_result* res) {
+  Workspace& w = WS();
+  rhosvd_report& rep = res->rep;
+  PhaseTimer tm(st);
+  Ctx c{st, comm, w, &rep, &tm};
+  g_launches = 0;
+  tm.mark(PH_NORM);
+  const int world = comm ? comm->world : 1;
+  const int64_t LDN = round_up(n, 16);
+  const int64_t Rp = round_up(std::max<int64_t>(Rl, 1), 16);
+  res->n = n;
+  res->ldz = LDN;
+  res->Rl = Rl;
+  res->Rp = Rp;
+
+  RH_CHECK(w.scal.ensure(256, st));
+  if (!w.flag) RH_CUDA(cudaMallocAsync((void**)&w.flag, 64, st));
+  RH_CUDA(cudaMemsetAsync(w.flag, 0, 64, st));
+  RH_CUDA(cudaMemsetAsync(w.scal.p, 0, 256 * sizeof(double), st));
+
+  // ---- agreement check + global R (SURVEY.md 8(b) EMISMATCH)
+  {
+    double h = (double)((n * 1000003 + o.rank_mode * 97 + o.r[0] * 7 + o.r[1] * 11 + o.r[2] * 13 +
+                         o.oversample * 17 + o.block0 * 19 + o.refine_steps * 23) % 1000000007) +
+               o.eps * 1e6;
+    double v[4] = {(double)Rl, h, h * h, 1.0};
+    RH_CUDA(cudaMemcpyAsync(w.scal.p, v, sizeof(v), cudaMemcpyHostToDevice, st));
+    RH_CHECK(allreduce(c, w.scal.p, 4));
+    RH_CUDA(cudaMemcpyAsync(v, w.scal.p, sizeof(v), cudaMemcpyDeviceToHost, st));
+    RH_CUDA(cudaStreamSynchronize(st));
+    if (std::fabs(v[1] - world * h) > 1e-6 * std::fabs(world * h) + 1e-9 ||
+        std::fabs(v[2] - world * h * h) > 1e-6 * std::fabs(world * h * h) + 1e-9)
+      return fail(RHOSVD_EMISMATCH, "ranks disagree on n / options");
+    rep.R_global = (int64_t)std::llround(v[0]);
+  }
+  const int64_t Rg = rep.R_global;
+  if (Rg == 0) {  // zero tensor: empty Tucker tensor (SURVEY.md 8(b) edge cases)
+    tm.mark(-1);
+    tm.collect(rep.ms);
+    rep.launches = g_launches;
+    return RHOSVD_OK;
+  }
+
+  // ---- S1 normalize (K0)
+  RH_CHECK(w.Uh.ensure((size_t)3 * LDN * Rp, st));
+  RH_CHECK(w.s.ensure((size_t)3 * Rp, st));
+  RH_CHECK(w.tcol.ensure((size_t)3 * Rp, st));
+  RH_CHECK(w.xip.ensure((size_t)Rp, st));
+  RH_CHECK(w.xip2.ensure((size_t)Rp, st));
+  RH_CHECK(w.part.ensure(1024, st));
+  double* Uh[3];
+  for (int l = 0; l < 3; ++l) {
+    Uh[l] = w.Uh.p + (size_t)l * LDN * Rp;
+    RH_CHECK(k_normalize(U[l], ldu, n, Rl, Rp, Uh[l], LDN, w.s.p + l * Rp, w.tcol.p + l * Rp, w.flag, st));
+    RH_CHECK(k_fixed_sum(w.tcol.p + l * Rp, Rp, w.scal.p + 4 + l, st));
+  }
+  RH_CHECK(k_xiprime(xi, w.s.p, w.s.p + Rp, w.s.p + 2 * Rp, Rl, Rp, w.xip.p, w.xip2.p, w.flag, st));
+  RH_CHECK(k_fixed_sum(w.xip2.p, Rp, w.scal.p + 7, st));
+  // flag -> scal[8] as double (non-finite count)
+  {
+    int fl = 0;
+    RH_CUDA(cudaMemcpyAsync(&fl, w.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+    RH_CUDA(cudaStreamSynchronize(st));
+    double f = fl ? 1.0 : 0.0;
+    RH_CUDA(cudaMemcpyAsync(w.scal.p + 8, &f, sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  tm.mark(PH_NORM);
+  RH_CHECK(allreduce(c, w.scal.p + 4, 5));  // T1..T3, ||xi'||^2, flag
+  double sc[5];
+  RH_CUDA(cudaMemcpyAsync(sc, w.scal.p + 4, sizeof(sc), cudaMemcpyDeviceToHost, st));
+  RH_CUDA(cudaStreamSynchronize(st));
+  if (sc[4] != 0.0) return fail(RHOSVD_ENONFINITE, "NaN/Inf in U or xi");
+  for (int l = 0; l < 3; ++l) rep.trace[l] = sc[l];
+  rep.xi_norm = std::sqrt(sc[3]);
+
+  // ---- S2 Gram (K1), all three modes, then all-reduce
+  tm.mark(PH_GRAM);
+  RH_CHECK(w.G.ensure_zero((size_t)3 * LDN * LDN, st));
+  cudaEvent_t g0, g1;
+  cudaEventCreate(&g0);
+  cudaEventCreate(&g1);
+  cudaEventRecord(g0, st);
+  for (int l = 0; l < 3; ++l) {
+    double* G = w.G.p + (size_t)l * LDN * LDN;
+    if (Rl > 0) {
+      RH_CHECK(mm(c, n, n, Rl, Uh[l], LDN, false, Uh[l], LDN, false, G, LDN, nullptr, true));
+    } else {
+      RH_CUDA(cudaMemsetAsync(G, 0, (size_t)LDN * LDN * sizeof(double), st));
+    }
+  }
+  cudaEventRecord(g1, st);
+  RH_CHECK(allreduce(c, w.G.p, 3 * LDN * LDN));
+  tm.mark(PH_EIG);
+
+  // ---- S3-S5 per mode
+  ModeOut mo[3];
+  for (int l = 0; l < 3; ++l) {
+    int st_ = solve_mode(c, l, n, LDN, Rl, Rp, Rg, Uh[l], w.G.p + (size_t)l * LDN * LDN, rep.trace[l], o, mo[l]);
+    if (st_ != RHOSVD_OK) {
+      for (int q = 0; q <= l; ++q) {
+        if (mo[q].Z) cudaFree(mo[q].Z);
+        if (mo[q].W) cudaFree(mo[q].W);
+        if (mo[q].sigma) cudaFree(mo[q].sigma);
+      }
+      return st_;
+    }
+    res->Z[l] = mo[l].Z;
+    res->W[l] = mo[l].W;
+    res->sigma[l] = mo[l].sigma;
+    res->ranks[l] = mo[l].r;
+    rep.ranks[l] = mo[l].r;
+    rep.block[l] = mo[l].b;
+    rep.iters[l] = mo[l].iters;
+    rep.grow_events[l] = mo[l].grows;
+    rep.rho[l] = mo[l].rho;
+    rep.tail[l] = std::sqrt(std::max(0.0, mo[l].tail2));
+    tm.mark(PH_EIG);
+  }
+
+  // ---- S6 core (K7): beta = (W1 (.) W2)(xi' o W3)^T, then all-reduce
+  tm.mark(PH_CORE);
+  const int64_t r1 = mo[0].r, r2 = mo[1].r, r3 = mo[2].r;
+  const int64_t total = r1 * r2 * r3;
+  cudaEvent_t c0, c1;
+  cudaEventCreate(&c0);
+  cudaEventCreate(&c1);
+  if (total > 0) {
+    RH_CUDA(cudaMallocAsync((void**)&res->beta, (size_t)total * sizeof(double), st));
+    RH_CHECK(w.W1x.ensure((size_t)r1 * Rp, st));
+    if (Rl > 0) {
+      RH_CHECK(scale_cols(mo[0].W, Rp, w.xip.p, r1, Rp, w.W1x.p, Rp, st));
+      size_t pc = std::min<size_t>((size_t)total * 8, (size_t)1 << 28);
+      RH_CHECK(w.corepart.ensure(pc, st));
+      cudaEventRecord(c0, st);
+      RH_CHECK(core_kr(w.W1x.p, Rp, mo[1].W, mo[2].W, Rp, r1, r2, r3, Rl, res->beta, w.corepart.p,
+                       w.corepart.cap, st, &c.flops));
+      cudaEventRecord(c1, st);
+    } else {
+      RH_CUDA(cudaMemsetAsync(res->beta, 0, (size_t)total * sizeof(double), st));
+      cudaEventRecord(c0, st);
+      cudaEventRecord(c1, st);
+    }
+    RH_CHECK(allreduce(c, res->beta, total));
+    tm.mark(PH_CORE);
+    RH_CHECK(k_sumsq(res->beta, total, w.part.p, w.scal.p + 12, st));
+  } else {
+    cudaEventRecord(c0, st);
+    cudaEventRecord(c1, st);
+  }
+  tm.mark(-1);
+  double bn2 = 0.0;
+  if (total > 0) {
+    RH_CUDA(cudaMemcpyAsync(&bn2, w.scal.p + 12, sizeof(double), cudaMemcpyDeviceToHost, st));
+  }
+  RH_CUDA(cudaStreamSynchronize(st));
+  RH_CUDA(cudaGetLastError());
+  rep.beta_norm = std::sqrt(bn2);
+  double st1 = 0.0, st2 = 0.0;
+  for (int l = 0; l < 3; ++l) {
+    st1 += rep.tail[l];
+    st2 += rep.tail[l] * rep.tail[l];
+  }
+  rep.bound_paper = rep.xi_norm * st1;  // Thm. 2.2
+  rep.bound_ns = rep.xi_norm * std::sqrt(st2);  // reading A12
+  tm.collect(rep.ms);
+  float gms = 0.f, cms = 0.f;
+  cudaEventElapsedTime(&gms, g0, g1);
+  cudaEventElapsedTime(&cms, c0, c1);
+  rep.gram_ms = gms;
+  rep.core_ms = cms;
+  cudaEventDestroy(g0);
+  cudaEventDestroy(g1);
+  cudaEventDestroy(c0);
+  cudaEventDestroy(c1);
+  rep.gemm_flops = c.flops;
+  rep.launches = g_launches;
+  return RHOSVD_OK;
+}
+
+int rhosvd_c2t(const double* U1, const double* U2, const double* U3, int64_t ldu, const double* xi, int64_t n,
+               int64_t R_local, const rhosvd_opts* opts, rhosvd_comm* comm, rhosvd_stream stream,
+               rhosvd_result** out) {
+  if (!out) return fail(RHOSVD_EINVAL, "out is null");
+  *out = nullptr;
+  if (!opts) return fail(RHOSVD_EINVAL, "opts is null");
+  if (n < 1 || R_local < 0 || ldu < n) return fail(RHOSVD_EINVAL, "need n >= 1, R_local >= 0, ldu >= n");
+  if (R_local > 0 && (!U1 || !U2 || !U3 || !xi)) return fail(RHOSVD_EINVAL, "null input pointer");
+  const rhosvd_opts& o = *opts;
+  if (o.rank_mode == RHOSVD_EPS) {
+    if (!(o.eps > 0.0 && o.eps < 1.0)) return fail(RHOSVD_EINVAL, "eps must lie in (0, 1)");
+  } else if (o.rank_mode == RHOSVD_FIXED_RANK) {
+    if (o.r[0] < 1 || o.r[1] < 1 || o.r[2] < 1) return fail(RHOSVD_EINVAL, "fixed ranks must be >= 1");
+  } else {
+    return fail(RHOSVD_EINVAL, "unknown rank_mode");
+  }
+  if (n > 16384) return fail(RHOSVD_EINVAL, "n > 16384 not supported");
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  static bool pool_set = false;
+  if (!pool_set) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+      uint64_t thr = UINT64_MAX;
+      cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    pool_set = true;
+  }
+  auto* res = new rhosvd_result();
+  const double* U[3] = {U1, U2, U3};
+  int s = c2t_impl(U, ldu, xi, n, R_local, o, comm, st, res);
+  if (s != RHOSVD_OK) {
+    std::string msg = g_err;
+    rhosvd_result_free(res);
+    g_err = msg;
+    return s;
+  }
+  *out = res;
+  return RHOSVD_OK;
+}
+
+// ---------------------------------------------------------------- kernel-level entry points
+int rhosvd_gram(const double* U, int64_t ldu, int64_t n, int64_t R, double* G, int64_t ldg, rhosvd_stream stream) {
+  if (!U || !G || n < 1 || R < 0 || ldu < n || ldg < n) return fail(RHOSVD_EINVAL, "bad args");
+  if ((ldu & 1) || ((uintptr_t)U & 15)) return fail(RHOSVD_EINVAL, "gram: ldu must be even, U 16B-aligned");
+  std::lock_guard<std::mutex> lk(g_mu);
+  GemmArgs g;
+  g.M = n; g.N = n; g.K = R; g.A = U; g.lda = ldu; g.a_k = false; g.B = U; g.ldb = ldu; g.b_k = false;
+  g.C = G; g.ldc = ldg; g.upper_sym = true;
+  g_launches = 0;
+  return gemm(g, WS().gsc, (cudaStream_t)stream);
+}
+
+int rhosvd_dgemm(char ta, char tb, int64_t M, int64_t N, int64_t K, double alpha, const double* A, int64_t lda,
+                 const double* B, int64_t ldb, double beta, double* C, int64_t ldc, rhosvd_stream stream) {
+  if (!A || !B || !C || M < 0 || N < 0 || K < 0) return fail(RHOSVD_EINVAL, "bad args");
+  if ((lda & 1) || (ldb & 1) || ((uintptr_t)A & 15) || ((uintptr_t)B & 15))
+    return fail(RHOSVD_EINVAL, "dgemm: lda/ldb must be even and A/B 16B-aligned");
+  std::lock_guard<std::mutex> lk(g_mu);
+  GemmArgs g;
+  g.M = M; g.N = N; g.K = K; g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc;
+  g.alpha = alpha; g.beta = beta;
+  // op(A)(m,k): 'N' -> A[k*lda + m] (m contiguous), 'T' -> A[m*lda + k] (k contiguous)
+  g.a_k = (ta == 'T' || ta == 't');
+  // op(B)(k,n): 'N' -> B[n*ldb + k] (k contiguous), 'T' -> B[k*ldb + n]
+  g.b_k = !(tb == 'T' || tb == 't');
+  g_launches = 0;
+  return gemm(g, WS().gsc, (cudaStream_t)stream);
+}
+
+int rhosvd_syevj(int64_t b, double* A, int64_t lda, double* lambda, double* V, int64_t ldv, double tol,
+                 int32_t* sweeps_out, rhosvd_stream stream) {
+  if (!A || !lambda || !V || b < 0 || lda < b || ldv < b) return fail(RHOSVD_EINVAL, "bad args");
+  std::lock_guard<std::mutex> lk(g_mu);
+  int sw = 0;
+  RH_CHECK(syevj(b, A, lda, lambda, V, ldv, tol > 0 ? tol : 1e-15, 1e-300, 80, WS().dws, (cudaStream_t)stream, &sw));
+  if (sweeps_out) *sweeps_out = sw;
+  return RHOSVD_OK;
+}
+
+int rhosvd_core(const double* W1, const double* W2, const double* W3, int64_t ldw, const double* xi, int64_t r1,
+                int64_t r2, int64_t r3, int64_t R, double* beta, rhosvd_stream stream) {
+  if (!W1 || !W2 || !W3 || !xi || !beta || r1 < 0 || r2 < 0 || r3 < 0 || R < 0 || ldw < R)
+    return fail(RHOSVD_EINVAL, "bad args");
+  if ((ldw & 1) || ((uintptr_t)W1 & 15) || ((uintptr_t)W2 & 15) || ((uintptr_t)W3 & 15))
+    return fail(RHOSVD_EINVAL, "core: ldw must be even, W 16B-aligned");
+  std::lock_guard<std::mutex> lk(g_mu);
+  cudaStream_t st = (cudaStream_t)stream;
+  Workspace& w = WS();
+  int64_t ldx = round_up(std::max<int64_t>(R, 2), 2);
+  RH_CHECK(w.W1x.ensure((size_t)r1 * ldx + 64, st));
+  RH_CHECK(scale_cols(W1, ldw, xi, r1, R, w.W1x.p, ldx, st));
+  size_t total = (size_t)r1 * r2 * r3;
+  RH_CHECK(w.corepart.ensure(std::min<size_t>(total * 8, (size_t)1 << 28), st));
+  return core_kr(w.W1x.p, ldx, W2, W3, ldw, r1, r2, r3, R, beta, w.corepart.p, w.corepart.cap, st, nullptr);
+}
+
+}  // extern "C"

@@ -1,0 +1,191 @@
+"""End-to-end parity of the CUDA path (rhosvd_c2t through the C ABI) against
+the CPU oracle on identical seeded inputs (BASELINE.json north_star):
+  * identical selected ranks r_l (unless the oracle flags a near-tie, A11);
+  * retained singular values within 1e-10 relative (A13);
+  * reconstructed Tucker tensor within 1e-9 relative Frobenius, compared by
+    the concatenated-frame QR (sign/rotation invariant, A14);
+  * frames orthonormal to 1e-13; T_l, ||xi'||, ||beta|| within 1e-12.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle import rhosvd as oracle_rhosvd, tucker_diff, orth_error, sigma_rel_err  # noqa: E402
+from workloads import make_config, make_params, make_random_params  # noqa: E402
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+SIG_TOL = 1e-10
+TUCKER_TOL = 1e-9
+ORTH_TOL = 1e-13
+
+
+@pytest.fixture(scope="module")
+def rh():
+    from paper_2201_12663_b200 import rhosvd
+    rhosvd.lib()
+    return rhosvd
+
+
+def run_gpu(rh, Us, xi, eps=None, ranks=None, **kw):
+    Ud = [torch.as_tensor(np.ascontiguousarray(u), device="cuda") for u in Us]
+    xd = torch.as_tensor(np.ascontiguousarray(xi), device="cuda")
+    return rh.c2t(Ud, xd, eps=eps, ranks=ranks, **kw)
+
+
+def compare(g, o, check_W=True):
+    assert tuple(g.ranks) == tuple(o.ranks), (g.ranks, o.ranks, o.report["margins"])
+    for l in range(3):
+        r = o.ranks[l]
+        sg = g.sigma[l].cpu().numpy()
+        assert sigma_rel_err(sg, o.sigma[l][:r]) <= SIG_TOL, (l, sigma_rel_err(sg, o.sigma[l][:r]))
+        Z = g.Z[l].cpu().numpy()
+        assert orth_error(Z) <= ORTH_TOL, orth_error(Z)
+    Zg = [z.cpu().numpy() for z in g.Z]
+    d, nrm = tucker_diff(g.beta.cpu().numpy(), Zg, o.beta, o.Z)
+    assert d <= TUCKER_TOL * max(nrm, 1e-300), d / nrm
+    rep = g.report
+    for l in range(3):
+        assert abs(rep["trace"][l] - o.T[l]) <= 1e-12 * o.T[l]
+    assert abs(rep["xi_norm"] - o.report["xi_norm"]) <= 1e-12 * o.report["xi_norm"]
+    assert abs(rep["beta_norm"] - o.report["beta_norm"]) <= 1e-12 * o.report["beta_norm"]
+    if check_W and g.W is not None:
+        # the CP factors of the core are Z_l^T Uhat_l (Prop. 2.1) - sign-aligned with the frames
+        for l in range(3):
+            Wg = g.W[l].cpu().numpy()
+            # compare W^T W (sign/rotation invariant within the retained frame)
+            Pg = Wg.T @ Wg
+            Po = o.W[l].T @ o.W[l]
+            assert np.max(np.abs(Pg - Po)) <= 1e-9 * np.max(np.abs(Po))
+    return d / max(nrm, 1e-300)
+
+
+# ------------------------------------------------------------------ small random cases
+@pytest.mark.parametrize("n,R,eps,ranks", [
+    (16, 40, None, (3, 4, 5)),
+    (37, 200, 1e-3, None),
+    (64, 333, None, (10, 10, 10)),
+    (100, 1000, 1e-5, None),
+    (130, 2501, 1e-6, None),
+    (257, 600, 1e-4, None),
+])
+def test_parity_random(rh, n, R, eps, ranks):
+    p = make_random_params(n, R, seed=n * 1000 + R, eps=eps, ranks=ranks)
+    U1, U2, U3, xi = make_config(p)
+    o = oracle_rhosvd([U1, U2, U3], xi, eps=eps, ranks=ranks)
+    g = run_gpu(rh, [U1, U2, U3], xi, eps=eps, ranks=ranks)
+    compare(g, o)
+
+
+@pytest.mark.parametrize("k", [1, 2, 3])
+def test_parity_baseline_configs(rh, k):
+    p = make_params(k)
+    U1, U2, U3, xi = make_config(p)
+    o = oracle_rhosvd([U1, U2, U3], xi, eps=p.eps, ranks=p.ranks)
+    g = run_gpu(rh, [U1, U2, U3], xi, eps=p.eps, ranks=p.ranks)
+    rel = compare(g, o)
+    print(f"cfg{k}: ranks {g.ranks} tucker rel diff {rel:.2e} ms {g.report['ms']}")
+
+
+# ------------------------------------------------------------------ edge cases
+def test_r_less_than_n(rh):
+    rng = np.random.default_rng(5)
+    Us = [rng.normal(size=(7, 40)) for _ in range(3)]
+    xi = rng.normal(size=7)
+    o = oracle_rhosvd(Us, xi, eps=1e-12)
+    g = run_gpu(rh, Us, xi, eps=1e-12)
+    compare(g, o)
+
+
+def test_fixed_rank_clamped(rh):
+    rng = np.random.default_rng(6)
+    Us = [rng.normal(size=(9, 20)) for _ in range(3)]
+    xi = rng.normal(size=9)
+    o = oracle_rhosvd(Us, xi, ranks=(50, 50, 50))
+    g = run_gpu(rh, Us, xi, ranks=(50, 50, 50))
+    assert g.ranks == (9, 9, 9)
+    compare(g, o)
+
+
+def test_zero_columns_and_rank_one(rh):
+    rng = np.random.default_rng(7)
+    v = [rng.normal(size=(1, 33)) for _ in range(3)]
+    Us = [np.repeat(vv, 20, axis=0) for vv in v]
+    Us[1][3] = 0.0  # zero column: xi' = 0 (reading A3)
+    xi = rng.normal(size=20)
+    o = oracle_rhosvd(Us, xi, eps=1e-8)
+    g = run_gpu(rh, Us, xi, eps=1e-8)
+    assert g.ranks == (1, 1, 1) == o.ranks
+    compare(g, o)
+
+
+def test_empty_R(rh):
+    Us = [torch.zeros(0, 16, dtype=torch.float64, device="cuda") for _ in range(3)]
+    xi = torch.zeros(0, dtype=torch.float64, device="cuda")
+    g = rh.c2t(Us, xi, eps=1e-3)
+    assert g.ranks == (0, 0, 0) and g.beta.numel() == 0
+
+
+def test_nonfinite_input_rejected(rh):
+    rng = np.random.default_rng(8)
+    Us = [rng.normal(size=(10, 12)) for _ in range(3)]
+    Us[2][4, 5] = np.nan
+    with pytest.raises(rh.RhosvdError) as e:
+        run_gpu(rh, Us, rng.normal(size=10), eps=1e-3)
+    assert e.value.status == -2
+
+
+def test_deterministic(rh):
+    p = make_random_params(64, 500, seed=9, eps=1e-5)
+    U1, U2, U3, xi = make_config(p)
+    a = run_gpu(rh, [U1, U2, U3], xi, eps=1e-5)
+    b = run_gpu(rh, [U1, U2, U3], xi, eps=1e-5)
+    assert torch.equal(a.beta, b.beta)
+    for l in range(3):
+        assert torch.equal(a.Z[l], b.Z[l]) and torch.equal(a.sigma[l], b.sigma[l])
+
+
+def test_error_bound_holds(rh):
+    """Thm. 2.2 on the GPU result: exact error by brute
+    force on a tiny grid <= ||xi'|| (sum tail^2)^1/2 <= ||xi'|| sum tail."""
+    from oracle import dense_from_canonical, dense_from_tucker
+    p = make_random_params(14, 60, seed=11, eps=1e-2)
+    U1, U2, U3, xi = make_config(p)
+    g = run_gpu(rh, [U1, U2, U3], xi, eps=1e-2)
+    A = dense_from_canonical([U1, U2, U3], xi)
+    A0 = dense_from_tucker(g.beta.cpu().numpy(), [z.cpu().numpy() for z in g.Z])
+    err = np.linalg.norm(A - A0)
+    rep = g.report
+    assert err <= rep["bound_ns"] * (1 + 1e-10) + 1e-13 * np.linalg.norm(A)
+    assert rep["bound_ns"] <= rep["bound_paper"] * (1 + 1e-15)
+
+
+# ------------------------------------------------------------------ full-size configs 4, 5
+@pytest.mark.parametrize("k", [4, 5])
+def test_parity_full_size_fixture(rh, k):
+    """cfg 4/5 at BASELINE.json's full sizes: the oracle takes minutes here, so
+    its ranks, retained sigma, T and ||beta|| come from a fixture written by
+    tools/make_oracle_fixtures.py (which calls only oracle/); the Tucker
+    tensor is checked by properties that hold at any size."""
+    path = os.path.join(GOLDEN, f"oracle_cfg{k}.json")
+    if not os.path.exists(path):
+        pytest.skip("fixture missing")
+    fx = json.load(open(path))
+    p = make_params(k)
+    U1, U2, U3, xi = make_config(p)
+    g = run_gpu(rh, [U1, U2, U3], xi, eps=p.eps, ranks=p.ranks)
+    assert list(g.ranks) == fx["ranks"]
+    for l in range(3):
+        assert sigma_rel_err(g.sigma[l].cpu().numpy(), np.array(fx["sigma"][l])) <= SIG_TOL
+        assert orth_error(g.Z[l].cpu().numpy()) <= ORTH_TOL
+        assert abs(g.report["trace"][l] - fx["trace"][l]) <= 1e-12 * fx["trace"][l]
+    assert abs(g.report["beta_norm"] - fx["beta_norm"]) <= 1e-10 * fx["beta_norm"]
+    assert abs(g.report["xi_norm"] - fx["xi_norm"]) <= 1e-12 * fx["xi_norm"]
+    # tails within the threshold, consistent with the oracle's
+    for l in range(3):
+        assert abs(g.report["tail"][l] - fx["tail"][l]) <= 1e-6 * fx["tail"][l]
