@@ -7,6 +7,7 @@ int k_normalize(const double* U, int64_t ldu, int64_t n, int64_t R, int64_t Rp, 
                 double* s, double* tcol, int* flag, cudaStream_t st);
 int k_xiprime(const double* xi, const double* s1, const double* s2, const double* s3, int64_t R, int64_t Rp,
               double* xip, double* xip2, int* flag, cudaStream_t st);
+int k_coldot(const double* Z, const double* Y, int64_t ld, int64_t n, int64_t b, double* d, cudaStream_t st);
 int k_fixed_sum(const double* x, int64_t n, double* out, cudaStream_t st);
 int k_sumsq(const double* x, int64_t n, double* part, double* out, cudaStream_t st);
 int k_random(double* M, int64_t ldm, int64_t n, int64_t c0, int64_t c1, uint64_t seed, cudaStream_t st);

@@ -234,6 +234,19 @@ __global__ void apply_sign_kernel(double* Z, int64_t ldz, int n, int r, double* 
   }
 }
 
+// d_j = sum_i Z(i,j) Y(i,j)  (diagonal of Z^T Y; one warp per column, fixed order)
+__global__ void coldot_kernel(const double* Z, const double* Y, int64_t ld, int n, int b, double* d) {
+  const int lane = threadIdx.x & 31;
+  const int j = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (j >= b) return;
+  const double* z = Z + (int64_t)j * ld;
+  const double* y = Y + (int64_t)j * ld;
+  double s = 0.0;
+  for (int i = lane; i < n; i += 32) s = fma(z[i], y[i], s);
+  s = warp_sum(s);
+  if (lane == 0) d[j] = s;
+}
+
 // ---------------------------------------------------------------- host wrappers
 #define LAUNCH_OK() \
   do {              \
@@ -254,6 +267,12 @@ int k_xiprime(const double* xi, const double* s1, const double* s2, const double
               double* xip, double* xip2, int* flag, cudaStream_t st) {
   if (Rp <= 0) return RHOSVD_OK;
   xiprime_kernel<<<(unsigned)cdiv(Rp, 256), 256, 0, st>>>(xi, s1, s2, s3, (int)R, (int)Rp, xip, xip2, flag);
+  LAUNCH_OK();
+  return RHOSVD_OK;
+}
+int k_coldot(const double* Z, const double* Y, int64_t ld, int64_t n, int64_t b, double* d, cudaStream_t st) {
+  if (b <= 0) return RHOSVD_OK;
+  coldot_kernel<<<(unsigned)cdiv(b, 8), 256, 0, st>>>(Z, Y, ld, (int)n, (int)b, d);
   LAUNCH_OK();
   return RHOSVD_OK;
 }

@@ -16,6 +16,8 @@
 //   S7 report          tails, ||xi'||, Thm. 2.2 bound and its orthogonal form, ||beta||
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <string>
@@ -148,12 +150,48 @@ static int allreduce(Ctx& c, double* p, int64_t count) {
   return r;
 }
 
+// RHOSVD_DEBUG=1: synchronise and scan a device array for non-finite values (debug only)
+static bool dbg_on() {
+  static int on = -1;
+  if (on < 0) {
+    const char* e = getenv("RHOSVD_DEBUG");
+    on = (e && e[0] == '1') ? 1 : 0;
+  }
+  return on == 1;
+}
+static void dbg_check(cudaStream_t st, const char* tag, const double* p, int64_t rows, int64_t cols, int64_t ld) {
+  if (!dbg_on() || !p) return;
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    fprintf(stderr, "[rhosvd dbg] %s: CUDA error %s\n", tag, cudaGetErrorString(e));
+    return;
+  }
+  std::vector<double> h((size_t)ld * cols);
+  cudaMemcpy(h.data(), p, h.size() * sizeof(double), cudaMemcpyDeviceToHost);
+  int64_t bad = 0, first = -1;
+  double mx = 0.0;
+  for (int64_t j = 0; j < cols; ++j)
+    for (int64_t i = 0; i < rows; ++i) {
+      double v = h[(size_t)j * ld + i];
+      if (!std::isfinite(v)) {
+        if (first < 0) first = j * rows + i;
+        ++bad;
+      } else {
+        mx = std::max(mx, std::fabs(v));
+      }
+    }
+  fprintf(stderr, "[rhosvd dbg] %-28s %lldx%lld nonfinite=%lld first=%lld maxabs=%.3e\n", tag, (long long)rows,
+          (long long)cols, (long long)bad, (long long)first, mx);
+}
+
 // CholeskyQR pass: dst = src * D L^{-T}, L = chol(D src^T src D + shift I)
 static int cholqr_pass(Ctx& c, int64_t n, int64_t b, int64_t ldn, const double* src, double* dst, double shift,
                        int64_t ldb_small) {
   Workspace& w = c.w;
   RH_CHECK(mm(c, b, b, n, src, ldn, true, src, ldn, true, w.S.p, ldb_small, nullptr, true));
+  dbg_check(c.st, "chol S", w.S.p, b, b, ldb_small);
   RH_CHECK(chol_inv_scaled(b, w.S.p, ldb_small, shift, w.Bp.p, ldb_small, w.dws, c.st));
+  dbg_check(c.st, "chol Bp", w.Bp.p, b, b, ldb_small);
   RH_CHECK(mm(c, n, b, b, src, ldn, false, w.Bp.p, ldb_small, true, dst, ldn));
   return RHOSVD_OK;
 }
@@ -163,7 +201,9 @@ static int orth(Ctx& c, int64_t n, int64_t b, int64_t ldn, const double* in, dou
                 int64_t ldb_small, bool shifted) {
   const double u = 1.1102230246251565e-16;
   if (shifted) {
-    double shift = 11.0 * ((double)n * b + (double)b * (b + 1)) * u;
+    // shifted CholeskyQR (Fukaya et al.): s = 11 (n b + b(b+1)) u ||X||_2^2, ||X||_2^2 <= b
+    // for the column-scaled X
+    double shift = 11.0 * ((double)n * b + (double)b * (b + 1)) * u * (double)b;
     RH_CHECK(cholqr_pass(c, n, b, ldn, in, tmp, shift, ldb_small));
     RH_CHECK(cholqr_pass(c, n, b, ldn, tmp, out, 0.0, ldb_small));
     RH_CHECK(cholqr_pass(c, n, b, ldn, out, tmp, 0.0, ldb_small));
@@ -222,25 +262,95 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
   RH_CHECK(k_random(w.M.p, LDN, n, 0, b, seed, st));
   RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldbs(b), true));
 
-  std::vector<double> th_h, th_old;
-  double dth_old = -1.0;
-  int it_total = 0, it_b = 0, guard = 0;
+  // ---------------- phase 1: orthogonal (subspace) iteration Z <- CholQR(G Z) with
+  // block growth; no eigensolver.  The span of Z converges to the dominant
+  // subspace (rate lambda_{b+1}/lambda_k) and CholQR keeps leading spans, so the
+  // diagonal of Z^T G Z (cheap column dots) gives a running tail estimate
+  // T - sum_j (Z^T G Z)_jj for the block-size decision (eps mode).
+  std::vector<double> th_h, th_old, d_h;
+  const double thr = epsmode ? o.eps * o.eps * T : 0.0;
+  auto predict_r = [&](const std::vector<double>& d, int64_t bb) -> int64_t {
+    double acc = 0.0;
+    std::vector<double> tc(bb);
+    for (int64_t k = 0; k < bb; ++k) {
+      acc += d[k];
+      tc[k] = T - acc;
+      if (tc[k] <= thr) return k + 1;
+    }
+    // not reached inside the block: extrapolate log10(tail) linearly over the last half
+    int64_t j0 = bb / 2;
+    double sx = 0, sy = 0, sxx = 0, sxy = 0;
+    int64_t cnt = 0;
+    for (int64_t k = j0; k < bb; ++k) {
+      double y = std::log10(std::max(tc[k], 1e-300));
+      double x = (double)(k + 1);
+      sx += x; sy += y; sxx += x * x; sxy += x * y;
+      ++cnt;
+    }
+    double den = cnt * sxx - sx * sx;
+    if (cnt < 2 || den <= 0) return 2 * bb;
+    double slope = (cnt * sxy - sx * sy) / den, icpt = (sy - slope * sx) / cnt;
+    if (!(slope < 0)) return 2 * bb;
+    double rr = (std::log10(thr) - icpt) / slope;
+    if (!(rr < 1e9)) return 2 * bb;
+    return (int64_t)std::ceil(rr);
+  };
+  int it_total = 0, itb = 0, guard = 0;
   while (true) {
     ++it_total;
-    ++it_b;
+    ++itb;
+    RH_CHECK(mm(c, n, b, n, G, LDN, false, w.Z.p, LDN, true, w.Y.p, LDN));
+    dbg_check(st, "p1 Y=GZ", w.Y.p, n, b, LDN);
+    if (epsmode) RH_CHECK(k_coldot(w.Z.p, w.Y.p, LDN, n, b, w.th.p, st));
+    RH_CHECK(orth(c, n, b, LDN, w.Y.p, w.Z.p, w.T1.p, ldbs(b), true));
+    dbg_check(st, "p1 Z=orth(Y)", w.Z.p, n, b, LDN);
+    if (b >= m) break;  // full space: nothing to iterate
+    if (itb < 2) continue;
+    if (!epsmode) break;
+    d_h.resize(b);
+    RH_CUDA(cudaMemcpyAsync(d_h.data(), w.th.p, b * sizeof(double), cudaMemcpyDeviceToHost, st));
+    RH_CUDA(cudaStreamSynchronize(st));
+    int64_t r_est = predict_r(d_h, b);
+    if (r_est + p > b && guard < 12) {
+      int64_t bn = std::min<int64_t>(m, std::min<int64_t>(2 * b, std::max<int64_t>((int64_t)(1.15 * r_est) + p, b + p)));
+      RH_CHECK(ensure_b(bn));
+      RH_CUDA(cudaMemcpyAsync(w.M.p, w.Z.p, (size_t)LDN * b * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      RH_CHECK(k_random(w.M.p, LDN, n, b, bn, seed + 7919ull * (uint64_t)(it_total + 1), st));
+      b = bn;
+      RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldbs(b), true));
+      itb = 0;
+      ++mo.grows;
+      ++guard;
+      continue;
+    }
+    break;
+  }
+  // ---------------- phase 2: Rayleigh-Ritz aligned iterations
+  //   Y = G Z, H = Z^T Y = V Theta V^T (Jacobi), Z <- CholQR(Y V Theta^-1)
+  // (Y V Theta^-1 = Z V + residual Theta^-1 with the residual orthogonal to Z, so
+  // its Gram is >= I: well conditioned).  The block is truncated to
+  // b' >= r + p chosen so that theta_b'/theta_r <= 0.05 (fast convergence).
+  double dth_old = -1.0;
+  int it2 = 0;
+  while (true) {
+    ++it_total;
+    ++it2;
     const int64_t ldb = ldbs(b);
-    // Y = G Z ; H = Z^T Y ; eig(H) = V Theta V^T
     RH_CHECK(mm(c, n, b, n, G, LDN, false, w.Z.p, LDN, true, w.Y.p, LDN));
     RH_CHECK(mm(c, b, b, n, w.Z.p, LDN, true, w.Y.p, LDN, true, w.H.p, ldb, nullptr, true));
     int sw = 0;
+    dbg_check(st, "p2 H", w.H.p, b, b, ldb);
     RH_CHECK(syevj(b, w.H.p, ldb, w.th.p, w.V.p, ldb, 1e-14, 1e-16, 60, w.dws, st, &sw));
+    dbg_check(st, "p2 theta", w.th.p, b, 1, b);
+    dbg_check(st, "p2 V", w.V.p, b, b, ldb);
+    if (dbg_on()) fprintf(stderr, "[rhosvd dbg] mode %d b %lld sweeps %d\n", mode, (long long)b, sw);
     th_h.resize(b);
     RH_CUDA(cudaMemcpyAsync(th_h.data(), w.th.p, b * sizeof(double), cudaMemcpyDeviceToHost, st));
     RH_CUDA(cudaStreamSynchronize(st));
-    // rank estimate from (squared) Ritz values - growth decisions only
-    int64_t r_est = -1;
+    int64_t r_est = rfix;
     if (epsmode) {
-      double thr = o.eps * o.eps * T, acc = 0.0;
+      double acc = 0.0;
+      r_est = -1;
       for (int64_t k = 0; k < b; ++k) {
         acc += th_h[k];
         if (T - acc <= thr) {
@@ -248,43 +358,44 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
           break;
         }
       }
-    } else {
-      r_est = rfix;
     }
-    double dth = -1.0;
-    if (!th_old.empty() && (int64_t)th_old.size() == b && r_est > 0) {
-      dth = 0.0;
-      for (int64_t k = 0; k < r_est; ++k) dth = std::max(dth, std::fabs(th_h[k] - th_old[k]) / std::fabs(th_h[k]));
-    }
-    // M = Y V Theta^-1 (Ritz-aligned, well conditioned: Gram >= I)
     RH_CHECK(k_ritz_floor(w.th.p, b, tau, w.inv.p, st));
     RH_CHECK(mm(c, n, b, b, w.Y.p, LDN, false, w.V.p, ldb, true, w.M.p, LDN, w.inv.p));
-    if (epsmode && b < m && (r_est < 0 || r_est + p > b) && guard < 16) {
-      int64_t bn = std::min<int64_t>(m, r_est < 0 ? 2 * b : r_est + p);
+    if (epsmode && b < m && (r_est < 0 || r_est + p > b) && guard < 12) {
+      int64_t bn = std::min<int64_t>(m, r_est < 0 ? 2 * b : r_est + 2 * p);
       RH_CHECK(ensure_b(bn));
       RH_CHECK(k_random(w.M.p, LDN, n, b, bn, seed + 7919ull * (uint64_t)(it_total + 1), st));
       b = bn;
       RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldbs(b), true));
       th_old.clear();
       dth_old = -1.0;
-      it_b = 0;
       ++mo.grows;
       ++guard;
       continue;
     }
-    if (epsmode && r_est > 0 && b > r_est + p && guard < 16) {
-      b = r_est + p;  // keep the leading Ritz directions (CholQR preserves leading spans)
-      RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldbs(b), true));
-      th_old.clear();
-      dth_old = -1.0;
-      it_b = 0;
-      ++guard;
-      continue;
+    // block truncation: smallest b' in [r+p, b] with theta_{b'} <= 0.05 theta_r
+    int64_t bt = b;
+    if (r_est > 0 && r_est + p < b) {
+      const double tr = th_h[r_est - 1];
+      bt = b;
+      for (int64_t j = r_est + p; j <= b; ++j)
+        if (th_h[j - 1] <= 0.05 * tr) {
+          bt = j;
+          break;
+        }
     }
-    RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldb, true));
+    double dth = -1.0;
+    if (r_est > 0 && (int64_t)th_old.size() >= r_est) {
+      dth = 0.0;
+      for (int64_t k = 0; k < r_est; ++k) dth = std::max(dth, std::fabs(th_h[k] - th_old[k]) / std::fabs(th_h[k]));
+    }
+    b = bt;
+    dbg_check(st, "p2 M", w.M.p, n, b, LDN);
+    RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldbs(b), true));
+    dbg_check(st, "p2 Z", w.Z.p, n, b, LDN);
     bool conv = dth >= 0.0 && (dth < 1e-10 || (dth_old >= 0.0 && dth > 0.25 * dth_old));
-    if (b >= m && it_b >= 1) conv = true;  // full space: the subspace is exact
-    if (conv || it_b >= std::max(2, o.max_iters)) break;
+    if (b >= m) conv = true;  // full space: the subspace is exact
+    if (conv || it2 >= std::max(2, o.max_iters)) break;
     th_old = th_h;
     dth_old = dth;
   }
@@ -301,7 +412,10 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     RH_CHECK(allreduce(c, w.S.p, ldb * b));
     c.tm->mark(PH_RR);
     int sw = 0;
+    dbg_check(st, "rr S", w.S.p, b, b, ldb);
     RH_CHECK(syevj(b, w.S.p, ldb, lam, P, ldb, 1e-15, 1e-300, 80, w.dws, st, &sw));
+    dbg_check(st, "rr lambda", lam, b, 1, b);
+    if (dbg_on()) fprintf(stderr, "[rhosvd dbg] mode %d rr b %lld sweeps %d\n", mode, (long long)b, sw);
     if (sw < 0) return fail(RHOSVD_ENOCONV, "Jacobi on W W^T did not converge");
     return RHOSVD_OK;
   };
@@ -398,13 +512,16 @@ void rhosvd_opts_default(rhosvd_opts* o) {
 
 void rhosvd_result_free(rhosvd_result* r) {
   if (!r) return;
+  // memory came from the stream-ordered pool: return it there (the pool keeps
+  // it for the next call instead of unmapping; cudaFree would release it)
   cudaDeviceSynchronize();
   for (int l = 0; l < 3; ++l) {
-    if (r->Z[l]) cudaFree(r->Z[l]);
-    if (r->sigma[l]) cudaFree(r->sigma[l]);
-    if (r->W[l]) cudaFree(r->W[l]);
+    if (r->Z[l]) cudaFreeAsync(r->Z[l], 0);
+    if (r->sigma[l]) cudaFreeAsync(r->sigma[l], 0);
+    if (r->W[l]) cudaFreeAsync(r->W[l], 0);
   }
-  if (r->beta) cudaFree(r->beta);
+  if (r->beta) cudaFreeAsync(r->beta, 0);
+  cudaStreamSynchronize(0);
   delete r;
 }
 
@@ -543,9 +660,9 @@ static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n
     int st_ = solve_mode(c, l, n, LDN, Rl, Rp, Rg, Uh[l], w.G.p + (size_t)l * LDN * LDN, rep.trace[l], o, mo[l]);
     if (st_ != RHOSVD_OK) {
       for (int q = 0; q <= l; ++q) {
-        if (mo[q].Z) cudaFree(mo[q].Z);
-        if (mo[q].W) cudaFree(mo[q].W);
-        if (mo[q].sigma) cudaFree(mo[q].sigma);
+        if (mo[q].Z) cudaFreeAsync(mo[q].Z, st);
+        if (mo[q].W) cudaFreeAsync(mo[q].W, st);
+        if (mo[q].sigma) cudaFreeAsync(mo[q].sigma, st);
       }
       return st_;
     }

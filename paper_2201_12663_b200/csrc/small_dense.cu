@@ -233,6 +233,143 @@ __global__ void __launch_bounds__(512) jacobi_kernel(JacParams p) {
   }
 }
 
+// Single-CTA variant for b <= 160: A lives in shared memory and is updated in
+// place (each 2x2 block (P,Q), P <= Q, is read and written by one thread, its
+// mirror (Q,P) by the same thread), so a step costs two __syncthreads.
+constexpr int JAC_SMEM_MAXB = 160;
+__global__ void __launch_bounds__(1024) jacobi_smem_kernel(JacParams p) {
+  extern __shared__ double sh[];
+  const int h = p.h, b = p.b, m = p.m;
+  const int lds = b | 1;  // odd pitch
+  double* A = sh;
+  double* c_ = A + (size_t)b * lds;
+  double* s_ = c_ + h;
+  double* t_ = s_ + h;
+  int* act_ = reinterpret_cast<int*>(t_ + h);
+  int* pp_ = act_ + h;
+  int* qq_ = pp_ + h;
+  __shared__ int red[32];
+  __shared__ double sdmax[32];
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int64_t ld = p.ld;
+  for (int e = tid; e < b * b; e += nth) {
+    int i = e % b, j = e / b;
+    A[j * lds + i] = p.Ain[(int64_t)j * p.lda + i];
+    p.V[j * ld + i] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  {
+    double dm = 0.0;
+    for (int i = tid; i < b; i += nth) dm = fmax(dm, fabs(A[i * lds + i]));
+    for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+    if ((tid & 31) == 0) sdmax[tid >> 5] = dm;
+    __syncthreads();
+    dm = 0.0;
+    for (int w = 0; w < (nth >> 5); ++w) dm = fmax(dm, sdmax[w]);
+    __syncthreads();
+    if (tid == 0) sdmax[0] = dm;
+    __syncthreads();
+  }
+  const double abstol = p.abstol * sdmax[0];
+  const int nblk = h * (h + 1) / 2;
+  const int items = nblk + b * h;
+  int sweeps = 0;
+  bool converged = false;
+  for (int sw = 0; sw < p.max_sweeps; ++sw) {
+    int mycount = 0;
+    for (int step = 0; step < m - 1; ++step) {
+      for (int k = tid; k < h; k += nth) {
+        int i1 = rr_index(k, step, m), i2 = rr_index(m - 1 - k, step, m);
+        int pq = min(i1, i2), qq = max(i1, i2);
+        pp_[k] = pq;
+        qq_[k] = qq;
+        double c = 1.0, s = 0.0, t = 0.0;
+        int act = 0;
+        if (qq < b) {
+          double app = A[pq * lds + pq], aqq = A[qq * lds + qq], apq = A[qq * lds + pq];
+          double thr = fmax(abstol, p.tol * sqrt(fabs(app * aqq)));
+          if (fabs(apq) > thr) {
+            act = 1;
+            double theta = (aqq - app) / (2.0 * apq);
+            if (fabs(theta) > 1e150)
+              t = 0.5 / theta;
+            else
+              t = copysign(1.0 / (fabs(theta) + sqrt(1.0 + theta * theta)), theta);
+            if (theta == 0.0) t = 1.0;
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+          }
+        }
+        c_[k] = c; s_[k] = s; t_[k] = t; act_[k] = act;
+        mycount += act;
+      }
+      __syncthreads();
+      for (int it = tid; it < items; it += nth) {
+        if (it < nblk) {
+          int Q = (int)((sqrtf(8.0f * (float)it + 1.0f) - 1.0f) * 0.5f);
+          while ((Q + 1) * (Q + 2) / 2 <= it) ++Q;
+          while (Q * (Q + 1) / 2 > it) --Q;
+          int P = it - Q * (Q + 1) / 2;
+          int p1 = pp_[P], q1 = qq_[P];
+          if (!act_[P] && !act_[Q]) continue;  // identity rotation on both sides
+          if (P == Q) {
+            double app = A[p1 * lds + p1], aqq = A[q1 * lds + q1], apq = A[q1 * lds + p1];
+            double t = t_[P];
+            A[p1 * lds + p1] = app - t * apq;
+            A[q1 * lds + q1] = aqq + t * apq;
+            A[q1 * lds + p1] = 0.0;
+            A[p1 * lds + q1] = 0.0;
+          } else {
+            int p2 = pp_[Q], q2 = qq_[Q];
+            bool vq1 = q1 < b, vq2 = q2 < b;
+            double a11 = A[p2 * lds + p1];
+            double a12 = vq2 ? A[q2 * lds + p1] : 0.0;
+            double a21 = vq1 ? A[p2 * lds + q1] : 0.0;
+            double a22 = (vq1 && vq2) ? A[q2 * lds + q1] : 0.0;
+            double c1 = c_[P], s1 = s_[P], c2 = c_[Q], s2 = s_[Q];
+            double b11 = c2 * a11 - s2 * a12, b12 = s2 * a11 + c2 * a12;
+            double b21 = c2 * a21 - s2 * a22, b22 = s2 * a21 + c2 * a22;
+            double n11 = c1 * b11 - s1 * b21, n21 = s1 * b11 + c1 * b21;
+            double n12 = c1 * b12 - s1 * b22, n22 = s1 * b12 + c1 * b22;
+            A[p2 * lds + p1] = n11; A[p1 * lds + p2] = n11;
+            if (vq2) { A[q2 * lds + p1] = n12; A[p1 * lds + q2] = n12; }
+            if (vq1) { A[p2 * lds + q1] = n21; A[q1 * lds + p2] = n21; }
+            if (vq1 && vq2) { A[q2 * lds + q1] = n22; A[q1 * lds + q2] = n22; }
+          }
+        } else {
+          int j = it - nblk;
+          int i = j % b, P = j / b;
+          if (act_[P]) {
+            int pc = pp_[P], qc = qq_[P];
+            double vp = p.V[pc * ld + i], vq = p.V[qc * ld + i];
+            double c = c_[P], s = s_[P];
+            p.V[pc * ld + i] = c * vp - s * vq;
+            p.V[qc * ld + i] = s * vp + c * vq;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    ++sweeps;
+    int v = mycount;
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    if ((tid & 31) == 0) red[tid >> 5] = v;
+    __syncthreads();
+    int tot = 0;
+    for (int w = 0; w < (nth >> 5); ++w) tot += red[w];
+    __syncthreads();
+    if (tot == 0) {
+      converged = true;
+      break;
+    }
+  }
+  for (int i = tid; i < b; i += nth) p.lam[i] = A[i * lds + i];
+  if (tid == 0) {
+    p.info[0] = sweeps;
+    p.info[2] = converged ? 0 : 1;
+  }
+}
+
 // sort eigenpairs descending (ties: lower index first); one CTA computes ranks
 __global__ void rank_sort_kernel(int b, const double* lam_u, double* lam, int* perm) {
   for (int i = threadIdx.x; i < b; i += blockDim.x) {
@@ -308,20 +445,32 @@ int syevj(int64_t b, const double* A, int64_t lda, double* lambda, double* Vout,
   jp.Ain = A; jp.lda = lda; jp.A0 = ws.A0; jp.A1 = ws.A1; jp.ld = ws.ld; jp.V = ws.V;
   jp.lam = ws.cs;  // unsorted eigenvalues staged in cs
   jp.tol = tol; jp.abstol = abstol; jp.max_sweeps = max_sweeps; jp.bar = ws.bar; jp.info = ws.info;
-  const int threads = 512;
-  size_t smem = (size_t)jp.h * (3 * sizeof(double) + 3 * sizeof(int)) + 64;
-  static bool attr = false;
-  if (!attr) {
-    RH_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-    attr = true;
+  if (b <= JAC_SMEM_MAXB) {
+    const int threads = 1024;
+    size_t smem = (size_t)b * (b | 1) * sizeof(double) + (size_t)jp.h * (3 * sizeof(double) + 3 * sizeof(int)) + 64;
+    static bool attr_s = false;
+    if (!attr_s) {
+      RH_CUDA(cudaFuncSetAttribute(jacobi_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
+      attr_s = true;
+    }
+    jacobi_smem_kernel<<<1, threads, smem, st>>>(jp);
+    count_launch();
+    RH_LAUNCH_CHECK();
+  } else {
+    const int threads = 512;
+    size_t smem = (size_t)jp.h * (3 * sizeof(double) + 3 * sizeof(int)) + 64;
+    static bool attr = false;
+    if (!attr) {
+      RH_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
+      attr = true;
+    }
+    int64_t items = (int64_t)jp.h * (jp.h + 1) / 2 + (int64_t)b * jp.h;
+    int64_t want = cdiv(items, threads * 4);
+    int grid = coop_grid((const void*)jacobi_kernel, threads, smem, want);
+    void* args[] = {&jp};
+    RH_CUDA(cudaLaunchCooperativeKernel((const void*)jacobi_kernel, dim3(grid), dim3(threads), args, smem, st));
+    count_launch();
   }
-  int64_t items = (int64_t)jp.h * (jp.h + 1) / 2 + (int64_t)b * jp.h;
-  int64_t want = cdiv(items, threads * 4);
-  if (b <= 96) want = 1;
-  int grid = coop_grid((const void*)jacobi_kernel, threads, smem, want);
-  void* args[] = {&jp};
-  RH_CUDA(cudaLaunchCooperativeKernel((const void*)jacobi_kernel, dim3(grid), dim3(threads), args, smem, st));
-  count_launch();
   rank_sort_kernel<<<1, 1024, 0, st>>>((int)b, ws.cs, lambda, ws.perm);
   permute_cols_kernel<<<(unsigned)cdiv(b * b, 256), 256, 0, st>>>((int)b, ws.V, ws.ld, ws.perm, Vout, ldv);
   count_launch(2);
@@ -342,6 +491,7 @@ struct CholParams {
   const double* S;
   int64_t lds;
   double shift;
+  double delta;  // pivot floor (relative to the unit scaled diagonal)
   double* A;  // work copy, ld
   double* Lt; // L^T (upper), ld
   double* d;  // column scaling D
@@ -354,9 +504,9 @@ constexpr int CW = 32;  // panel width
 
 __global__ void __launch_bounds__(256) chol_kernel(CholParams p) {
   __shared__ double Ljj[CW][CW + 1];
-  __shared__ double Inv[CW][CW + 1];
   __shared__ double Xi[CW][CW + 1];
   __shared__ double Xk[CW][CW + 1];
+  __shared__ unsigned depmask;
   const int b = p.b;
   const int64_t ld = p.ld;
   const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -387,14 +537,24 @@ __global__ void __launch_bounds__(256) chol_kernel(CholParams p) {
     __syncthreads();
     if (tid < 32) {
       const int lane = tid;
+      unsigned dep = 0u;
       for (int c = 0; c < w; ++c) {
         double dcc = Ljj[c][c];
-        if (!(dcc > 0.0)) {
+        // A pivot below delta means column c is numerically dependent on the
+        // previous ones: give it a unit pivot and a zero sub-column, i.e. keep
+        // the (tiny) residual of that column as is.  The next column-scaled
+        // CholQR pass normalises it.  Stable, unlike flooring the pivot.
+        const bool d = !(dcc > p.delta);
+        __syncwarp();
+        if (d) {
           if (lane == 0 && blockIdx.x == 0) atomicOr(p.info + 1, 1);
-          dcc = 1e-300;
+          dep |= 1u << c;
+          if (lane == c) Ljj[c][c] = 1.0;
+          if (lane > c && lane < w) Ljj[lane][c] = 0.0;
+          __syncwarp();
+          continue;
         }
         double piv = sqrt(dcc);
-        __syncwarp();
         if (lane == c) Ljj[c][c] = piv;
         if (lane > c && lane < w) Ljj[lane][c] /= piv;
         __syncwarp();
@@ -404,17 +564,7 @@ __global__ void __launch_bounds__(256) chol_kernel(CholParams p) {
         }
         __syncwarp();
       }
-      // inverse of the lower-triangular Ljj: lane c builds column c
-      if (lane < w) {
-        const int c = lane;
-        for (int i = 0; i < CW; ++i) Inv[i][c] = 0.0;
-        Inv[c][c] = 1.0 / Ljj[c][c];
-        for (int i = c + 1; i < w; ++i) {
-          double s = 0.0;
-          for (int k = c; k < i; ++k) s = fma(Ljj[i][k], Inv[k][c], s);
-          Inv[i][c] = -s / Ljj[i][i];
-        }
-      }
+      if (lane == 0) depmask = dep;
     }
     __syncthreads();
     if (blockIdx.x == 0) {
@@ -445,24 +595,22 @@ __global__ void __launch_bounds__(256) chol_kernel(CholParams p) {
         Xk[r][c] = ak;
       }
       __syncthreads();
-      double li[4], lk[4];
-      int cnt = 0;
-      for (int e = tid; e < CW * CW; e += blockDim.x, ++cnt) {
-        int r = e % CW, c = e / CW;
-        double s = 0.0, sk = 0.0;
-        for (int k = 0; k <= c && k < w; ++k) {
-          s = fma(Xi[r][k], Inv[c][k], s);
-          sk = fma(Xk[r][k], Inv[c][k], sk);
+      // forward substitution L_Ij Ljj^T = A_Ij (and L_Kj), dependent columns zero
+      if (tid < 2 * CW) {
+        double(*X)[CW + 1] = tid < CW ? Xi : Xk;
+        const int r = tid & (CW - 1);
+        const int wr = tid < CW ? wi : wk;
+        if (r < wr) {
+          for (int cc = 0; cc < w; ++cc) {
+            if (depmask & (1u << cc)) {
+              X[r][cc] = 0.0;
+              continue;
+            }
+            double v = X[r][cc];
+            for (int k = 0; k < cc; ++k) v -= X[r][k] * Ljj[cc][k];
+            X[r][cc] = v / Ljj[cc][cc];
+          }
         }
-        li[cnt] = s;
-        lk[cnt] = sk;
-      }
-      __syncthreads();
-      cnt = 0;
-      for (int e = tid; e < CW * CW; e += blockDim.x, ++cnt) {
-        int r = e % CW, c = e / CW;
-        Xi[r][c] = (r < wi && c < w) ? li[cnt] : 0.0;
-        Xk[r][c] = (r < wk && c < w) ? lk[cnt] : 0.0;
       }
       __syncthreads();
       if (I == K) {  // owner writes the panel block of L (as L^T)
@@ -512,6 +660,7 @@ int chol_inv_scaled(int64_t b, const double* S, int64_t lds, double shift_rel, d
   CholParams cp{};
   cp.b = (int)b; cp.S = S; cp.lds = lds; cp.shift = shift_rel; cp.A = ws.A0; cp.Lt = ws.A1;
   cp.d = ws.cs; cp.ld = ws.ld; cp.bar = ws.bar; cp.info = ws.info;
+  cp.delta = 1e-13;
   const int threads = 256;
   int nbk = (int)cdiv(b, CW);
   int64_t want = std::max<int64_t>(1, (int64_t)(nbk - 1) * nbk / 2);

@@ -344,29 +344,36 @@ def gram(U, stream=None):
     return G  # symmetric; column-major == row-major
 
 
+def _even_ld(X):
+    """Row-major 2-D tensor with an even, 16-byte aligned leading dimension (zero padded)."""
+    import torch
+    X = X.contiguous()
+    r, c = X.shape
+    if c % 2 == 0 and X.data_ptr() % 16 == 0:
+        return X, c
+    P = torch.zeros(r, c + (c % 2), dtype=X.dtype, device=X.device)
+    P[:, :c] = X
+    return P, P.shape[1]
+
+
 def dgemm(A, B, transa=False, transb=False, stream=None):
-    """C = op(A) op(B) with torch row-major tensors (maps onto the col-major ABI)."""
+    """C = op(A) op(B) for torch row-major tensors (mapped onto the col-major ABI:
+    row-major C (M x N) is col-major C^T = op(B)^T op(A)^T)."""
     import torch
     _need_cuda_f64(A, "A")
     _need_cuda_f64(B, "B")
-    A = A.contiguous()
-    B = B.contiguous()
-    # row-major X (r x c) is col-major X^T (c x r).  C^T = op(B)^T op(A)^T.
-    opA = A.t() if transa else A
-    opB = B.t() if transb else B
-    M, K = opA.shape
-    K2, N = opB.shape
+    M, K = (A.shape[1], A.shape[0]) if transa else (A.shape[0], A.shape[1])
+    K2, N = (B.shape[1], B.shape[0]) if transb else (B.shape[0], B.shape[1])
     assert K == K2
-    Ct = torch.empty(N, M, dtype=torch.float64, device=A.device)  # row-major C (M x N) = col-major C^T
-    # col-major: C^T (N x M) = op'(B) (N x K) * op'(A) (K x M)
-    # B row-major (rB x cB) is col-major B^T.  If not transb: op(B) = B, need B^T col-major = 'N' on buffer.
-    ta = b"N" if not transb else b"T"
-    tb = b"N" if not transa else b"T"
-    ldb_buf = B.shape[1]
-    lda_buf = A.shape[1]
-    _check(lib().rhosvd_dgemm(ta, tb, N, M, K, 1.0, _ptr(B), ldb_buf, _ptr(A), lda_buf, 0.0,
+    Ab, lda = _even_ld(A)
+    Bb, ldb = _even_ld(B)
+    Ct = torch.empty(M, N, dtype=torch.float64, device=A.device)
+    # col-major view of a row-major buffer X is X^T: op(B)^T is 'N' on B's buffer unless transb
+    ta = b"T" if transb else b"N"
+    tb = b"T" if transa else b"N"
+    _check(lib().rhosvd_dgemm(ta, tb, N, M, K, 1.0, _ptr(Bb), ldb, _ptr(Ab), lda, 0.0,
                               _ptr(Ct), N, _stream_ptr(stream)))
-    return Ct.view(M, N)
+    return Ct
 
 
 def syevj(S, tol=1e-15, stream=None):

@@ -1,0 +1,46 @@
+"""Run rhosvd_c2t on a BASELINE.json config (inputs generated on the GPU) and
+print the per-phase report; used for ncu launch lists and quick timing.
+
+    python tools/run_config.py --config 2 --reps 2
+"""
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--reps", type=int, default=2)
+    ap.add_argument("--block0", type=int, default=128)
+    ap.add_argument("--oversample", type=int, default=16)
+    args = ap.parse_args()
+    import torch
+    from paper_2201_12663_b200 import rhosvd
+    from workloads import make_config, make_params
+    p = make_params(args.config)
+    dev = torch.device("cuda:0")
+    U1, U2, U3, xi = make_config(p, backend="torch", device=dev)
+    lib = rhosvd.lib()
+    opts = rhosvd.make_opts(eps=p.eps, ranks=p.ranks, block0=args.block0, oversample=args.oversample)
+    for i in range(args.reps):
+        t0 = time.perf_counter()
+        h = rhosvd.c2t_raw((U1, U2, U3), xi, opts)
+        rep = rhosvd.Report()
+        lib.rhosvd_result_report(h, rhosvd.C.byref(rep))
+        lib.rhosvd_result_free(h)
+        torch.cuda.synchronize()
+        d = rhosvd._report_dict(rep)
+        d["wall_s"] = time.perf_counter() - t0
+        print(json.dumps({"config": args.config, "rep": i, **{k: d[k] for k in
+                          ("ranks", "block", "iters", "grow_events", "ms", "core_ms", "gram_ms", "launches",
+                           "gemm_flops", "wall_s", "tail", "beta_norm")}}), flush=True)
+
+
+if __name__ == "__main__":
+    main()
