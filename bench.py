@@ -170,6 +170,16 @@ def run_reference(args):
     return 0
 
 
+def max_over_ranks(ms, dev=None):
+    """Max of a per-rank time over all ranks (bench contract: max over ranks)."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(ms)], dtype=torch.float64, device=dev)
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
 # ---------------------------------------------------------------- our arm
 def run_ours(args):
     import torch
@@ -225,11 +235,7 @@ def run_ours(args):
     e1.record(stream)
     torch.cuda.synchronize(dev)
     clk = clocks.stop()
-    ms = e0.elapsed_time(e1)
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
-    if distributed:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = max_over_ranks(e0.elapsed_time(e1), dev)
     value = p.R * args.steps / (ms_max * 1e-3)
 
     # dominant kernel roofline (FP64 DMMA pipe): the core K7 for cfg 2/4, the Gram K1 for cfg 3/5
@@ -286,11 +292,8 @@ def run_ours(args):
             e2e_step()
         q1.record(stream)
         torch.cuda.synchronize(dev)
-        ems = q0.elapsed_time(q1)
-        te = torch.tensor([ems], dtype=torch.float64, device=dev)
-        if distributed:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e = {"value": p.R * ks / (float(te.item()) * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
+        ems = max_over_ranks(q0.elapsed_time(q1), dev)
+        e2e = {"value": p.R * ks / (ems * 1e-3), "unit": UNIT, "h2d_bytes_per_step": h2d,
                "d2h_bytes_per_step": d2h, "steps": ks, "wall_s": time.perf_counter() - t0}
 
     cpu = None
