@@ -4,135 +4,183 @@
 // of the RHOSVD Tucker tensor is the rank-R CP tensor with factors W_l = Z_l^T Uhat_l,
 // "calculated entry-wise in O(R r1 ... rd) operations".  We compute it densely as
 //     beta_(12)(3) = (W1 (.) W2) (xi' o W3)^T      M = r1 r2, N = r3, K = R
-// where the Khatri-Rao row (a,b) of a k-tile is never materialised: the CTA
-// stages W1 (TA rows), W2 (TB rows) and W3 (BN rows) k-tiles in shared memory by
-// cp.async and each DMMA A-fragment is formed in registers as W1[a,k] * W2[b,k]
-// (one DMUL per fragment element; xi' is pre-folded into W1).  The materialised
-// Khatri-Rao operand would be 152 GiB on cfg 4.
-// Output beta[a,b,c] in C order (c fastest).  Split-K (for small r, large R)
-// writes fixed-order partials reduced by a second kernel (deterministic).
-#include "common.cuh"
+// with the Khatri-Rao operand never materialised (152 GiB on cfg 4).
+//
+// Design (B200):
+//  * M is the FLATTENED Khatri-Rao row index m = a r2 + b, tiled by BM = 128, so the
+//    only padding is the ragged end of r1 r2 (no per-mode padding of r2).  N = r3 is
+//    tiled by BN in {64, 96, 128}, chosen per call to minimise padding.
+//  * Operands arrive by TMA (cp.async.bulk.tensor.2d, 128-B swizzle, 16-double k
+//    slabs): per k-slab, one box of A1 = (BM-1)/r2 + 2 rows of xi' o W1 (every a the
+//    tile touches), one box of 128 rows of W2ext (W2 with its first rows repeated
+//    after the end, so the wrap b -> 0 inside a tile is a contiguous box), one box of
+//    BN rows of W3.  Out-of-range rows/columns are zero-filled by TMA (ragged R, r1).
+//  * Pipeline: thread 0 issues TMA into a STAGES-deep ring guarded by full/empty
+//    mbarriers (it refills the stage the 8 warps released one step earlier, so the
+//    ring stays STAGES-1 slabs ahead); 8 warps stacked along M (warp tile 16 x BN, so no
+//    Khatri-Rao row is formed twice; 2 warps per SM sub-partition so each may hold 255
+//    registers - a 9th producer warp would cap them at 168) form each A fragment in
+//    registers as W1[a,k] * W2[b,k] (one DMUL) and
+//    issue mma.sync.m8n8k4.f64 (SASS DMMA.8x8x4 - the only FP64 tensor instruction on
+//    sm_100a; tcgen05 has no f64 kind).
+//  * Persistent grid (one CTA per SM, static stride over work items) so all CTAs
+//    stream the same k-slabs at the same time and the W tiles are L2 hits.
+//  * Small problems split K; partials go to scratch and a second kernel sums them in
+//    fixed order (deterministic, no FP64 atomics; reading A18).
+// Output beta[a,b,c] in C order (c fastest).
+#include <algorithm>
+
+#include "tma.cuh"
 
 namespace rhosvd {
 
-struct CoreParams {
+constexpr int CORE_BM = 128, CORE_BK = 16, CORE_WARPS = 8;
+constexpr int CORE_THREADS = 32 * CORE_WARPS;
+
+struct CoreArgs {
   int r1, r2, r3, R;
-  const double* W1;  // xi' o W1, row-major r1 x R (ld ldw1)
-  int64_t ldw1;
-  const double* W2;
-  const double* W3;
-  int64_t ldw;
-  double* out;       // beta or partials [split][r1 r2 r3]
-  int splits, kchunk;
-  int tiles_a, tiles_b, tiles_n;
+  int A1;            // W1 rows per box
+  int A1pad;         // rounded to 8 (1024-B aligned sub-tiles)
+  int mt, nt, tiles, splits, kchunk, items;
+  int stages;
+  uint32_t stage_bytes, tx_bytes;
+  double* out;       // beta (splits == 1) or partials [split][r1 r2 r3]
 };
 
-template <int TA, int TB, int BN, int BK, int WM, int WN, int STAGES>
-struct CoreCfg {
-  static constexpr int BM = TA * TB;
-  static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
-  static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
-  static constexpr int FM = WM / 8, FN = WN / 8;
-  static constexpr int P = BK + 4;  // k-contiguous pitch (== 4 mod 16)
-  static constexpr int S1 = TA * P, S2 = TB * P, S3 = BN * P;
-  static constexpr int STAGE = S1 + S2 + S3;
-  static constexpr size_t SMEM = size_t(STAGES) * STAGE * sizeof(double);
-};
+template <int BN>
+__global__ void __launch_bounds__(CORE_THREADS, 1)
+    core_kr_tma_kernel(const __grid_constant__ CUtensorMap tW1, const __grid_constant__ CUtensorMap tW2,
+                       const __grid_constant__ CUtensorMap tW3, const CoreArgs p) {
+  constexpr int WM = 16, FM = 2, FN = BN / 8;  // 8 warps stacked along M, each 16 x BN
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  // 1024-B align the ring (128-B swizzle atoms); offsetting the __shared__ array keeps
+  // the address space visible to the compiler (LDS, 32-bit addressing)
+  unsigned char* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = (uint64_t*)(ring + (size_t)p.stages * p.stage_bytes);
+  uint64_t* empty = full + p.stages;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool producer = (tid == 0);
+  const int M = p.r1 * p.r2;
+  const uint32_t w2_off = (uint32_t)p.A1pad * 128, w3_off = w2_off + CORE_BM * 128;
 
-template <int TA, int TB, int BN, int BK, int WM, int WN, int STAGES>
-__global__ void __launch_bounds__(CoreCfg<TA, TB, BN, BK, WM, WN, STAGES>::THREADS)
-    core_kr_kernel(CoreParams p) {
-  using Cfg = CoreCfg<TA, TB, BN, BK, WM, WN, STAGES>;
-  static_assert(TB % 8 == 0, "TB multiple of 8");
-  extern __shared__ __align__(16) double smem[];
-  int t = blockIdx.x;
-  const int tn = t % p.tiles_n;
-  t /= p.tiles_n;
-  const int tb = t % p.tiles_b;
-  const int ta = t / p.tiles_b;
-  const int a0 = ta * TA, b0 = tb * TB, n0 = tn * BN;
-  const int split = blockIdx.y;
-  const int kbeg = split * p.kchunk, kend = min(p.R, kbeg + p.kchunk);
-  const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm0 = (warp % Cfg::WARPS_M) * WM, wn0 = (warp / Cfg::WARPS_M) * WN;
-
-  auto load_rows = [&](double* dst, const double* src, int64_t ld, int row0, int nrows_tile, int nrows_tot,
-                       int k0) {
-    constexpr int CPR = BK / 2;
-    const int TOT = nrows_tile * CPR;
-    for (int c = tid; c < TOT; c += Cfg::THREADS) {
-      int r = c / CPR, cc = (c % CPR) * 2;
-      int gr = row0 + r, gk = k0 + cc;
-      int nb = (gr < nrows_tot) ? max(0, min(2, kend - gk)) : 0;
-      const double* s = nb ? src + (int64_t)gr * ld + gk : src;
-      cp_async16(dst + r * Cfg::P + cc, s, nb * 8);
+  // producer cursor over this CTA's k-tile stream (items strided by gridDim.x); the
+  // item's box coordinates are recomputed only when the cursor moves to a new item
+  int pit = blockIdx.x, pk = 0, pkend = 0, pa = 0, pb = 0, pn = 0;
+  auto set_item = [&]() {
+    if (pit >= p.items) return;
+    const int split = pit / p.tiles, tile = pit % p.tiles;
+    const int m0 = (tile % p.mt) * CORE_BM;
+    pk = split * p.kchunk;
+    pkend = min(p.R, pk + p.kchunk);
+    pa = m0 / p.r2;
+    pb = m0 % p.r2;
+    pn = (tile / p.mt) * BN;
+  };
+  auto issue_next = [&](int stage) {
+    if (pit >= p.items) return;
+    unsigned char* st = ring + (size_t)stage * p.stage_bytes;
+    mbar_arrive_expect_tx(&full[stage], p.tx_bytes);
+    tma_load_2d(st, &tW1, pk, pa, &full[stage]);
+    tma_load_2d(st + w2_off, &tW2, pk, pb, &full[stage]);
+    tma_load_2d(st + w3_off, &tW3, pk, pn, &full[stage]);
+    pk += CORE_BK;
+    if (pk >= pkend) {
+      pit += gridDim.x;
+      set_item();
     }
   };
-  auto load_stage = [&](int stage, int kt) {
-    const int k0 = kbeg + kt * BK;
-    double* base = smem + stage * Cfg::STAGE;
-    load_rows(base, p.W1, p.ldw1, a0, TA, p.r1, k0);
-    load_rows(base + Cfg::S1, p.W2, p.ldw, b0, TB, p.r2, k0);
-    load_rows(base + Cfg::S1 + Cfg::S2, p.W3, p.ldw, n0, BN, p.r3, k0);
-  };
 
-  double acc[Cfg::FM][Cfg::FN][2];
-#pragma unroll
-  for (int i = 0; i < Cfg::FM; ++i)
-#pragma unroll
-    for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) load_stage(s, s);
-    cp_async_commit();
+  if (producer) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CORE_WARPS);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&tW1);
+    tma_prefetch_desc(&tW2);
+    tma_prefetch_desc(&tW3);
   }
+  __syncthreads();
+  if (producer) {
+    set_item();
+    for (int s = 0; s < p.stages; ++s) issue_next(s);
+  }
+
   const int fr = lane >> 2, fc = lane & 3;
-  for (int kt = 0; kt < nk; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    {
-      int nx = kt + STAGES - 1;
-      if (nx < nk) load_stage(nx % STAGES, nx);
-      cp_async_commit();
+  const int wm0 = warp * WM;
+  // per-lane byte offsets of (row with row%8 == fr, k = kk + fc) inside a swizzled slab
+  uint32_t koff[CORE_BK / 4];
+#pragma unroll
+  for (int q = 0; q < CORE_BK / 4; ++q) koff[q] = sw128_off(fr, 4 * q + fc) - fr * 128;
+  const uint32_t ring_s = smem_u32(ring);
+  uint32_t g = 0;  // k-tiles consumed by this CTA
+  for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
+    const int split = it / p.tiles, tile = it % p.tiles;
+    const int tm = tile % p.mt, tn = tile / p.mt;
+    const int m0 = tm * CORE_BM, n0 = tn * BN;
+    const int a_lo = m0 / p.r2;
+    const int kbeg = split * p.kchunk, kend = min(p.R, kbeg + p.kchunk);
+    // W1 row (inside the box) of each fragment row this lane touches -> byte offsets
+    uint32_t w1off[FM][CORE_BK / 4];
+#pragma unroll
+    for (int i = 0; i < FM; ++i) {
+      const int m = min(m0 + wm0 + i * 8 + fr, M - 1);
+      const int row = m / p.r2 - a_lo;
+#pragma unroll
+      for (int q = 0; q < CORE_BK / 4; ++q) w1off[i][q] = sw128_off(row, 4 * q + fc);
     }
-    const double* w1 = smem + (kt % STAGES) * Cfg::STAGE;
-    const double* w2 = w1 + Cfg::S1;
-    const double* w3 = w2 + Cfg::S2;
+    double acc[FM][FN][2];
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[Cfg::FM], bf[Cfg::FN];
+    for (int i = 0; i < FM; ++i)
 #pragma unroll
-      for (int i = 0; i < Cfg::FM; ++i) {
-        const int mi = wm0 + i * 8;        // fragment rows mi .. mi+7 share a_loc
-        const int al = mi / TB, bl = mi % TB + fr;
-        af[i] = w1[al * Cfg::P + kk + fc] * w2[bl * Cfg::P + kk + fc];
-      }
-#pragma unroll
-      for (int j = 0; j < Cfg::FN; ++j) bf[j] = w3[(wn0 + j * 8 + fr) * Cfg::P + kk + fc];
-#pragma unroll
-      for (int i = 0; i < Cfg::FM; ++i)
-#pragma unroll
-        for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-    }
-  }
-  cp_async_wait<0>();
+      for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-  double* out = p.out + (p.splits > 1 ? (int64_t)split * p.r1 * p.r2 * p.r3 : 0);
-#pragma unroll
-  for (int i = 0; i < Cfg::FM; ++i) {
-    const int mi = wm0 + i * 8 + fr;
-    const int a = a0 + mi / TB, bb = b0 + mi % TB;
-    if (a >= p.r1 || bb >= p.r2) continue;
-    double* row = out + ((int64_t)a * p.r2 + bb) * p.r3;
-#pragma unroll
-    for (int j = 0; j < Cfg::FN; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        int n = n0 + wn0 + j * 8 + 2 * fc + h;
-        if (n < p.r3) row[n] = acc[i][j][h];
+    for (int k0 = kbeg; k0 < kend; k0 += CORE_BK, ++g) {
+      // refill the stage released one step ago (its 8 warps are done with it)
+      if (producer && g >= 1) {
+        const uint32_t gp = g - 1, sp = gp % p.stages;
+        mbar_wait(&empty[sp], (gp / p.stages) & 1);
+        issue_next((int)sp);
       }
+      const uint32_t s = g % p.stages;
+      mbar_wait(&full[s], (g / p.stages) & 1);
+      const uint32_t w1 = ring_s + s * p.stage_bytes;
+      const uint32_t w2 = w1 + w2_off + (wm0 + fr) * 128;
+      const uint32_t w3 = w1 + w3_off + fr * 128;
+#pragma unroll
+      for (int q = 0; q < CORE_BK / 4; ++q) {
+        double af[FM], bf[FN];
+#pragma unroll
+        for (int i = 0; i < FM; ++i) af[i] = lds_f64(w1 + w1off[i][q]) * lds_f64(w2 + koff[q] + i * 1024);
+#pragma unroll
+        for (int j = 0; j < FN; ++j) bf[j] = lds_f64(w3 + koff[q] + j * 1024);
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    // epilogue: rows m (flattened a r2 + b), columns n of beta_(12)(3)
+    double* out = p.out + (p.splits > 1 ? (int64_t)split * M * p.r3 : 0);
+    const bool even = (p.r3 & 1) == 0;
+#pragma unroll
+    for (int i = 0; i < FM; ++i) {
+      const int m = m0 + wm0 + i * 8 + fr;
+      if (m >= M) continue;
+      double* row = out + (int64_t)m * p.r3;
+#pragma unroll
+      for (int j = 0; j < FN; ++j) {
+        const int n = n0 + j * 8 + 2 * fc;
+        if (even && n + 1 < p.r3) {
+          *(double2*)(row + n) = make_double2(acc[i][j][0], acc[i][j][1]);
+        } else {
+          if (n < p.r3) row[n] = acc[i][j][0];
+          if (n + 1 < p.r3) row[n + 1] = acc[i][j][1];
+        }
+      }
+    }
   }
 }
 
@@ -153,41 +201,106 @@ __global__ void scale_cols_kernel(const double* W, int64_t ldw, const double* xi
   out[a * ldo + k] = W[a * ldw + k] * xi[k];
 }
 
-// host entry: beta (r1 x r2 x r3, C order) = sum_k xi_k W1[:,k] (x) W2[:,k] (x) W3[:,k]
-// W1x must already hold xi' o W1.  part: scratch for split-K (may be null when splits == 1)
-int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3, int64_t ldw, int64_t r1,
-            int64_t r2, int64_t r3, int64_t R, double* beta, double* part, size_t part_cap, cudaStream_t st,
-            double* flops_acc) {
-  if (r1 <= 0 || r2 <= 0 || r3 <= 0) return RHOSVD_OK;
-  constexpr int TA = 2, TB = 64, BN = 128, BK = 16, WM = 64, WN = 32, ST = 3;
-  using Cfg = CoreCfg<TA, TB, BN, BK, WM, WN, ST>;
-  auto kern = core_kr_kernel<TA, TB, BN, BK, WM, WN, ST>;
-  static bool attr = false;
-  if (!attr) {
-    RH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
-    attr = true;
+// W2ext[j] = W2[j mod r2] for j < r2 + ext (row-major, ld ldw -> ldo)
+__global__ void wrap_rows_kernel(const double* W, int64_t ldw, int r2, int ext, int R, double* out, int64_t ldo) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)(r2 + ext) * R) return;
+  int j = (int)(e / R), k = (int)(e % R);
+  out[(int64_t)j * ldo + k] = W[(int64_t)(j % r2) * ldw + k];
+}
+
+static int pick_bn(int64_t r3) {
+  // padded N work with a mild preference for wide tiles (fewer W1/W2 re-reads)
+  const int cand[3] = {128, 96, 64};
+  int best = 128;
+  double bc = 1e300;
+  for (int bn : cand) {
+    double c = (double)cdiv(r3, bn) * bn * (1.0 + 0.03 * (128.0 / bn - 1.0));
+    if (c < bc) {
+      bc = c;
+      best = bn;
+    }
   }
-  CoreParams cp{};
-  cp.r1 = (int)r1; cp.r2 = (int)r2; cp.r3 = (int)r3; cp.R = (int)R;
-  cp.W1 = W1x; cp.ldw1 = ldw1; cp.W2 = W2; cp.W3 = W3; cp.ldw = ldw;
-  cp.tiles_a = (int)cdiv(r1, TA); cp.tiles_b = (int)cdiv(r2, TB); cp.tiles_n = (int)cdiv(r3, BN);
-  int64_t tiles = (int64_t)cp.tiles_a * cp.tiles_b * cp.tiles_n;
-  int64_t total = r1 * r2 * r3;
-  int splits = 1;
+  return best;
+}
+
+size_t core_ws_doubles(int64_t r2, int64_t R, int64_t ldw) {
+  return (size_t)(r2 + CORE_BM) * std::max<int64_t>(ldw, round_up(std::max<int64_t>(R, 2), 16));
+}
+
+template <int BN>
+static int launch_core(const CUtensorMap& t1, const CUtensorMap& t2, const CUtensorMap& t3, const CoreArgs& a,
+                       size_t smem, int grid, cudaStream_t st) {
+  auto kern = core_kr_tma_kernel<BN>;
+  RH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  kern<<<grid, CORE_THREADS, smem, st>>>(t1, t2, t3, a);
+  count_launch();
+  RH_LAUNCH_CHECK();
+  return RHOSVD_OK;
+}
+
+// host entry: beta (r1 x r2 x r3, C order) = sum_k W1x[:,k] (x) W2[:,k] (x) W3[:,k]
+// W1x must already hold xi' o W1.  All W row-major with k fastest, leading dims ldw1 / ldw
+// (multiples of 2 doubles, 16-B aligned rows).  ws: >= core_ws_doubles(r2, R, ldw) doubles
+// (W2ext); part: split-K scratch of part_cap doubles (may be 0).
+int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3, int64_t ldw, int64_t r1,
+            int64_t r2, int64_t r3, int64_t R, double* beta, double* ws, double* part, size_t part_cap,
+            cudaStream_t st, double* flops_acc) {
+  if (r1 <= 0 || r2 <= 0 || r3 <= 0) return RHOSVD_OK;
+  const int64_t M = r1 * r2, total = M * r3;
+  if (M > INT32_MAX || total > ((int64_t)1 << 40) || R > INT32_MAX)
+    return fail(RHOSVD_EINVAL, "core: problem too large");
+  if (R == 0) {
+    RH_CUDA(cudaMemsetAsync(beta, 0, (size_t)total * sizeof(double), st));
+    return RHOSVD_OK;
+  }
+  const int BN = pick_bn(r3);
+  CoreArgs a{};
+  a.r1 = (int)r1; a.r2 = (int)r2; a.r3 = (int)r3; a.R = (int)R;
+  a.A1 = (int)std::min<int64_t>((CORE_BM - 1) / r2 + 2, r1 + 1);
+  a.A1 = std::max(1, std::min(a.A1, 256));
+  a.A1pad = (int)round_up(a.A1, 8);
+  a.mt = (int)cdiv(M, CORE_BM);
+  a.nt = (int)cdiv(r3, BN);
+  a.tiles = a.mt * a.nt;
+  a.stage_bytes = (uint32_t)((a.A1pad + CORE_BM + BN) * 128);
+  a.tx_bytes = (uint32_t)((a.A1 + CORE_BM + BN) * 128);
+  const size_t budget = 227 * 1024 - 1024 - 256;
+  a.stages = (int)std::min<size_t>(8, budget / a.stage_bytes);
+  if (a.stages < 2) return fail(RHOSVD_EINVAL, "core: tile does not fit shared memory");
   const int sms = num_sms();
-  if (tiles < 2 * sms && R >= 1024) {
-    splits = (int)std::min<int64_t>(cdiv(2 * sms, tiles), R / 512);
+  int splits = 1;
+  if (a.tiles < sms && R >= 2048) {
+    splits = (int)std::min<int64_t>(cdiv(sms, a.tiles), R / 1024);
     splits = std::max(1, std::min(splits, 32));
     while (splits > 1 && (size_t)splits * total > part_cap) --splits;
   }
-  cp.kchunk = (int)round_up(cdiv(std::max<int64_t>(R, 1), splits), BK);
-  splits = (int)std::max<int64_t>(1, cdiv(std::max<int64_t>(R, 1), cp.kchunk));
-  cp.splits = splits;
-  cp.out = splits > 1 ? part : beta;
-  if (tiles > INT32_MAX) return fail(RHOSVD_EINVAL, "core: too many tiles");
-  kern<<<dim3((unsigned)tiles, splits), Cfg::THREADS, Cfg::SMEM, st>>>(cp);
-  count_launch();
-  RH_LAUNCH_CHECK();
+  a.kchunk = (int)round_up(cdiv(R, splits), CORE_BK);
+  splits = (int)cdiv(R, a.kchunk);
+  a.splits = splits;
+  a.items = a.tiles * splits;
+  a.out = splits > 1 ? part : beta;
+
+  // W2ext = W2 with rows [0, BM) repeated after row r2 - 1 (the wrap inside a tile)
+  const int64_t ldx = round_up(std::max<int64_t>(R, 2), 16);
+  {
+    const int64_t n_el = (r2 + CORE_BM) * R;
+    wrap_rows_kernel<<<(unsigned)cdiv(n_el, 256), 256, 0, st>>>(W2, ldw, (int)r2, CORE_BM, (int)R, ws, ldx);
+    count_launch();
+    RH_LAUNCH_CHECK();
+  }
+  CUtensorMap t1, t2, t3;
+  RH_CHECK(make_tmap_2d(&t1, W1x, r1, R, ldw1, CORE_BK, a.A1, true));
+  RH_CHECK(make_tmap_2d(&t2, ws, r2 + CORE_BM, R, ldx, CORE_BK, CORE_BM, true));
+  RH_CHECK(make_tmap_2d(&t3, W3, r3, R, ldw, CORE_BK, BN, true));
+  const size_t smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * a.stages * sizeof(uint64_t);
+  const int grid = (int)std::min<int64_t>(a.items, sms);
+  if (BN == 128)
+    RH_CHECK(launch_core<128>(t1, t2, t3, a, smem, grid, st));
+  else if (BN == 96)
+    RH_CHECK(launch_core<96>(t1, t2, t3, a, smem, grid, st));
+  else
+    RH_CHECK(launch_core<64>(t1, t2, t3, a, smem, grid, st));
   if (splits > 1) {
     core_splitk_reduce<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(part, splits, total, beta);
     count_launch();
@@ -203,6 +316,34 @@ int scale_cols(const double* W, int64_t ldw, const double* xi, int64_t r, int64_
   scale_cols_kernel<<<(unsigned)cdiv(r * R, 256), 256, 0, st>>>(W, ldw, xi, (int)r, (int)R, out, ldo);
   count_launch();
   RH_LAUNCH_CHECK();
+  return RHOSVD_OK;
+}
+
+// ------------------------------------------------------------------ tensor maps
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                  const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+int make_tmap_2d(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld, int box_cols,
+                 int box_rows, bool swizzle128) {
+  static EncodeTiledFn enc = nullptr;
+  if (!enc) {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    RH_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
+    if (!fn || q != cudaDriverEntryPointSuccess) return fail(RHOSVD_ECUDA, "cuTensorMapEncodeTiled unavailable");
+    enc = (EncodeTiledFn)fn;
+  }
+  if (((uintptr_t)base & 15) || ((ld * 8) & 15)) return fail(RHOSVD_EINVAL, "tensor map: 16-B alignment");
+  cuuint64_t gdim[2] = {(cuuint64_t)std::max<int64_t>(cols, 1), (cuuint64_t)std::max<int64_t>(rows, 1)};
+  cuuint64_t gstride[1] = {(cuuint64_t)(ld * 8)};
+  cuuint32_t box[2] = {(cuuint32_t)box_cols, (cuuint32_t)box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)base, gdim, gstride, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE,
+                   swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) return fail(RHOSVD_ECUDA, "cuTensorMapEncodeTiled failed: " + std::to_string((int)r));
   return RHOSVD_OK;
 }
 

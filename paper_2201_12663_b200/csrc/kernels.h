@@ -17,8 +17,9 @@ int k_select_rank(const double* lam, int64_t b, const double* rho, double T, dou
 int k_sign_fix(double* Z, int64_t ldz, int64_t n, int64_t r, double* W, int64_t ldw, int64_t Rl, double* sgn,
                cudaStream_t st);
 int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3, int64_t ldw, int64_t r1,
-            int64_t r2, int64_t r3, int64_t R, double* beta, double* part, size_t part_cap, cudaStream_t st,
-            double* flops_acc);
+            int64_t r2, int64_t r3, int64_t R, double* beta, double* ws, double* part, size_t part_cap,
+            cudaStream_t st, double* flops_acc);
+size_t core_ws_doubles(int64_t r2, int64_t R, int64_t ldw);
 int scale_cols(const double* W, int64_t ldw, const double* xi, int64_t r, int64_t R, double* out, int64_t ldo,
                cudaStream_t st);
 }  // namespace rhosvd

@@ -81,7 +81,7 @@ struct Workspace {
   DBuf Uh, s, tcol, xip, xip2, scal, part;
   DBuf G, Z, Y, M, T1;
   DBuf H, V, S, Bp, th, inv, tail2, sgn;
-  DBuf W, X, W1x, corepart;
+  DBuf W, X, W1x, W2x, corepart;
   Scratch gsc;
   DenseWs dws;
   int* flag = nullptr;
@@ -693,8 +693,9 @@ static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n
       RH_CHECK(scale_cols(mo[0].W, Rp, w.xip.p, r1, Rp, w.W1x.p, Rp, st));
       size_t pc = std::min<size_t>((size_t)total * 8, (size_t)1 << 28);
       RH_CHECK(w.corepart.ensure(pc, st));
+      RH_CHECK(w.W2x.ensure(core_ws_doubles(r2, Rl, Rp), st));
       cudaEventRecord(c0, st);
-      RH_CHECK(core_kr(w.W1x.p, Rp, mo[1].W, mo[2].W, Rp, r1, r2, r3, Rl, res->beta, w.corepart.p,
+      RH_CHECK(core_kr(w.W1x.p, Rp, mo[1].W, mo[2].W, Rp, r1, r2, r3, Rl, res->beta, w.W2x.p, w.corepart.p,
                        w.corepart.cap, st, &c.flops));
       cudaEventRecord(c1, st);
     } else {
@@ -835,7 +836,9 @@ int rhosvd_core(const double* W1, const double* W2, const double* W3, int64_t ld
   RH_CHECK(scale_cols(W1, ldw, xi, r1, R, w.W1x.p, ldx, st));
   size_t total = (size_t)r1 * r2 * r3;
   RH_CHECK(w.corepart.ensure(std::min<size_t>(total * 8, (size_t)1 << 28), st));
-  return core_kr(w.W1x.p, ldx, W2, W3, ldw, r1, r2, r3, R, beta, w.corepart.p, w.corepart.cap, st, nullptr);
+  RH_CHECK(w.W2x.ensure(core_ws_doubles(r2, R, ldw), st));
+  return core_kr(w.W1x.p, ldx, W2, W3, ldw, r1, r2, r3, R, beta, w.W2x.p, w.corepart.p, w.corepart.cap, st,
+                 nullptr);
 }
 
 }  // extern "C"

@@ -92,7 +92,9 @@ def test_syevj_graded_high_relative_accuracy(rh, b):
 
 
 @pytest.mark.parametrize("r,R", [((1, 1, 1), 1), ((3, 5, 7), 50), ((10, 10, 10), 200), ((70, 129, 33), 1500),
-                                 ((20, 20, 20), 40001)])
+                                 ((20, 20, 20), 40001), ((5, 130, 97), 3000), ((4, 3, 130), 777),
+                                 ((2, 1, 65), 100), ((40, 200, 300), 2000), ((130, 131, 97), 513),
+                                 ((30, 30, 60), 10), ((9, 256, 200), 4099)])
 def test_core(rh, r, R):
     from oracle import core_kr
     rng = np.random.default_rng(sum(r) + R)
