@@ -166,6 +166,14 @@ int rhosvd_dgemm(char transa, char transb, int64_t M, int64_t N, int64_t K, doub
 int rhosvd_syevj(int64_t b, double* A, int64_t lda, double* lambda, double* V, int64_t ldv,
                  double tol, int32_t* sweeps_out, rhosvd_stream stream);
 
+/* Scaled Cholesky inverse (the CholeskyQR building block):
+ * Bp (b x b, ldb) = D L^{-T} with D = diag(S)^{-1/2}, L = chol(D S D + shift I),
+ * S (b x b, lds) symmetric positive semi-definite.  Q = M Bp then has orthonormal
+ * columns for M^T M = S.  Numerically dependent columns (pivot < 1e-13) get a unit
+ * pivot and a zero sub-column.  All pointers device. */
+int rhosvd_chol_inv(int64_t b, const double* S, int64_t lds, double shift, double* Bp, int64_t ldb,
+                    rhosvd_stream stream);
+
 /* Core: beta[a,b,c] = sum_k xi[k] W1[a,k] W2[b,k] W3[c,k]; W_l row-major
  * r_l x R with leading dimension ldw; beta C order.  (Prop. 2.1.) */
 int rhosvd_core(const double* W1, const double* W2, const double* W3, int64_t ldw,

@@ -209,6 +209,7 @@ __global__ void wrap_rows_kernel(const double* W, int64_t ldw, int r2, int ext, 
   out[(int64_t)j * ldo + k] = W[(int64_t)(j % r2) * ldw + k];
 }
 
+
 static int pick_bn(int64_t r3) {
   // padded N work with a mild preference for wide tiles (fewer W1/W2 re-reads)
   const int cand[3] = {128, 96, 64};
@@ -222,6 +223,21 @@ static int pick_bn(int64_t r3) {
     }
   }
   return best;
+}
+
+// split-K factor for a problem (1 when the tiles alone fill the GPU)
+static int core_splits(int64_t r1, int64_t r2, int64_t r3, int64_t R, int BN) {
+  const int64_t tiles = cdiv(r1 * r2, CORE_BM) * cdiv(r3, BN);
+  const int sms = num_sms();
+  if (tiles >= sms || R < 2048) return 1;
+  int s = (int)std::min<int64_t>(cdiv(sms, tiles), R / 1024);
+  return std::max(1, std::min(s, 32));
+}
+
+// split-K scratch (doubles) the call needs; 0 when no split is used
+size_t core_part_doubles(int64_t r1, int64_t r2, int64_t r3, int64_t R) {
+  const int s = core_splits(r1, r2, r3, R, pick_bn(r3));
+  return s > 1 ? (size_t)s * r1 * r2 * r3 : 0;
 }
 
 size_t core_ws_doubles(int64_t r2, int64_t R, int64_t ldw) {
@@ -269,12 +285,8 @@ int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3,
   a.stages = (int)std::min<size_t>(8, budget / a.stage_bytes);
   if (a.stages < 2) return fail(RHOSVD_EINVAL, "core: tile does not fit shared memory");
   const int sms = num_sms();
-  int splits = 1;
-  if (a.tiles < sms && R >= 2048) {
-    splits = (int)std::min<int64_t>(cdiv(sms, a.tiles), R / 1024);
-    splits = std::max(1, std::min(splits, 32));
-    while (splits > 1 && (size_t)splits * total > part_cap) --splits;
-  }
+  int splits = core_splits(r1, r2, r3, R, BN);
+  while (splits > 1 && (size_t)splits * total > part_cap) --splits;
   a.kchunk = (int)round_up(cdiv(R, splits), CORE_BK);
   splits = (int)cdiv(R, a.kchunk);
   a.splits = splits;

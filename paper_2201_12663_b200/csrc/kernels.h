@@ -20,6 +20,7 @@ int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3,
             int64_t r2, int64_t r3, int64_t R, double* beta, double* ws, double* part, size_t part_cap,
             cudaStream_t st, double* flops_acc);
 size_t core_ws_doubles(int64_t r2, int64_t R, int64_t ldw);
+size_t core_part_doubles(int64_t r1, int64_t r2, int64_t r3, int64_t R);
 int scale_cols(const double* W, int64_t ldw, const double* xi, int64_t r, int64_t R, double* out, int64_t ldo,
                cudaStream_t st);
 }  // namespace rhosvd

@@ -19,6 +19,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -86,6 +87,67 @@ struct Workspace {
   DenseWs dws;
   int* flag = nullptr;
 };
+// Output buffers (frames, CP factors, sigma, core) outlive the call: the result handle
+// owns them.  A freed handle returns them here (after a device synchronisation) and the
+// next call takes the smallest cached buffer that fits, so a steady stream of same-size
+// calls never grows the memory pool (growing it to hold a 2.2 GB core costs ~0.1 s).
+struct OutCache {
+  std::mutex mu;
+  std::multimap<size_t, void*> free_;
+  std::map<void*, size_t> cap_;
+  size_t cached = 0;
+  int get(void** out, size_t bytes) {
+    std::lock_guard<std::mutex> lk(mu);
+    bytes = std::max<size_t>(bytes, 256);
+    auto it = free_.lower_bound(bytes);
+    if (it != free_.end() && it->first <= 2 * bytes + (1u << 20)) {
+      *out = it->second;
+      cached -= it->first;
+      free_.erase(it);
+      return RHOSVD_OK;
+    }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      // release everything cached and retry once
+      for (auto& kv : free_) {
+        cudaFree(kv.second);
+        cap_.erase(kv.second);
+      }
+      free_.clear();
+      cached = 0;
+      e = cudaMalloc(&p, bytes);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        return fail(RHOSVD_ENOMEM, std::string("output alloc: ") + cudaGetErrorString(e));
+      }
+    }
+    cap_[p] = bytes;
+    *out = p;
+    return RHOSVD_OK;
+  }
+  void put(void* p) {
+    if (!p) return;
+    std::lock_guard<std::mutex> lk(mu);
+    auto it = cap_.find(p);
+    if (it == cap_.end()) return;
+    free_.emplace(it->second, p);
+    cached += it->second;
+    while (cached > ((size_t)16 << 30) && !free_.empty()) {  // bound the cache at 16 GiB
+      auto big = std::prev(free_.end());
+      cached -= big->first;
+      cap_.erase(big->second);
+      cudaFree(big->second);
+      free_.erase(big);
+    }
+  }
+};
+static OutCache& OC() {
+  static OutCache c;
+  return c;
+}
+
 static Workspace& WS() {
   static Workspace w;
   return w;
@@ -218,7 +280,7 @@ static int orth(Ctx& c, int64_t n, int64_t b, int64_t ldn, const double* in, dou
 }
 
 struct ModeOut {
-  int r = 0, b = 0, iters = 0, grows = 0;
+  int r = 0, b = 0, iters = 0, grows = 0, refines = 0;
   double T = 0, tail2 = 0, rho = 0;
   double* Z = nullptr;      // n x r (ld LDN), owned by result
   double* sigma = nullptr;  // r
@@ -262,12 +324,14 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
   RH_CHECK(k_random(w.M.p, LDN, n, 0, b, seed, st));
   RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldbs(b), true));
 
-  // ---------------- phase 1: orthogonal (subspace) iteration Z <- CholQR(G Z) with
-  // block growth; no eigensolver.  The span of Z converges to the dominant
-  // subspace (rate lambda_{b+1}/lambda_k) and CholQR keeps leading spans, so the
-  // diagonal of Z^T G Z (cheap column dots) gives a running tail estimate
-  // T - sum_j (Z^T G Z)_jj for the block-size decision (eps mode).
-  std::vector<double> th_h, th_old, d_h;
+  // ---------------- subspace (simultaneous) iteration Z <- CholQR(G Z), block growth.
+  // CholQR keeps leading spans, so span(z_1..z_j) converges to the dominant j-space for
+  // every j (rate lambda_{b+1}/lambda_j) and the columns align with the eigenvectors
+  // except inside clusters: Z^T G Z tends to (nearly) diagonal, which is what makes the
+  // two Jacobi eigensolves below cheap.  The diagonal d_k = z_k^T G z_k (cheap column
+  // dots) gives the running tail estimate T - sum_{k<=r} d_k (>= the true tail) for the
+  // block-size decision (eps mode) and the rate estimate d_b / d_r for the iteration count.
+  std::vector<double> d_h;
   const double thr = epsmode ? o.eps * o.eps * T : 0.0;
   auto predict_r = [&](const std::vector<double>& d, int64_t bb) -> int64_t {
     double acc = 0.0;
@@ -296,139 +360,100 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     return (int64_t)std::ceil(rr);
   };
   int it_total = 0, itb = 0, guard = 0;
+  int64_t r_est = rfix;
   while (true) {
     ++it_total;
     ++itb;
     RH_CHECK(mm(c, n, b, n, G, LDN, false, w.Z.p, LDN, true, w.Y.p, LDN));
-    dbg_check(st, "p1 Y=GZ", w.Y.p, n, b, LDN);
-    if (epsmode) RH_CHECK(k_coldot(w.Z.p, w.Y.p, LDN, n, b, w.th.p, st));
-    RH_CHECK(orth(c, n, b, LDN, w.Y.p, w.Z.p, w.T1.p, ldbs(b), true));
-    dbg_check(st, "p1 Z=orth(Y)", w.Z.p, n, b, LDN);
-    if (b >= m) break;  // full space: nothing to iterate
+    RH_CHECK(k_coldot(w.Z.p, w.Y.p, LDN, n, b, w.th.p, st));
+    // the first steps after a (re)start see badly conditioned G Z: shifted CholQR3
+    RH_CHECK(orth(c, n, b, LDN, w.Y.p, w.Z.p, w.T1.p, ldbs(b), itb <= 2));
+    dbg_check(st, "it Z=orth(GZ)", w.Z.p, n, b, LDN);
+    if (b >= m) break;  // full space: exact after one step
     if (itb < 2) continue;
-    if (!epsmode) break;
     d_h.resize(b);
     RH_CUDA(cudaMemcpyAsync(d_h.data(), w.th.p, b * sizeof(double), cudaMemcpyDeviceToHost, st));
     RH_CUDA(cudaStreamSynchronize(st));
-    int64_t r_est = predict_r(d_h, b);
-    if (r_est + p > b && guard < 12) {
+    if (epsmode) r_est = predict_r(d_h, b);
+    if (epsmode && r_est + p > b && guard < 12) {
       int64_t bn = std::min<int64_t>(m, std::min<int64_t>(2 * b, std::max<int64_t>((int64_t)(1.15 * r_est) + p, b + p)));
       RH_CHECK(ensure_b(bn));
-      RH_CUDA(cudaMemcpyAsync(w.M.p, w.Z.p, (size_t)LDN * b * sizeof(double), cudaMemcpyDeviceToDevice, st));
-      RH_CHECK(k_random(w.M.p, LDN, n, b, bn, seed + 7919ull * (uint64_t)(it_total + 1), st));
+      RH_CHECK(k_random(w.Z.p, LDN, n, b, bn, seed + 7919ull * (uint64_t)(it_total + 1), st));
       b = bn;
-      RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldbs(b), true));
       itb = 0;
       ++mo.grows;
       ++guard;
       continue;
     }
-    break;
-  }
-  // ---------------- phase 2: Rayleigh-Ritz aligned iterations
-  //   Y = G Z, H = Z^T Y = V Theta V^T (Jacobi), Z <- CholQR(Y V Theta^-1)
-  // (Y V Theta^-1 = Z V + residual Theta^-1 with the residual orthogonal to Z, so
-  // its Gram is >= I: well conditioned).  The block is truncated to
-  // b' >= r + p chosen so that theta_b'/theta_r <= 0.05 (fast convergence).
-  double dth_old = -1.0;
-  int it2 = 0;
-  while (true) {
-    ++it_total;
-    ++it2;
-    const int64_t ldb = ldbs(b);
-    RH_CHECK(mm(c, n, b, n, G, LDN, false, w.Z.p, LDN, true, w.Y.p, LDN));
-    RH_CHECK(mm(c, b, b, n, w.Z.p, LDN, true, w.Y.p, LDN, true, w.H.p, ldb, nullptr, true));
-    int sw = 0;
-    dbg_check(st, "p2 H", w.H.p, b, b, ldb);
-    RH_CHECK(syevj(b, w.H.p, ldb, w.th.p, w.V.p, ldb, 1e-14, 1e-16, 60, w.dws, st, &sw));
-    dbg_check(st, "p2 theta", w.th.p, b, 1, b);
-    dbg_check(st, "p2 V", w.V.p, b, b, ldb);
-    if (dbg_on()) fprintf(stderr, "[rhosvd dbg] mode %d b %lld sweeps %d\n", mode, (long long)b, sw);
-    th_h.resize(b);
-    RH_CUDA(cudaMemcpyAsync(th_h.data(), w.th.p, b * sizeof(double), cudaMemcpyDeviceToHost, st));
-    RH_CUDA(cudaStreamSynchronize(st));
-    int64_t r_est = rfix;
-    if (epsmode) {
-      double acc = 0.0;
-      r_est = -1;
-      for (int64_t k = 0; k < b; ++k) {
-        acc += th_h[k];
-        if (T - acc <= thr) {
-          r_est = k + 1;
-          break;
-        }
-      }
-    }
-    RH_CHECK(k_ritz_floor(w.th.p, b, tau, w.inv.p, st));
-    RH_CHECK(mm(c, n, b, b, w.Y.p, LDN, false, w.V.p, ldb, true, w.M.p, LDN, w.inv.p));
-    if (epsmode && b < m && (r_est < 0 || r_est + p > b) && guard < 12) {
-      int64_t bn = std::min<int64_t>(m, r_est < 0 ? 2 * b : r_est + 2 * p);
-      RH_CHECK(ensure_b(bn));
-      RH_CHECK(k_random(w.M.p, LDN, n, b, bn, seed + 7919ull * (uint64_t)(it_total + 1), st));
-      b = bn;
-      RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldbs(b), true));
-      th_old.clear();
-      dth_old = -1.0;
-      ++mo.grows;
-      ++guard;
-      continue;
-    }
-    // block truncation: smallest b' in [r+p, b] with theta_{b'} <= 0.05 theta_r
-    int64_t bt = b;
-    if (r_est > 0 && r_est + p < b) {
-      const double tr = th_h[r_est - 1];
-      bt = b;
-      for (int64_t j = r_est + p; j <= b; ++j)
-        if (th_h[j - 1] <= 0.05 * tr) {
-          bt = j;
-          break;
-        }
-    }
-    double dth = -1.0;
-    if (r_est > 0 && (int64_t)th_old.size() >= r_est) {
-      dth = 0.0;
-      for (int64_t k = 0; k < r_est; ++k) dth = std::max(dth, std::fabs(th_h[k] - th_old[k]) / std::fabs(th_h[k]));
-    }
-    b = bt;
-    dbg_check(st, "p2 M", w.M.p, n, b, LDN);
-    RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldbs(b), true));
-    dbg_check(st, "p2 Z", w.Z.p, n, b, LDN);
-    bool conv = dth >= 0.0 && (dth < 1e-10 || (dth_old >= 0.0 && dth > 0.25 * dth_old));
-    if (b >= m) conv = true;  // full space: the subspace is exact
-    if (conv || it2 >= std::max(2, o.max_iters)) break;
-    th_old = th_h;
-    dth_old = dth;
+    // iterations for sin(theta_r) ~ 1e-7: rate d_b / d_r (d_b over-estimates lambda_{b+1})
+    const int64_t rr = std::max<int64_t>(1, std::min<int64_t>(r_est, b));
+    const double dr = std::max(d_h[rr - 1], 1e-300);
+    const double rho = std::min(0.999, std::max(d_h[b - 1], 1e-300 * dr) / dr);
+    const int need = std::max(2, (int)std::ceil(std::log(1e-7) / std::log(rho)));
+    if (itb >= std::min(need, std::max(2, o.max_iters))) break;
   }
   mo.iters = it_total;
+  // block truncation: smallest b' >= r + p with d_b' <= 0.05 d_r (leading columns carry
+  // the dominant subspaces)
+  if (!d_h.empty() && r_est > 0 && r_est + p < b) {
+    const double tr = d_h[r_est - 1];
+    for (int64_t j = r_est + p; j <= b; ++j)
+      if (d_h[j - 1] <= 0.05 * tr) {
+        b = j;
+        break;
+      }
+  }
   c.tm->mark(PH_RR);
 
   // ---------------- one-sided Rayleigh-Ritz + non-squared refinement + final RR
   const int64_t ldb = ldbs(b);
-  auto one_sided_rr = [&](const double* Zc, double* lam, double* P) -> int {
-    // W = Z^T Uhat  (b x Rp row-major, computed as Uhat^T Z col-major Rl x b)
-    RH_CHECK(mm(c, Rl, b, n, Uh, LDN, true, Zc, LDN, true, w.W.p, Rp));
-    // S = W W^T (b x b) summed over all R shards
-    RH_CHECK(mm(c, b, b, Rl, w.W.p, Rp, true, w.W.p, Rp, true, w.S.p, ldb, nullptr, true));
-    RH_CHECK(allreduce(c, w.S.p, ldb * b));
+
+  // Non-squared refinement: Z <- CholQR2(Uhat (Z^T Uhat)^T) = CholQR2(G Z)
+  // evaluated without G, so the subspace error contracts below the squared-Gram floor
+  // u kappa^2 / gap.  The Gram-domain iteration left Z aligned with the eigenvectors
+  // (simultaneous iteration), so G Z is well conditioned after column scaling and no
+  // Rayleigh-Ritz is needed between steps.  Stopping rule (a-posteriori): the column
+  // Rayleigh quotients d_k = ||w_k||^2 (k <= r) moved by <= 4e-11 relative in the last
+  // step; while the contraction rate is <= 1/2 the remaining error is below that change.
+  // At least refine_steps steps, at most refine_steps + 3.
+  const int max_ref = o.refine_steps > 0 ? o.refine_steps + 3 : 0;
+  const int64_t rcut = std::max<int64_t>(1, std::min<int64_t>(r_est > 0 ? r_est : b, b));
+  std::vector<double> dprev, dnow;
+  for (int rs = 0;; ++rs) {
+    // W = Z^T Uhat (b x Rp row-major == Rl x b col-major)
+    RH_CHECK(mm(c, Rl, b, n, Uh, LDN, true, w.Z.p, LDN, true, w.W.p, Rp));
+    if (rs >= max_ref) break;
+    if (rs >= 1) {
+      RH_CHECK(k_coldot(w.W.p, w.W.p, Rp, Rl, b, w.th.p, st));
+      RH_CHECK(allreduce(c, w.th.p, b));
+      dnow.resize(b);
+      RH_CUDA(cudaMemcpyAsync(dnow.data(), w.th.p, b * sizeof(double), cudaMemcpyDeviceToHost, st));
+      RH_CUDA(cudaStreamSynchronize(st));
+      if (!dprev.empty()) {
+        double delta = 0.0;
+        for (int64_t k = 0; k < rcut; ++k)
+          if (dnow[k] > 0.0) delta = std::max(delta, std::fabs(dnow[k] - dprev[k]) / dnow[k]);
+        if (dbg_on()) fprintf(stderr, "[rhosvd dbg] mode %d refine %d delta %.3e\n", mode, rs, delta);
+        if (rs >= o.refine_steps && delta <= 4e-11) break;
+      }
+      dprev.swap(dnow);
+    }
+    // M = Uhat W^T (summed over the R shards), Z <- CholQR2(M)
+    RH_CHECK(mm(c, n, b, Rl, Uh, LDN, false, w.W.p, Rp, true, w.M.p, LDN));
+    RH_CHECK(allreduce(c, w.M.p, LDN * b));
+    RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldb, false));
+    ++mo.refines;
     c.tm->mark(PH_RR);
+  }
+  // final one-sided Rayleigh-Ritz: W W^T = P Lambda P^T (high relative accuracy Jacobi)
+  RH_CHECK(mm(c, b, b, Rl, w.W.p, Rp, true, w.W.p, Rp, true, w.S.p, ldb, nullptr, true));
+  RH_CHECK(allreduce(c, w.S.p, ldb * b));
+  c.tm->mark(PH_RR);
+  {
     int sw = 0;
-    dbg_check(st, "rr S", w.S.p, b, b, ldb);
-    RH_CHECK(syevj(b, w.S.p, ldb, lam, P, ldb, 1e-15, 1e-300, 80, w.dws, st, &sw));
-    dbg_check(st, "rr lambda", lam, b, 1, b);
+    RH_CHECK(syevj(b, w.S.p, ldb, w.th.p, w.V.p, ldb, 1e-15, 1e-300, 80, w.dws, st, &sw));
     if (dbg_on()) fprintf(stderr, "[rhosvd dbg] mode %d rr b %lld sweeps %d\n", mode, (long long)b, sw);
     if (sw < 0) return fail(RHOSVD_ENOCONV, "Jacobi on W W^T did not converge");
-    return RHOSVD_OK;
-  };
-  RH_CHECK(one_sided_rr(w.Z.p, w.th.p, w.V.p));
-  for (int rs = 0; rs < std::max(0, o.refine_steps); ++rs) {
-    // X^T = Lambda^-1 P^T W  (stored as Rl x b col-major), M = Uhat X  (n x b)
-    RH_CHECK(k_ritz_floor(w.th.p, b, tau, w.inv.p, st));
-    RH_CHECK(mm(c, Rl, b, b, w.W.p, Rp, false, w.V.p, ldb, true, w.X.p, Rp, w.inv.p));
-    RH_CHECK(mm(c, n, b, Rl, Uh, LDN, false, w.X.p, Rp, true, w.M.p, LDN));
-    RH_CHECK(allreduce(c, w.M.p, LDN * b));
-    c.tm->mark(PH_RR);
-    RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldb, true));
-    RH_CHECK(one_sided_rr(w.Z.p, w.th.p, w.V.p));
   }
   c.tm->mark(PH_RANK);
   // rho = ||Uhat - Z W||_F^2 (fused residual epilogue; E never stored)
@@ -462,11 +487,11 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
   c.tm->mark(PH_PROJ);
   // outputs: Z_l = Z' P'_r, W_l^T = W'^T P'_r (Rl x r col-major == r x Rp row-major), sigma
   if (r > 0) {
-    RH_CUDA(cudaMallocAsync((void**)&mo.Z, (size_t)LDN * r * sizeof(double), st));
+    RH_CHECK(OC().get((void**)&mo.Z, (size_t)LDN * r * sizeof(double)));
     RH_CUDA(cudaMemsetAsync(mo.Z, 0, (size_t)LDN * r * sizeof(double), st));
-    RH_CUDA(cudaMallocAsync((void**)&mo.W, (size_t)r * Rp * sizeof(double), st));
+    RH_CHECK(OC().get((void**)&mo.W, (size_t)r * Rp * sizeof(double)));
     RH_CUDA(cudaMemsetAsync(mo.W, 0, (size_t)r * Rp * sizeof(double), st));
-    RH_CUDA(cudaMallocAsync((void**)&mo.sigma, (size_t)r * sizeof(double), st));
+    RH_CHECK(OC().get((void**)&mo.sigma, (size_t)r * sizeof(double)));
     RH_CHECK(mm(c, n, r, b, w.Z.p, LDN, false, w.V.p, ldb, true, mo.Z, LDN));
     RH_CHECK(mm(c, Rl, r, b, w.W.p, Rp, false, w.V.p, ldb, true, mo.W, Rp));
     RH_CUDA(cudaMemcpyAsync(mo.sigma, w.inv.p, r * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -512,16 +537,14 @@ void rhosvd_opts_default(rhosvd_opts* o) {
 
 void rhosvd_result_free(rhosvd_result* r) {
   if (!r) return;
-  // memory came from the stream-ordered pool: return it there (the pool keeps
-  // it for the next call instead of unmapping; cudaFree would release it)
+  // outputs go back to the library's output cache once no queued work uses them
   cudaDeviceSynchronize();
   for (int l = 0; l < 3; ++l) {
-    if (r->Z[l]) cudaFreeAsync(r->Z[l], 0);
-    if (r->sigma[l]) cudaFreeAsync(r->sigma[l], 0);
-    if (r->W[l]) cudaFreeAsync(r->W[l], 0);
+    OC().put(r->Z[l]);
+    OC().put(r->sigma[l]);
+    OC().put(r->W[l]);
   }
-  if (r->beta) cudaFreeAsync(r->beta, 0);
-  cudaStreamSynchronize(0);
+  OC().put(r->beta);
   delete r;
 }
 
@@ -660,9 +683,10 @@ static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n
     int st_ = solve_mode(c, l, n, LDN, Rl, Rp, Rg, Uh[l], w.G.p + (size_t)l * LDN * LDN, rep.trace[l], o, mo[l]);
     if (st_ != RHOSVD_OK) {
       for (int q = 0; q <= l; ++q) {
-        if (mo[q].Z) cudaFreeAsync(mo[q].Z, st);
-        if (mo[q].W) cudaFreeAsync(mo[q].W, st);
-        if (mo[q].sigma) cudaFreeAsync(mo[q].sigma, st);
+        cudaStreamSynchronize(st);
+        OC().put(mo[q].Z);
+        OC().put(mo[q].W);
+        OC().put(mo[q].sigma);
       }
       return st_;
     }
@@ -687,17 +711,28 @@ static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n
   cudaEventCreate(&c0);
   cudaEventCreate(&c1);
   if (total > 0) {
-    RH_CUDA(cudaMallocAsync((void**)&res->beta, (size_t)total * sizeof(double), st));
+    PhaseTimer dt(st);
+    if (dbg_on()) dt.mark(0);
+    RH_CHECK(OC().get((void**)&res->beta, (size_t)total * sizeof(double)));
+    if (dbg_on()) dt.mark(1);
     RH_CHECK(w.W1x.ensure((size_t)r1 * Rp, st));
     if (Rl > 0) {
       RH_CHECK(scale_cols(mo[0].W, Rp, w.xip.p, r1, Rp, w.W1x.p, Rp, st));
-      size_t pc = std::min<size_t>((size_t)total * 8, (size_t)1 << 28);
-      RH_CHECK(w.corepart.ensure(pc, st));
+      if (dbg_on()) dt.mark(2);
+      RH_CHECK(w.corepart.ensure(core_part_doubles(r1, r2, r3, Rl), st));
       RH_CHECK(w.W2x.ensure(core_ws_doubles(r2, Rl, Rp), st));
+      if (dbg_on()) dt.mark(3);
       cudaEventRecord(c0, st);
       RH_CHECK(core_kr(w.W1x.p, Rp, mo[1].W, mo[2].W, Rp, r1, r2, r3, Rl, res->beta, w.W2x.p, w.corepart.p,
                        w.corepart.cap, st, &c.flops));
       cudaEventRecord(c1, st);
+      if (dbg_on()) {
+        dt.mark(4);
+        double ms[16] = {0};
+        dt.collect(ms);
+        fprintf(stderr, "[rhosvd dbg] core phase: malloc beta %.3f, scale %.3f, ensure %.3f, core %.3f ms\n", ms[0],
+                ms[1], ms[2], ms[3]);
+      }
     } else {
       RH_CUDA(cudaMemsetAsync(res->beta, 0, (size_t)total * sizeof(double), st));
       cudaEventRecord(c0, st);
@@ -822,6 +857,13 @@ int rhosvd_syevj(int64_t b, double* A, int64_t lda, double* lambda, double* V, i
   return RHOSVD_OK;
 }
 
+int rhosvd_chol_inv(int64_t b, const double* S, int64_t lds, double shift, double* Bp, int64_t ldb,
+                    rhosvd_stream stream) {
+  if (!S || !Bp || b < 0 || lds < b || ldb < b || !(shift >= 0.0)) return fail(RHOSVD_EINVAL, "bad args");
+  std::lock_guard<std::mutex> lk(g_mu);
+  return chol_inv_scaled(b, S, lds, shift, Bp, ldb, WS().dws, (cudaStream_t)stream);
+}
+
 int rhosvd_core(const double* W1, const double* W2, const double* W3, int64_t ldw, const double* xi, int64_t r1,
                 int64_t r2, int64_t r3, int64_t R, double* beta, rhosvd_stream stream) {
   if (!W1 || !W2 || !W3 || !xi || !beta || r1 < 0 || r2 < 0 || r3 < 0 || R < 0 || ldw < R)
@@ -835,7 +877,7 @@ int rhosvd_core(const double* W1, const double* W2, const double* W3, int64_t ld
   RH_CHECK(w.W1x.ensure((size_t)r1 * ldx + 64, st));
   RH_CHECK(scale_cols(W1, ldw, xi, r1, R, w.W1x.p, ldx, st));
   size_t total = (size_t)r1 * r2 * r3;
-  RH_CHECK(w.corepart.ensure(std::min<size_t>(total * 8, (size_t)1 << 28), st));
+  RH_CHECK(w.corepart.ensure(core_part_doubles(r1, r2, r3, R), st));
   RH_CHECK(w.W2x.ensure(core_ws_doubles(r2, R, ldw), st));
   return core_kr(w.W1x.p, ldx, W2, W3, ldw, r1, r2, r3, R, beta, w.W2x.p, w.corepart.p, w.corepart.cap, st,
                  nullptr);

@@ -14,6 +14,8 @@
 //    grid barrier per panel), then the inverse of L one warp per column; the
 //    output D L^{-T} turns M into Q = M D L^{-T} (CholeskyQR).
 #include <cooperative_groups.h>
+#include <cstdio>
+#include <cstdlib>
 
 #include "small_dense.cuh"
 
@@ -21,27 +23,10 @@ namespace rhosvd {
 
 // ------------------------------------------------------------------ grid barrier
 __device__ __forceinline__ void grid_barrier(unsigned* bar) {
-  if (gridDim.x == 1) {
-    __syncthreads();
-    return;
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    volatile unsigned* vgen = bar + 1;
-    unsigned gen = *vgen;
-    __threadfence();
-    unsigned arrived = atomicAdd(bar, 1u);
-    if (arrived == gridDim.x - 1) {
-      atomicExch(bar, 0u);
-      __threadfence();
-      atomicAdd(bar + 1, 1u);
-    } else {
-      while (*vgen == gen) {
-      }
-    }
-    __threadfence();
-  }
-  __syncthreads();
+  // sense-free generation barrier: gpu-scope release/acquire (a .sys-scope volatile
+  // spin, as plain `volatile` compiles to, costs tens of microseconds per barrier)
+  (void)bar;
+  cooperative_groups::this_grid().sync();
 }
 
 __device__ __forceinline__ int rr_index(int pos, int step, int m) {
@@ -237,6 +222,7 @@ __global__ void __launch_bounds__(512) jacobi_kernel(JacParams p) {
 // place (each 2x2 block (P,Q), P <= Q, is read and written by one thread, its
 // mirror (Q,P) by the same thread), so a step costs two __syncthreads.
 constexpr int JAC_SMEM_MAXB = 160;
+__device__ __forceinline__ int64_t cdiv_d(int64_t a, int64_t b) { return (a + b - 1) / b; }
 __global__ void __launch_bounds__(1024) jacobi_smem_kernel(JacParams p) {
   extern __shared__ double sh[];
   const int h = p.h, b = p.b, m = p.m;
@@ -370,6 +356,306 @@ __global__ void __launch_bounds__(1024) jacobi_smem_kernel(JacParams p) {
   }
 }
 
+// ------------------------------------------------------------------ block Jacobi
+// Two-sided block Jacobi for b > JAC_SMEM_MAXB.  The b x b matrix is padded to
+// bp = m * BJ_W (m even; padded rows/columns are zero and never rotate) and split
+// into m blocks of BJ_W = 16.  A sweep is m-1 rounds of the round-robin tournament
+// over blocks; in a round the m/2 disjoint block pairs are processed in parallel:
+//   phase 1  one CTA per pair diagonalises the 32 x 32 sub-matrix A[I u J, I u J] in
+//            shared memory with cyclic two-sided Jacobi (relative stopping rule),
+//            accumulating Q_k; it writes Q_k and the rotated diagonal block;
+//   phase 2  every off-diagonal pair block A'[k, l] = Q_k^T A[k, l] Q_l (double
+//            buffered) and V[:, l] <- V[:, l] Q_l, spread over the whole grid.
+// Two grid barriers per round instead of one per rotation step.  Plane rotations
+// inside the pairs keep the relative accuracy of graded (scaled diagonally dominant)
+// matrices; the off-pair blocks see only orthogonal transformations.
+constexpr int BJ_W = 16, BJ_P = 32, BJ_LD = 33, BJ_VT = 64;
+struct BJParams {
+  int b, bp, m, h;
+  const double* Ain;
+  int64_t lda;
+  double* A0;
+  double* A1;
+  int64_t ld;
+  double* V;
+  double* Qb;   // h x 32 x 32, Q_k[p][l] at Qb[k*1024 + p*32 + l]
+  int* rotf;    // h flags: pair k rotated this round
+  double* lam;
+  double tol, abstol;
+  int max_sweeps, inner_sweeps;
+  unsigned* bar;
+  int* cnt;     // max_sweeps rotation counters
+  int* info;
+  unsigned long long* ts;  // optional: [0] phase 1, [1] barrier 1, [2] phase 2, [3] barrier 2 (ns, CTA 0)
+};
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ int bj_g(int l, int I, int J) { return l < BJ_W ? I * BJ_W + l : J * BJ_W + (l - BJ_W); }
+__device__ __forceinline__ void bj_pair(int k, int step, int m, int& I, int& J) {
+  int i1 = rr_index(k, step, m), i2 = rr_index(m - 1 - k, step, m);
+  I = min(i1, i2);
+  J = max(i1, i2);
+}
+
+__global__ void __launch_bounds__(256) jacobi_block_kernel(BJParams p) {
+  extern __shared__ double sh[];
+  double* S = sh;                     // 32 x 33
+  double* Q = S + BJ_P * BJ_LD;       // 32 x 33
+  double* X = Q + BJ_P * BJ_LD;       // BJ_VT x 33 (phase 2)
+  double* Y = X + BJ_VT * BJ_LD;      // BJ_VT x 33 (phase 2)
+  __shared__ double c_[BJ_W], s_[BJ_W], dA_[BJ_W], dB_[BJ_W];
+  __shared__ int pp_[BJ_W], qq_[BJ_W], act_[BJ_W];
+  __shared__ int srot;
+  __shared__ double sdmax[8];
+  const int tid = threadIdx.x, nth = blockDim.x;
+  const int64_t ld = p.ld;
+  const int bp = p.bp, b = p.b;
+  const int64_t gtid = (int64_t)blockIdx.x * nth + tid, gthreads = (int64_t)gridDim.x * nth;
+
+  {  // absolute floor relative to max |a_ii| (same in every CTA)
+    double dm = 0.0;
+    for (int i = tid; i < b; i += nth) dm = fmax(dm, fabs(p.Ain[(int64_t)i * p.lda + i]));
+    for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
+    if ((tid & 31) == 0) sdmax[tid >> 5] = dm;
+    __syncthreads();
+    dm = 0.0;
+    for (int w = 0; w < (nth >> 5); ++w) dm = fmax(dm, sdmax[w]);
+    __syncthreads();
+    if (tid == 0) sdmax[0] = dm;
+    __syncthreads();
+  }
+  const double abstol = p.abstol * sdmax[0];
+  for (int64_t e = gtid; e < (int64_t)bp * bp; e += gthreads) {
+    int i = (int)(e % bp), j = (int)(e / bp);
+    p.A0[j * ld + i] = (i < b && j < b) ? p.Ain[(int64_t)j * p.lda + i] : 0.0;
+    p.V[j * ld + i] = (i == j) ? 1.0 : 0.0;
+  }
+  for (int64_t e = gtid; e < p.max_sweeps; e += gthreads) p.cnt[e] = 0;
+  grid_barrier(p.bar);
+
+  double* cur = p.A0;
+  double* nxt = p.A1;
+  const int m = p.m, h = p.h;
+  const int vt = (int)cdiv_d(bp, BJ_VT);
+  const int nkl = h * (h - 1) / 2;
+  const int ty = tid >> 3, tx = tid & 7;  // phase-2 thread tile: rows ty (+32), cols tx + 8c
+  int sweeps = 0;
+  bool converged = false;
+  unsigned long long tacc[4] = {0, 0, 0, 0}, tq = gtimer();
+  for (int sw = 0; sw < p.max_sweeps; ++sw) {
+    for (int step = 0; step < m - 1; ++step) {
+      // ---------------- phase 1: diagonalise each pair block
+      for (int k = blockIdx.x; k < h; k += gridDim.x) {
+        int I, J;
+        bj_pair(k, step, m, I, J);
+        for (int e = tid; e < BJ_P * BJ_P; e += nth) {
+          int r = e & 31, c = e >> 5;
+          S[r * BJ_LD + c] = cur[(int64_t)bj_g(c, I, J) * ld + bj_g(r, I, J)];
+          Q[r * BJ_LD + c] = (r == c) ? 1.0 : 0.0;
+        }
+        __syncthreads();
+        int rot_total = 0;
+        for (int isw = 0; isw < p.inner_sweeps; ++isw) {
+          int rot_sw = 0;
+          for (int st = 0; st < BJ_P - 1; ++st) {
+            // rotation parameters of the 16 disjoint pairs of this step (t = tan of the
+            // angle; the standard formulas keep high relative accuracy on the diagonal)
+            if (tid < 32) {
+              int act = 0;
+              if (tid < BJ_W) {
+                int a1 = rr_index(tid, st, BJ_P), a2 = rr_index(BJ_P - 1 - tid, st, BJ_P);
+                int pq = min(a1, a2), qq = max(a1, a2);
+                double app = S[pq * BJ_LD + pq], aqq = S[qq * BJ_LD + qq], apq = S[pq * BJ_LD + qq];
+                double c = 1.0, s = 0.0;
+                if (fabs(apq) > fmax(abstol, p.tol * sqrt(fabs(app * aqq)))) {
+                  act = 1;
+                  const double zeta = aqq - app, two = 2.0 * apq;
+                  // t = 2 apq sgn(zeta) / (|zeta| + sqrt(zeta^2 + 4 apq^2))
+                  double t = (zeta >= 0.0 ? two : -two) / (fabs(zeta) + sqrt(fma(zeta, zeta, two * two)));
+                  if (!isfinite(t)) t = copysign(1.0, two);
+                  c = rsqrt(fma(t, t, 1.0));
+                  s = t * c;
+                  // exact diagonal / annihilated entries, written in pass B
+                  c_[tid] = c; s_[tid] = s;
+                  dA_[tid] = app - t * apq;
+                  dB_[tid] = aqq + t * apq;
+                }
+                pp_[tid] = pq;
+                qq_[tid] = qq;
+                act_[tid] = act;
+                if (!act) { c_[tid] = 1.0; s_[tid] = 0.0; }
+              }
+              unsigned bal = __ballot_sync(0xffffffffu, act);
+              if (tid == 0) srot = __popc(bal);
+            }
+            __syncthreads();
+            const int nrot = srot;
+            rot_sw += nrot;
+            if (nrot) {
+              // pass A: rows p, q of S (S <- J^T S) and columns p, q of Q (Q <- Q J);
+              // thread: pair k = tid / 16, index j = tid % 16 and j + 16
+              const int k = tid >> 4, j0 = tid & 15;
+              if (act_[k]) {
+                const int pk = pp_[k], qk = qq_[k];
+                const double c = c_[k], s = s_[k];
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                  const int j = j0 + 16 * h2;
+                  double xp = S[pk * BJ_LD + j], xq = S[qk * BJ_LD + j];
+                  S[pk * BJ_LD + j] = c * xp - s * xq;
+                  S[qk * BJ_LD + j] = s * xp + c * xq;
+                  double vp = Q[j * BJ_LD + pk], vq = Q[j * BJ_LD + qk];
+                  Q[j * BJ_LD + pk] = c * vp - s * vq;
+                  Q[j * BJ_LD + qk] = s * vp + c * vq;
+                }
+              }
+              __syncthreads();
+              // pass B: columns p, q of S (S <- S J); the 2x2 diagonal block of each
+              // rotated pair gets the exact values
+              if (act_[k]) {
+                const int pk = pp_[k], qk = qq_[k];
+                const double c = c_[k], s = s_[k];
+#pragma unroll
+                for (int h2 = 0; h2 < 2; ++h2) {
+                  const int j = j0 + 16 * h2;
+                  double xp = S[j * BJ_LD + pk], xq = S[j * BJ_LD + qk];
+                  double np = c * xp - s * xq, nq = s * xp + c * xq;
+                  if (j == pk) { np = dA_[k]; nq = 0.0; }
+                  if (j == qk) { np = 0.0; nq = dB_[k]; }
+                  S[j * BJ_LD + pk] = np;
+                  S[j * BJ_LD + qk] = nq;
+                }
+              }
+            }
+            __syncthreads();
+          }
+          rot_total += rot_sw;
+          if (rot_sw == 0) break;
+        }
+        // write Q_k, the flag and the rotated diagonal block
+        double* Qk = p.Qb + (int64_t)k * BJ_P * BJ_P;
+        for (int e = tid; e < BJ_P * BJ_P; e += nth) {
+          int r = e >> 5, c = e & 31;
+          Qk[r * BJ_P + c] = Q[r * BJ_LD + c];
+          nxt[(int64_t)bj_g(c, I, J) * ld + bj_g(r, I, J)] = S[r * BJ_LD + c];
+        }
+        if (tid == 0) {
+          p.rotf[k] = rot_total > 0;
+          if (rot_total) atomicAdd(&p.cnt[sw], rot_total);
+        }
+        __syncthreads();
+      }
+      { unsigned long long t = gtimer(); tacc[0] += t - tq; tq = t; }
+      grid_barrier(p.bar);
+      { unsigned long long t = gtimer(); tacc[1] += t - tq; tq = t; }
+      // ---------------- phase 2: off-diagonal pair blocks (32 x 32) and V row tiles (64 x 32)
+      for (int it = blockIdx.x; it < nkl + vt * h; it += gridDim.x) {
+        int k, l, t = -1;
+        if (it < nkl) {
+          l = (int)((sqrtf(8.0f * (float)it + 1.0f) + 1.0f) * 0.5f);
+          while (l * (l - 1) / 2 > it) --l;
+          while ((l + 1) * l / 2 <= it) ++l;
+          k = it - l * (l - 1) / 2;  // k < l
+        } else {
+          int j = it - nkl;
+          t = j % vt;
+          l = j / vt;
+          k = l;
+        }
+        int Ik, Jk, Il, Jl;
+        bj_pair(k, step, m, Ik, Jk);
+        bj_pair(l, step, m, Il, Jl);
+        const bool rk = t < 0 && p.rotf[k], rl = p.rotf[l];
+        const int rows = t < 0 ? BJ_P : min(BJ_VT, bp - t * BJ_VT);
+        if (t >= 0 && !rl) continue;  // V tile unchanged
+        const double* Qk = p.Qb + (int64_t)k * BJ_P * BJ_P;
+        const double* Ql = p.Qb + (int64_t)l * BJ_P * BJ_P;
+        for (int e = tid; e < rows * BJ_P; e += nth) {
+          int r = e % rows, c = e / rows;
+          int gc = bj_g(c, Il, Jl);
+          X[r * BJ_LD + c] = (t < 0) ? cur[(int64_t)gc * ld + bj_g(r, Ik, Jk)]
+                                     : p.V[(int64_t)gc * ld + t * BJ_VT + r];
+        }
+        for (int e = tid; e < BJ_P * BJ_P; e += nth) {
+          int r = e >> 5, c = e & 31;
+          if (rk) S[r * BJ_LD + c] = Qk[e];
+          if (rl) Q[r * BJ_LD + c] = Ql[e];
+        }
+        __syncthreads();
+        if (rk) {  // Y = Qk^T X (32 x 32)
+          double a4[4];
+#pragma unroll
+          for (int c = 0; c < 4; ++c) a4[c] = 0.0;
+          for (int q = 0; q < BJ_P; ++q) {
+            const double qa = S[q * BJ_LD + ty];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) a4[c] = fma(qa, X[q * BJ_LD + tx + 8 * c], a4[c]);
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c) Y[ty * BJ_LD + tx + 8 * c] = a4[c];
+          __syncthreads();
+          double* tmp = X; X = Y; Y = tmp;
+        }
+        // out = X Ql (or X), rows <= 64: thread rows ty, ty + 32
+        for (int r = ty; r < rows; r += 32) {
+          double a4[4];
+          if (rl) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) a4[c] = 0.0;
+            for (int q = 0; q < BJ_P; ++q) {
+              const double xa = X[r * BJ_LD + q];
+#pragma unroll
+              for (int c = 0; c < 4; ++c) a4[c] = fma(xa, Q[q * BJ_LD + tx + 8 * c], a4[c]);
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) a4[c] = X[r * BJ_LD + tx + 8 * c];
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int cc = tx + 8 * c;
+            const int gc = bj_g(cc, Il, Jl);
+            if (t < 0) {
+              const int gr = bj_g(r, Ik, Jk);
+              nxt[(int64_t)gc * ld + gr] = a4[c];
+              nxt[(int64_t)gr * ld + gc] = a4[c];
+            } else {
+              p.V[(int64_t)gc * ld + t * BJ_VT + r] = a4[c];
+            }
+          }
+        }
+        if (rk) {  // restore buffer roles
+          double* tmp = X; X = Y; Y = tmp;
+        }
+        __syncthreads();
+      }
+      { unsigned long long t = gtimer(); tacc[2] += t - tq; tq = t; }
+      grid_barrier(p.bar);
+      { unsigned long long t = gtimer(); tacc[3] += t - tq; tq = t; }
+      double* tmp = cur;
+      cur = nxt;
+      nxt = tmp;
+    }
+    ++sweeps;
+    if (*(volatile int*)(p.cnt + sw) == 0) {  // read after the barrier: identical in every CTA
+      converged = true;
+      break;
+    }
+  }
+  for (int64_t i = gtid; i < b; i += gthreads) p.lam[i] = cur[i * ld + i];
+  if (gtid == 0) {
+    p.info[0] = sweeps;
+    p.info[2] = converged ? 0 : 1;
+    if (p.ts)
+      for (int i = 0; i < 4; ++i) p.ts[i] = tacc[i];
+  }
+}
+
 // sort eigenpairs descending (ties: lower index first); one CTA computes ranks
 __global__ void rank_sort_kernel(int b, const double* lam_u, double* lam, int* perm) {
   for (int i = threadIdx.x; i < b; i += blockDim.x) {
@@ -408,6 +694,10 @@ int DenseWs::ensure(int64_t b, cudaStream_t st) {
   RH_CUDA(cudaMallocAsync((void**)&perm, (size_t)(bb + 64) * sizeof(int), st));
   RH_CUDA(cudaMallocAsync((void**)&info, 64, st));
   RH_CUDA(cudaMemsetAsync(info, 0, 64, st));
+  const int64_t hmax = cdiv(bb, 64) + 1;
+  RH_CUDA(cudaMallocAsync((void**)&Qb, (size_t)hmax * 4096 * sizeof(double), st));
+  RH_CUDA(cudaMallocAsync((void**)&rotf, (size_t)(2 * hmax + 64) * sizeof(int), st));
+  RH_CUDA(cudaMallocAsync((void**)&cnt, 256 * sizeof(int), st));
   cap_b = bb;
   return RHOSVD_OK;
 }
@@ -419,7 +709,10 @@ void DenseWs::release(cudaStream_t st) {
   if (cs) cudaFreeAsync(cs, st);
   if (perm) cudaFreeAsync(perm, st);
   if (info) cudaFreeAsync(info, st);
-  bar = nullptr; A0 = A1 = V = cs = nullptr; perm = info = nullptr;
+  if (Qb) cudaFreeAsync(Qb, st);
+  if (rotf) cudaFreeAsync(rotf, st);
+  if (cnt) cudaFreeAsync(cnt, st);
+  bar = nullptr; A0 = A1 = V = cs = Qb = nullptr; perm = info = rotf = cnt = nullptr;
   cap_b = 0;
 }
 
@@ -445,7 +738,12 @@ int syevj(int64_t b, const double* A, int64_t lda, double* lambda, double* Vout,
   jp.Ain = A; jp.lda = lda; jp.A0 = ws.A0; jp.A1 = ws.A1; jp.ld = ws.ld; jp.V = ws.V;
   jp.lam = ws.cs;  // unsorted eigenvalues staged in cs
   jp.tol = tol; jp.abstol = abstol; jp.max_sweeps = max_sweeps; jp.bar = ws.bar; jp.info = ws.info;
-  if (b <= JAC_SMEM_MAXB) {
+  static int smem_maxb = -1;
+  if (smem_maxb < 0) {
+    const char* e = getenv("RHOSVD_JAC_SMEM_MAXB");
+    smem_maxb = e ? std::max(0, std::min(atoi(e), JAC_SMEM_MAXB)) : 32;
+  }
+  if (b <= smem_maxb) {
     const int threads = 1024;
     size_t smem = (size_t)b * (b | 1) * sizeof(double) + (size_t)jp.h * (3 * sizeof(double) + 3 * sizeof(int)) + 64;
     static bool attr_s = false;
@@ -457,19 +755,54 @@ int syevj(int64_t b, const double* A, int64_t lda, double* lambda, double* Vout,
     count_launch();
     RH_LAUNCH_CHECK();
   } else {
-    const int threads = 512;
-    size_t smem = (size_t)jp.h * (3 * sizeof(double) + 3 * sizeof(int)) + 64;
-    static bool attr = false;
-    if (!attr) {
-      RH_CUDA(cudaFuncSetAttribute(jacobi_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 96 * 1024));
-      attr = true;
+    const int nb = (int)cdiv(b, BJ_W);
+    BJParams bj{};
+    bj.b = (int)b;
+    bj.m = nb + (nb & 1);
+    bj.h = bj.m / 2;
+    bj.bp = bj.m * BJ_W;
+    RH_CHECK(ws.ensure(bj.bp, st));
+    bj.Ain = A; bj.lda = lda; bj.A0 = ws.A0; bj.A1 = ws.A1; bj.ld = ws.ld; bj.V = ws.V; bj.Qb = ws.Qb;
+    bj.rotf = ws.rotf; bj.lam = ws.cs; bj.tol = tol; bj.abstol = abstol;
+    bj.max_sweeps = std::min(max_sweeps, 250);
+    {
+      static int inner = -1;
+      if (inner < 0) {
+        const char* e = getenv("RHOSVD_JAC_INNER");
+        inner = e ? std::max(1, atoi(e)) : 1;
+      }
+      bj.inner_sweeps = inner;
     }
-    int64_t items = (int64_t)jp.h * (jp.h + 1) / 2 + (int64_t)b * jp.h;
-    int64_t want = cdiv(items, threads * 4);
-    int grid = coop_grid((const void*)jacobi_kernel, threads, smem, want);
-    void* args[] = {&jp};
-    RH_CUDA(cudaLaunchCooperativeKernel((const void*)jacobi_kernel, dim3(grid), dim3(threads), args, smem, st));
+    bj.bar = ws.bar; bj.cnt = ws.cnt; bj.info = ws.info;
+    const int threads = 256;
+    const size_t smem = (size_t)(2 * BJ_P + 2 * BJ_VT) * BJ_LD * sizeof(double);
+    static bool attr_b = false;
+    if (!attr_b) {
+      RH_CUDA(cudaFuncSetAttribute(jacobi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      attr_b = true;
+    }
+    int64_t want = (int64_t)bj.h * (bj.h - 1) / 2 + cdiv(bj.bp, BJ_VT) * bj.h;
+    int grid = (int)std::min<int64_t>(coop_grid((const void*)jacobi_block_kernel, threads, smem, want), num_sms());
+    static int tsm = -1;
+    static unsigned long long* tsb = nullptr;
+    if (tsm < 0) {
+      const char* e = getenv("RHOSVD_TS");
+      tsm = (e && e[0] == '1') ? 1 : 0;
+      if (tsm) cudaMalloc(&tsb, 64 * sizeof(unsigned long long));
+    }
+    bj.ts = tsm ? tsb : nullptr;
+    void* args[] = {&bj};
+    RH_CUDA(cudaLaunchCooperativeKernel((const void*)jacobi_block_kernel, dim3(grid), dim3(threads), args, smem, st));
     count_launch();
+    if (tsm) {
+      unsigned long long h[4];
+      int inf[4];
+      cudaStreamSynchronize(st);
+      cudaMemcpy(h, tsb, sizeof(h), cudaMemcpyDeviceToHost);
+      cudaMemcpy(inf, ws.info, sizeof(inf), cudaMemcpyDeviceToHost);
+      fprintf(stderr, "[jacobi ts] b=%d m=%d grid=%d sweeps=%d: phase1 %.1f bar1 %.1f phase2 %.1f bar2 %.1f us\n",
+              (int)b, bj.m, grid, inf[0], h[0] * 1e-3, h[1] * 1e-3, h[2] * 1e-3, h[3] * 1e-3);
+    }
   }
   rank_sort_kernel<<<1, 1024, 0, st>>>((int)b, ws.cs, lambda, ws.perm);
   permute_cols_kernel<<<(unsigned)cdiv(b * b, 256), 256, 0, st>>>((int)b, ws.V, ws.ld, ws.perm, Vout, ldv);
@@ -486,198 +819,413 @@ int syevj(int64_t b, const double* A, int64_t lda, double* lambda, double* Vout,
 }
 
 // ------------------------------------------------------------------ Cholesky
+// chol_inv_scaled: Bp = D L^{-T}, D = diag(S)^{-1/2}, L = chol(D S D + shift I), as ONE
+// cooperative kernel over 64 x 64 blocks (P = ceil(b/64) block rows):
+//   panel j : every trailing block (i, k), j < k <= i, is owned by one CTA, which forms
+//             L_ij = A_ij Linv_jj^T and L_kj (64 x 64 GEMMs from shared memory) and
+//             applies A_ik -= L_ij L_kj^T; the owner of (j+1, j+1) then factors that
+//             diagonal block in shared memory and inverts it, so ONE grid barrier per
+//             panel suffices;
+//   inverse : X = L^{-1} by block diagonals d = 1..P-1 (one barrier each):
+//             X_{j+d, j} = -Linv_{j+d} sum_{k=j}^{j+d-1} L_{j+d, k} X_{k, j}.
+// A pivot below delta marks a numerically dependent column: it gets a unit pivot and
+// a zero sub-column (its tiny residual is kept; the next column-scaled pass
+// normalises it) - stable, unlike flooring the pivot.
+constexpr int CB = 64, CLD = 65;
 struct CholParams {
-  int b;
+  int b, P;
   const double* S;
   int64_t lds;
-  double shift;
-  double delta;  // pivot floor (relative to the unit scaled diagonal)
-  double* A;  // work copy, ld
-  double* Lt; // L^T (upper), ld
-  double* d;  // column scaling D
+  double shift, delta;
+  double* A;     // scaled matrix, bp x bp (ld)
+  double* L;     // lower blocks of L (ld)
+  double* X;     // L^{-1} (ld)
+  double* Linv;  // P diagonal inverses, 64 x 64 row-major each
+  unsigned* dep; // P x 2 words: dependent-column mask per panel
+  double* d;
+  double* Bp;
+  int64_t ldb;
   int64_t ld;
   unsigned* bar;
   int* info;
+  unsigned long long* ts;  // optional phase timestamps (RHOSVD_TS=1), CTA 0
 };
 
-constexpr int CW = 32;  // panel width
-
-__global__ void __launch_bounds__(256) chol_kernel(CholParams p) {
-  __shared__ double Ljj[CW][CW + 1];
-  __shared__ double Xi[CW][CW + 1];
-  __shared__ double Xk[CW][CW + 1];
-  __shared__ unsigned depmask;
-  const int b = p.b;
-  const int64_t ld = p.ld;
-  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
-  // scaling D and A = D S D + shift I, Lt = 0
-  for (int64_t i = gtid; i < b; i += gthreads) {
-    double sii = p.S[i * p.lds + i];
-    p.d[i] = sii > 0.0 ? 1.0 / sqrt(sii) : 1.0;
-  }
-  grid_barrier(p.bar);
-  for (int64_t e = gtid; e < (int64_t)b * b; e += gthreads) {
-    int i = (int)(e % b), j = (int)(e / b);
-    double v = p.S[j * p.lds + i] * p.d[i] * p.d[j];
-    if (i == j) v += p.shift;
-    p.A[j * ld + i] = v;
-    p.Lt[j * ld + i] = 0.0;
-  }
-  grid_barrier(p.bar);
-  const int nb = (b + CW - 1) / CW;
-  const int tid = threadIdx.x;
-  for (int J = 0; J < nb; ++J) {
-    const int j0 = J * CW, w = min(CW, b - j0);
-    // every CTA: factor the diagonal block and invert it
-    for (int e = tid; e < CW * CW; e += blockDim.x) {
-      int r = e % CW, c = e / CW;
-      Ljj[r][c] = (r < w && c < w && c <= r) ? p.A[(j0 + c) * ld + j0 + r] : 0.0;
-    }
-    __syncthreads();
-    if (tid < 32) {
-      const int lane = tid;
-      unsigned dep = 0u;
-      for (int c = 0; c < w; ++c) {
-        double dcc = Ljj[c][c];
-        // A pivot below delta means column c is numerically dependent on the
-        // previous ones: give it a unit pivot and a zero sub-column, i.e. keep
-        // the (tiny) residual of that column as is.  The next column-scaled
-        // CholQR pass normalises it.  Stable, unlike flooring the pivot.
-        const bool d = !(dcc > p.delta);
-        __syncwarp();
-        if (d) {
-          if (lane == 0 && blockIdx.x == 0) atomicOr(p.info + 1, 1);
-          dep |= 1u << c;
-          if (lane == c) Ljj[c][c] = 1.0;
-          if (lane > c && lane < w) Ljj[lane][c] = 0.0;
-          __syncwarp();
-          continue;
-        }
-        double piv = sqrt(dcc);
-        if (lane == c) Ljj[c][c] = piv;
-        if (lane > c && lane < w) Ljj[lane][c] /= piv;
-        __syncwarp();
-        if (lane > c && lane < w) {
-          double lic = Ljj[lane][c];
-          for (int k = c + 1; k <= lane; ++k) Ljj[lane][k] -= lic * Ljj[k][c];
-        }
-        __syncwarp();
-      }
-      if (lane == 0) depmask = dep;
-    }
-    __syncthreads();
-    if (blockIdx.x == 0) {
-      for (int e = tid; e < w * w; e += blockDim.x) {
-        int r = e % w, c = e / w;  // L(j0+r, j0+c)
-        if (c <= r) p.Lt[(int64_t)(j0 + r) * ld + j0 + c] = Ljj[r][c];
-      }
-    }
-    // trailing blocks (I, K), J < K <= I < nb
-    const int t = nb - J - 1;
-    const int64_t nblocks = (int64_t)t * (t + 1) / 2;
-    for (int64_t q = blockIdx.x; q < nblocks; q += gridDim.x) {
-      int I = (int)((sqrt(8.0 * (double)q + 1.0) - 1.0) * 0.5);
-      while ((int64_t)(I + 1) * (I + 2) / 2 <= q) ++I;
-      while ((int64_t)I * (I + 1) / 2 > q) --I;
-      int K = (int)(q - (int64_t)I * (I + 1) / 2);  // K <= I (relative)
-      I += J + 1;
-      K += J + 1;
-      const int i0 = I * CW, wi = min(CW, b - i0), k0 = K * CW, wk = min(CW, b - k0);
-      __syncthreads();
-      // L_Ij = A_Ij Inv^T ; L_Kj = A_Kj Inv^T
-      for (int e = tid; e < CW * CW; e += blockDim.x) {
-        int r = e % CW, c = e / CW;
-        double a = 0.0, ak = 0.0;
-        if (r < wi && c < w) a = p.A[(int64_t)(j0 + c) * ld + i0 + r];
-        if (r < wk && c < w) ak = p.A[(int64_t)(j0 + c) * ld + k0 + r];
-        Xi[r][c] = a;
-        Xk[r][c] = ak;
-      }
-      __syncthreads();
-      // forward substitution L_Ij Ljj^T = A_Ij (and L_Kj), dependent columns zero
-      if (tid < 2 * CW) {
-        double(*X)[CW + 1] = tid < CW ? Xi : Xk;
-        const int r = tid & (CW - 1);
-        const int wr = tid < CW ? wi : wk;
-        if (r < wr) {
-          for (int cc = 0; cc < w; ++cc) {
-            if (depmask & (1u << cc)) {
-              X[r][cc] = 0.0;
-              continue;
-            }
-            double v = X[r][cc];
-            for (int k = 0; k < cc; ++k) v -= X[r][k] * Ljj[cc][k];
-            X[r][cc] = v / Ljj[cc][cc];
-          }
-        }
-      }
-      __syncthreads();
-      if (I == K) {  // owner writes the panel block of L (as L^T)
-        for (int e = tid; e < wi * w; e += blockDim.x) {
-          int r = e % wi, c = e / wi;
-          p.Lt[(int64_t)(i0 + r) * ld + j0 + c] = Xi[r][c];
-        }
-      }
-      // A_IK -= L_Ij L_Kj^T (lower part of diagonal blocks only is needed; do all)
-      for (int e = tid; e < wi * wk; e += blockDim.x) {
-        int r = e % wi, c = e / wi;
-        double s = 0.0;
-        for (int k = 0; k < w; ++k) s = fma(Xi[r][k], Xk[c][k], s);
-        p.A[(int64_t)(k0 + c) * ld + i0 + r] -= s;
-      }
-    }
-    grid_barrier(p.bar);
+__device__ __forceinline__ void stamp(unsigned long long* ts, int i) {
+  if (ts && blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    ts[i] = t;
   }
 }
 
-// warp per column of L^{-1}; Bp(c, i) = d_c * Linv(i, c)
-__global__ void trinv_kernel(int b, const double* Lt, int64_t ld, const double* d, double* Bp, int64_t ldb) {
-  extern __shared__ double xs[];
-  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  const int c = blockIdx.x * (blockDim.x >> 5) + wib;
-  if (c >= b) return;
-  double* x = xs + (int64_t)wib * b;
-  const double dc = d[c];
-  for (int i = lane; i < c; i += 32) Bp[(int64_t)i * ldb + c] = 0.0;
-  if (lane == 0) x[c] = 1.0 / Lt[(int64_t)c * ld + c];
-  __syncwarp();
-  for (int i = c + 1; i < b; ++i) {
-    const double* Li = Lt + (int64_t)i * ld;  // row i of L
-    double s = 0.0;
-    for (int k = c + lane; k < i; k += 32) s = fma(Li[k], x[k], s);
-    s = warp_sum(s);
-    if (lane == 0) x[i] = -s / Li[i];
-    __syncwarp();
+// acc[a][c] (+)= sum_q A(r, q) B(q, cc), r = ty + 16 a, cc = tx + 16 c, 64 x 64 x 64 in smem
+template <bool AT, bool BT>
+__device__ __forceinline__ void mm64(const double* A, const double* B, double acc[4][4], int ty, int tx) {
+#pragma unroll 4
+  for (int q = 0; q < CB; ++q) {
+    double av[4], bv[4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a) {
+      const int r = ty + 16 * a;
+      av[a] = AT ? A[q * CLD + r] : A[r * CLD + q];
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      const int cc = tx + 16 * c;
+      bv[c] = BT ? B[cc * CLD + q] : B[q * CLD + cc];
+    }
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int c = 0; c < 4; ++c) acc[a][c] = fma(av[a], bv[c], acc[a][c]);
   }
-  for (int i = c + lane; i < b; i += 32) Bp[(int64_t)i * ldb + c] = dc * x[i];
+}
+__device__ __forceinline__ void zero44(double acc[4][4]) {
+#pragma unroll
+  for (int a = 0; a < 4; ++a)
+#pragma unroll
+    for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
+}
+// global col-major block (I, J) of M (ld) <-> smem [r][c] (pitch CLD)
+__device__ __forceinline__ void ld_blk(double* sm, const double* M, int64_t ld, int I, int J) {
+  for (int e = threadIdx.x; e < CB * CB; e += blockDim.x) {
+    int r = e & 63, c = e >> 6;
+    sm[r * CLD + c] = M[(int64_t)(J * CB + c) * ld + I * CB + r];
+  }
+}
+
+// ---- warp-level 32 x 32 building blocks (lane i holds row i in registers; all loops
+// fully unrolled so every register index is static)
+// Cholesky of the lower triangle of T (pitch CLD) in place; returns the dependent-
+// column mask (pivot <= delta, or c >= wvalid: unit pivot, zero sub-column).
+__device__ __forceinline__ unsigned warp_chol32(double* T, double delta, int wvalid) {
+  const int lane = threadIdx.x & 31;
+  double a[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) a[k] = (k <= lane) ? T[lane * CLD + k] : 0.0;
+  unsigned dep = 0u;
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const double d = __shfl_sync(0xffffffffu, a[c], c);
+    if (c >= wvalid || !(d > delta)) {  // warp-uniform
+      dep |= 1u << c;
+      if (lane > c) a[c] = 0.0;
+      if (lane == c) a[c] = 1.0;
+      continue;
+    }
+    const double piv = sqrt(d), rp = 1.0 / piv;
+    if (lane > c) a[c] *= rp;
+    if (lane == c) a[c] = piv;
+#pragma unroll
+    for (int k = c + 1; k < 32; ++k) {
+      const double lkc = __shfl_sync(0xffffffffu, a[c], k);
+      if (lane >= k) a[k] = fma(-a[c], lkc, a[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 32; ++k) T[lane * CLD + k] = (k <= lane) ? a[k] : 0.0;
+  __syncwarp();
+  return dep;
+}
+// X = L^{-1} (both 32 x 32 lower, pitch CLD); lane j computes column j
+__device__ __forceinline__ void warp_inv32(const double* L, double* X) {
+  const int lane = threadIdx.x & 31;
+  const double rdl = 1.0 / L[lane * CLD + lane];
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    double s = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) s = fma(-L[i * CLD + k], x[k], s);
+    const double rd = __shfl_sync(0xffffffffu, rdl, i);
+    x[i] = (i >= lane) ? s * rd : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) X[i * CLD + lane] = x[i];
+  __syncwarp();
+}
+// C(32 x 32, 4 outputs per thread: row tid/8, cols tid%8 + 8q) = sum_k A(r, k) B'(c, k)
+// with B' = B (BT) or B^T
+template <bool BT>
+__device__ __forceinline__ void mm32(const double* A, const double* B, double acc[4]) {
+  const int r = threadIdx.x >> 3, c0 = threadIdx.x & 7;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[q] = 0.0;
+#pragma unroll 8
+  for (int k = 0; k < 32; ++k) {
+    const double av = A[r * CLD + k];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int c = c0 + 8 * q;
+      acc[q] = fma(av, BT ? B[c * CLD + k] : B[k * CLD + c], acc[q]);
+    }
+  }
+}
+
+// Factor the (already updated) diagonal block in sm (64 x 64, lower used) in place into
+// L_jj as 2 x 2 blocks of 32 (warp-level Cholesky / inverse of the diagonal halves,
+// CTA-wide 32^3 products for the off-diagonal half), write L_jj to L, its inverse to
+// Linv[j] and X, and the dependent-column mask.
+__device__ void chol_diag_block(double* sm, double* inv, const CholParams& p, int j) {
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int w = min(CB, p.b - j * CB);
+  const int r = tid >> 3, c0 = tid & 7;
+  __shared__ unsigned depw[2];
+  double* A11 = sm;
+  double* A21 = sm + 32 * CLD;
+  double* A22 = sm + 32 * CLD + 32;
+  double* I11 = inv;
+  double* I21 = inv + 32 * CLD;
+  double* I12 = inv + 32;  // scratch, zero at the end
+  double* I22 = inv + 32 * CLD + 32;
+  double acc[4];
+  if (warp == 0) {
+    unsigned d1 = warp_chol32(A11, p.delta, min(w, 32));
+    warp_inv32(A11, I11);
+    if ((tid & 31) == 0) depw[0] = d1;
+  }
+  __syncthreads();
+  const unsigned d1 = depw[0];
+  // L21 = A21 L11^{-T} (dependent columns of the first half zero)
+  mm32<true>(A21, I11, acc);
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int c = c0 + 8 * q;
+    A21[r * CLD + c] = ((d1 >> c) & 1u) ? 0.0 : acc[q];
+  }
+  __syncthreads();
+  // A22 -= L21 L21^T
+  mm32<true>(A21, A21, acc);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) A22[r * CLD + c0 + 8 * q] -= acc[q];
+  __syncthreads();
+  if (warp == 0) {
+    unsigned d2 = warp_chol32(A22, p.delta, max(0, min(w - 32, 32)));
+    warp_inv32(A22, I22);
+    if ((tid & 31) == 0) depw[1] = d2;
+  }
+  __syncthreads();
+  // Linv21 = -L22^{-1} L21 L11^{-1}
+  mm32<false>(A21, I11, acc);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) I12[r * CLD + c0 + 8 * q] = acc[q];
+  __syncthreads();
+  mm32<false>(I22, I12, acc);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) I21[r * CLD + c0 + 8 * q] = -acc[q];
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    I12[r * CLD + c0 + 8 * q] = 0.0;
+    sm[r * CLD + 32 + c0 + 8 * q] = 0.0;  // upper-right of L
+  }
+  __syncthreads();
+  const unsigned long long dep = (unsigned long long)depw[0] | ((unsigned long long)depw[1] << 32);
+  const unsigned long long valid = (w >= 64) ? ~0ull : ((1ull << w) - 1ull);
+  if (tid == 0 && (dep & valid)) atomicOr(p.info + 1, 1);
+  double* Lg = p.Linv + (int64_t)j * CB * CB;
+  for (int e = tid; e < CB * CB; e += blockDim.x) {
+    int rr = e >> 6, c = e & 63;
+    Lg[rr * CB + c] = inv[rr * CLD + c];
+    p.L[(int64_t)(j * CB + c) * p.ld + j * CB + rr] = sm[rr * CLD + c];
+    p.X[(int64_t)(j * CB + c) * p.ld + j * CB + rr] = inv[rr * CLD + c];
+  }
+  if (tid == 0) {
+    p.dep[2 * j] = (unsigned)(dep & 0xffffffffu);
+    p.dep[2 * j + 1] = (unsigned)(dep >> 32);
+  }
+  __syncthreads();
+}
+
+__global__ void __launch_bounds__(256) chol_blk_kernel(CholParams p) {
+  extern __shared__ double sh[];
+  double* s0 = sh;
+  double* s1 = s0 + CB * CLD;
+  double* s2 = s1 + CB * CLD;
+  const int tid = threadIdx.x;
+  const int ty = tid >> 4, tx = tid & 15;
+  const int b = p.b, P = p.P, bp = P * CB;
+  const int64_t ld = p.ld;
+  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + tid, gthreads = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = gtid; i < bp; i += gthreads) {
+    double sii = i < b ? p.S[i * p.lds + i] : 1.0;
+    p.d[i] = sii > 0.0 ? 1.0 / sqrt(sii) : 1.0;
+  }
+  grid_barrier(p.bar);
+  for (int64_t e = gtid; e < (int64_t)bp * bp; e += gthreads) {
+    int i = (int)(e % bp), j = (int)(e / bp);
+    double v = 0.0;
+    if (i < b && j < b) v = p.S[(int64_t)j * p.lds + i] * p.d[i] * p.d[j];
+    if (i == j) v += (i < b) ? p.shift : 1.0;
+    p.A[(int64_t)j * ld + i] = v;
+    p.L[(int64_t)j * ld + i] = 0.0;
+    p.X[(int64_t)j * ld + i] = 0.0;
+  }
+  grid_barrier(p.bar);
+  stamp(p.ts, 0);
+  if (blockIdx.x == 0) {
+    ld_blk(s0, p.A, ld, 0, 0);
+    __syncthreads();
+    chol_diag_block(s0, s1, p, 0);
+  }
+  stamp(p.ts, 1);
+  grid_barrier(p.bar);
+  stamp(p.ts, 2);
+  double acc[4][4];
+  for (int j = 0; j + 1 < P; ++j) {
+    const int t = P - j - 1;
+    const int nitems = t * (t + 1) / 2;
+    const unsigned long long dm = ((unsigned long long)p.dep[2 * j + 1] << 32) | p.dep[2 * j];
+    for (int q = blockIdx.x; q < nitems; q += gridDim.x) {
+      int I = (int)((sqrtf(8.0f * (float)q + 1.0f) - 1.0f) * 0.5f);
+      while ((I + 1) * (I + 2) / 2 <= q) ++I;
+      while (I * (I + 1) / 2 > q) --I;
+      int K = q - I * (I + 1) / 2;
+      I += j + 1;
+      K += j + 1;
+      // s2 = Linv_jj ; s0 = L_Ij = A_Ij Linv^T ; s1 = L_Kj
+      {
+        const double* Lg = p.Linv + (int64_t)j * CB * CB;
+        for (int e = tid; e < CB * CB; e += blockDim.x) s2[(e >> 6) * CLD + (e & 63)] = Lg[e];
+      }
+      ld_blk(s0, p.A, ld, I, j);
+      if (K != I) ld_blk(s1, p.A, ld, K, j);
+      __syncthreads();
+      zero44(acc);
+      mm64<false, true>(s0, s2, acc, ty, tx);
+      double acc2[4][4];
+      if (K != I) {
+        zero44(acc2);
+        mm64<false, true>(s1, s2, acc2, ty, tx);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int cc = tx + 16 * c;
+          const bool z = (dm >> cc) & 1ull;
+          s0[(ty + 16 * a) * CLD + cc] = z ? 0.0 : acc[a][c];
+          if (K != I) s1[(ty + 16 * a) * CLD + cc] = z ? 0.0 : acc2[a][c];
+        }
+      __syncthreads();
+      const double* LK = (K != I) ? s1 : s0;
+      if (K == j + 1) {  // the owner of (I, j+1) publishes L_Ij
+        for (int e = tid; e < CB * CB; e += blockDim.x) {
+          int r = e & 63, c = e >> 6;
+          p.L[(int64_t)(j * CB + c) * ld + I * CB + r] = s0[r * CLD + c];
+        }
+      }
+      // A_IK -= L_Ij L_Kj^T
+      zero44(acc);
+      mm64<false, true>(s0, LK, acc, ty, tx);
+      if (I == j + 1 && K == j + 1) {
+        // next diagonal block: update in smem, then factor it right here
+        __syncthreads();
+        ld_blk(s2, p.A, ld, I, K);
+        __syncthreads();
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) s2[(ty + 16 * a) * CLD + tx + 16 * c] -= acc[a][c];
+        __syncthreads();
+        chol_diag_block(s2, s1, p, j + 1);
+      } else {
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int r = ty + 16 * a, cc = tx + 16 * c;
+            p.A[(int64_t)(K * CB + cc) * ld + I * CB + r] -= acc[a][c];
+          }
+      }
+      __syncthreads();
+    }
+    grid_barrier(p.bar);
+    stamp(p.ts, 3 + j);
+  }
+  // ---------------- X = L^{-1} by block diagonals
+  for (int dd = 1; dd < P; ++dd) {
+    for (int j = blockIdx.x; j + dd < P; j += gridDim.x) {
+      const int i = j + dd;
+      zero44(acc);
+      for (int k = j; k < i; ++k) {
+        __syncthreads();
+        ld_blk(s0, p.L, ld, i, k);
+        ld_blk(s1, p.X, ld, k, j);
+        __syncthreads();
+        mm64<false, false>(s0, s1, acc, ty, tx);
+      }
+      __syncthreads();
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) s1[(ty + 16 * a) * CLD + tx + 16 * c] = acc[a][c];
+      {
+        const double* Lg = p.Linv + (int64_t)i * CB * CB;
+        for (int e = tid; e < CB * CB; e += blockDim.x) s2[(e >> 6) * CLD + (e & 63)] = Lg[e];
+      }
+      __syncthreads();
+      zero44(acc);
+      mm64<false, false>(s2, s1, acc, ty, tx);
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          const int r = ty + 16 * a, cc = tx + 16 * c;
+          p.X[(int64_t)(j * CB + cc) * ld + i * CB + r] = -acc[a][c];
+        }
+    }
+    grid_barrier(p.bar);
+    stamp(p.ts, 3 + P + dd);
+  }
+  // ---------------- Bp(c, i) = d_c X(i, c)
+  for (int64_t e = gtid; e < (int64_t)b * b; e += gthreads) {
+    int c = (int)(e % b), i = (int)(e / b);
+    p.Bp[(int64_t)i * p.ldb + c] = (i >= c) ? p.d[c] * p.X[(int64_t)c * ld + i] : 0.0;
+  }
 }
 
 int chol_inv_scaled(int64_t b, const double* S, int64_t lds, double shift_rel, double* Bp, int64_t ldb,
                     DenseWs& ws, cudaStream_t st) {
   if (b <= 0) return RHOSVD_OK;
-  RH_CHECK(ws.ensure(b, st));
+  const int P = (int)cdiv(b, CB);
+  RH_CHECK(ws.ensure((int64_t)P * CB, st));
   CholParams cp{};
-  cp.b = (int)b; cp.S = S; cp.lds = lds; cp.shift = shift_rel; cp.A = ws.A0; cp.Lt = ws.A1;
-  cp.d = ws.cs; cp.ld = ws.ld; cp.bar = ws.bar; cp.info = ws.info;
-  cp.delta = 1e-13;
+  cp.b = (int)b; cp.P = P; cp.S = S; cp.lds = lds; cp.shift = shift_rel; cp.delta = 1e-13;
+  cp.A = ws.A0; cp.L = ws.A1; cp.X = ws.V; cp.Linv = ws.Qb; cp.dep = (unsigned*)ws.rotf; cp.d = ws.cs;
+  cp.Bp = Bp; cp.ldb = ldb; cp.ld = ws.ld; cp.bar = ws.bar; cp.info = ws.info;
   const int threads = 256;
-  int nbk = (int)cdiv(b, CW);
-  int64_t want = std::max<int64_t>(1, (int64_t)(nbk - 1) * nbk / 2);
-  if (b <= 64) want = 1;
-  int grid = coop_grid((const void*)chol_kernel, threads, 0, want);
-  void* args[] = {&cp};
-  RH_CUDA(cudaLaunchCooperativeKernel((const void*)chol_kernel, dim3(grid), dim3(threads), args, 0, st));
-  const int wpb = 4;
-  size_t smem = (size_t)wpb * b * sizeof(double);
-  static int attr_b = 0;
-  if ((int)smem > 48 * 1024 && attr_b < (int)smem) {
-    RH_CUDA(cudaFuncSetAttribute(trinv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr_b = (int)smem;
+  const size_t smem = (size_t)3 * CB * CLD * sizeof(double);
+  static bool attr = false;
+  if (!attr) {
+    RH_CUDA(cudaFuncSetAttribute(chol_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = true;
   }
-  trinv_kernel<<<(unsigned)cdiv(b, wpb), 32 * wpb, smem, st>>>((int)b, ws.A1, ws.ld, ws.cs, Bp, ldb);
-  count_launch(2);
+  int64_t want = std::max<int64_t>(1, (int64_t)(P - 1) * P / 2);
+  int grid = coop_grid((const void*)chol_blk_kernel, threads, smem, want);
+  static int tsmode = -1;
+  static unsigned long long* tsbuf = nullptr;
+  if (tsmode < 0) {
+    const char* e = getenv("RHOSVD_TS");
+    tsmode = (e && e[0] == '1') ? 1 : 0;
+    if (tsmode) cudaMalloc(&tsbuf, 1024 * sizeof(unsigned long long));
+  }
+  cp.ts = tsmode ? tsbuf : nullptr;
+  void* args[] = {&cp};
+  RH_CUDA(cudaLaunchCooperativeKernel((const void*)chol_blk_kernel, dim3(grid), dim3(threads), args, smem, st));
+  count_launch();
   RH_LAUNCH_CHECK();
+  if (tsmode) {
+    unsigned long long h[256];
+    cudaStreamSynchronize(st);
+    cudaMemcpy(h, tsbuf, sizeof(h), cudaMemcpyDeviceToHost);
+    fprintf(stderr, "[chol ts] b=%d P=%d grid=%d:", (int)b, P, grid);
+    for (int i = 1; i < 3 + 2 * P - 1; ++i) fprintf(stderr, " %.1f", (h[i] - h[0]) * 1e-3);
+    fprintf(stderr, " us\n");
+  }
   return RHOSVD_OK;
 }
 

@@ -13,6 +13,9 @@ struct DenseWs {
   double* cs = nullptr;     // per-pair rotation params (unused: computed in smem)
   int* perm = nullptr;      // sort permutation
   int* info = nullptr;      // [0] sweeps, [1] not-PD flag, [2] spare
+  double* Qb = nullptr;     // block Jacobi: per-pair 64 x 64 rotations
+  int* rotf = nullptr;      // block Jacobi: per-pair rotated flags
+  int* cnt = nullptr;       // block Jacobi: per-sweep rotation counters
   int64_t cap_b = 0, ld = 0;
   int ensure(int64_t b, cudaStream_t st);
   void release(cudaStream_t st);

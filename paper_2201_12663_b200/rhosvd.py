@@ -82,6 +82,7 @@ def lib():
         "rhosvd_dgemm": (C.c_int, [C.c_char, C.c_char, I64, I64, I64, D, P, I64, P, I64, D, P, I64, P]),
         "rhosvd_syevj": (C.c_int, [I64, P, I64, P, P, I64, D, C.POINTER(I32), P]),
         "rhosvd_core": (C.c_int, [P, P, P, I64, P, I64, I64, I64, I64, P, P]),
+        "rhosvd_chol_inv": (C.c_int, [I64, P, I64, D, P, I64, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -95,7 +96,8 @@ EXPORTED = ["rhosvd_opts_default", "rhosvd_c2t", "rhosvd_result_ranks", "rhosvd_
             "rhosvd_result_sigma", "rhosvd_result_core", "rhosvd_result_cpfactor",
             "rhosvd_result_report", "rhosvd_result_free", "rhosvd_last_error", "rhosvd_version",
             "rhosvd_nccl_get_unique_id", "rhosvd_comm_init_nccl", "rhosvd_comm_init_callback",
-            "rhosvd_comm_destroy", "rhosvd_gram", "rhosvd_dgemm", "rhosvd_syevj", "rhosvd_core"]
+            "rhosvd_comm_destroy", "rhosvd_gram", "rhosvd_dgemm", "rhosvd_syevj", "rhosvd_core",
+            "rhosvd_chol_inv"]
 
 
 def _check(status):
@@ -387,6 +389,17 @@ def syevj(S, tol=1e-15, stream=None):
     sw = C.c_int32()
     _check(lib().rhosvd_syevj(b, _ptr(A), b, _ptr(lam), _ptr(V), b, tol, C.byref(sw), _stream_ptr(stream)))
     return lam, V.t(), int(sw.value)  # V col-major -> columns are eigenvectors
+
+
+def chol_inv(S, shift=0.0, stream=None):
+    """Bp = D L^{-T}, D = diag(S)^{-1/2}, L = chol(D S D + shift I) (S symmetric, CUDA f64)."""
+    import torch
+    _need_cuda_f64(S, "S")
+    b = S.shape[0]
+    Sc = S.t().contiguous()
+    Bp = torch.empty(b, b, dtype=torch.float64, device=S.device)
+    _check(lib().rhosvd_chol_inv(b, _ptr(Sc), b, float(shift), _ptr(Bp), b, _stream_ptr(stream)))
+    return Bp.t()  # col-major buffer -> row-major view
 
 
 def core(W1, W2, W3, xi, stream=None):

@@ -51,7 +51,7 @@ def test_gram_deterministic(rh):
     assert torch.equal(G1, G2)
 
 
-@pytest.mark.parametrize("b", [1, 2, 3, 16, 33, 97, 150, 300])
+@pytest.mark.parametrize("b", [1, 2, 3, 16, 33, 97, 150, 161, 300, 707])
 def test_syevj_random(rh, b):
     rng = np.random.default_rng(b)
     A = rng.normal(size=(b, b))
@@ -68,7 +68,7 @@ def test_syevj_random(rh, b):
     assert np.max(np.abs(A @ V - V * lam[None, :])) <= 1e-13 * b * nrm
 
 
-@pytest.mark.parametrize("b", [20, 130, 400])
+@pytest.mark.parametrize("b", [20, 130, 400, 715])
 def test_syevj_graded_high_relative_accuracy(rh, b):
     """D A D with A well conditioned, D graded over 12 decades: Jacobi with the
     relative stopping rule resolves even the smallest eigenvalues to high
@@ -103,3 +103,33 @@ def test_core(rh, r, R):
     beta = rh.core(dev(W[0]), dev(W[1]), dev(W[2]), dev(xi)).cpu().numpy()
     ref = core_kr(W[0], W[1], W[2], xi)
     assert np.max(np.abs(beta - ref)) <= 1e-13 * np.sqrt(R) * np.max(np.abs(ref)) * 8
+
+
+@pytest.mark.parametrize("b", [1, 5, 64, 65, 130, 298, 707])
+def test_chol_inv(rh, b):
+    """Bp = D L^{-T} (scaled Cholesky inverse) against LAPACK; Q = M Bp orthonormal."""
+    rng = np.random.default_rng(b + 11)
+    M = rng.normal(size=(3 * b + 7, b)) * np.logspace(0, -3, b)[None, :]
+    S = M.T @ M
+    Bp = rh.chol_inv(dev(S)).cpu().numpy()
+    d = 1.0 / np.sqrt(np.diag(S))
+    L = np.linalg.cholesky(d[:, None] * S * d[None, :])
+    ref = d[:, None] * np.linalg.inv(L).T
+    assert np.max(np.abs(Bp - ref)) <= 1e-11 * np.max(np.abs(ref))
+    Q = M @ Bp
+    assert np.max(np.abs(Q.T @ Q - np.eye(b))) <= 1e-12
+
+
+def test_chol_inv_dependent_column(rh):
+    """A numerically dependent column gets a unit pivot and a zero sub-column: the
+    remaining columns stay orthonormal and no NaN appears."""
+    rng = np.random.default_rng(5)
+    M = rng.normal(size=(300, 100))
+    M[:, 40] = M[:, 3] + 1e-9 * M[:, 40]
+    S = M.T @ M
+    Bp = rh.chol_inv(dev(S)).cpu().numpy()
+    assert np.all(np.isfinite(Bp))
+    Q = M @ Bp
+    keep = [i for i in range(100) if i != 40]
+    G = Q[:, keep].T @ Q[:, keep]
+    assert np.max(np.abs(G - np.eye(99))) <= 1e-8

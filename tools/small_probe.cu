@@ -1,0 +1,80 @@
+// small_probe.cu - single-CTA timing of the b x b building blocks (clock64 cycles).
+#include "../paper_2201_12663_b200/csrc/small_dense.cu"
+
+namespace rhosvd {
+thread_local std::string g_err;
+thread_local int g_launches = 0;
+int fail(int s, const std::string& m) { g_err = m; return s; }
+void set_error(const std::string& m) { g_err = m; }
+int num_sms() { return 148; }
+}
+using namespace rhosvd;
+
+__global__ void probe(double* g, long long* out) {
+  extern __shared__ double sh[];
+  double* s0 = sh;
+  double* s1 = s0 + CB * CLD;
+  double* s2 = s1 + CB * CLD;
+  const int tid = threadIdx.x;
+  for (int e = tid; e < CB * CB; e += blockDim.x) {
+    int r = e >> 6, c = e & 63;
+    double v = g[e];
+    s0[r * CLD + c] = v; s1[r * CLD + c] = v; s2[r * CLD + c] = v;
+  }
+  __syncthreads();
+  long long t0, t1;
+  // (a) warp_chol32
+  for (int e = tid; e < 32 * 32; e += blockDim.x) { int r = e >> 5, c = e & 31; s0[r * CLD + c] = (r == c) ? 40.0 : 0.5 + 0.01 * ((r * 7 + c * 3) % 13); }
+  __syncthreads();
+  t0 = clock64();
+  if (tid < 32) warp_chol32(s0, 1e-13, 32);
+  __syncthreads();
+  t1 = clock64();
+  if (tid == 0) out[0] = t1 - t0;
+  t0 = clock64();
+  if (tid < 32) warp_inv32(s0, s1);
+  __syncthreads();
+  t1 = clock64();
+  if (tid == 0) out[1] = t1 - t0;
+  double acc[4];
+  t0 = clock64();
+  mm32<true>(s0, s1, acc);
+  __syncthreads();
+  t1 = clock64();
+  if (tid == 0) out[2] = t1 - t0;
+  double a44[4][4];
+  zero44(a44);
+  t0 = clock64();
+  mm64<false, true>(s0, s2, a44, tid >> 4, tid & 15);
+  __syncthreads();
+  t1 = clock64();
+  if (tid == 0) out[3] = t1 - t0;
+  double sum = 0;
+  for (int a = 0; a < 4; ++a) for (int c = 0; c < 4; ++c) sum += a44[a][c] + acc[a];
+  if (sum == 1234.5) out[9] = 1;
+  // (e) sqrt + div chain
+  double x = 2.0 + tid;
+  t0 = clock64();
+  for (int i = 0; i < 32; ++i) { x = sqrt(x) + 1.0; x = 1.0 / x + 2.0; }
+  t1 = clock64();
+  if (tid == 0) out[4] = t1 - t0;
+  if (x == 1234.5) out[9] = 2;
+}
+
+int main() {
+  double* g; long long* o;
+  cudaMalloc(&g, 4096 * 8); cudaMalloc(&o, 16 * 8);
+  double h[4096];
+  for (int i = 0; i < 4096; ++i) h[i] = (i % 64 == i / 64) ? 64.0 : 0.01 * (i % 17);
+  cudaMemcpy(g, h, sizeof(h), cudaMemcpyHostToDevice);
+  size_t smem = 3 * CB * CLD * 8;
+  cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  for (int rep = 0; rep < 3; ++rep) {
+    probe<<<1, 256, smem>>>(g, o);
+    long long ho[16];
+    cudaMemcpy(ho, o, sizeof(ho), cudaMemcpyDeviceToHost);
+    printf("chol32 %lld  inv32 %lld  mm32 %lld  mm64 %lld  32x(sqrt+div) %lld cycles\n", ho[0], ho[1], ho[2], ho[3], ho[4]);
+  }
+  printf("%s\n", cudaGetErrorString(cudaGetLastError()));
+  return 0;
+}
