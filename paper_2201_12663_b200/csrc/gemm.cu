@@ -1,231 +1,215 @@
-// gemm.cu - FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) GEMM engine for sm_100a.
+// gemm.cu - FP64 tensor-core (DMMA, mma.sync.m8n8k4.f64) GEMM engine for sm_100a, TMA-fed.
 //
-// sm_100a has no FP64 tcgen05 kind (ptxas rejects kind::f64), so
-// the FP64 tensor path is the warp-synchronous mma.sync.m8n8k4 (SASS
-// DMMA.8x8x4) with register accumulators.  Operand tiles are staged in shared
-// memory by a STAGES-deep cp.async pipeline; smem row pitches are padded so
-// every fragment load is two 128-byte wavefronts (conflict-free):
-//   m/n-contiguous tile  T[k][m], pitch BM+8 (== 8 mod 16 doubles)
-//   k-contiguous  tile   T[m][k], pitch BK+4 (== 4 mod 16 doubles)
-// Split-K writes fixed-order partials that a reduce kernel sums in order, so
+// sm_100a has no FP64 tcgen05 kind (ptxas rejects kind::f64), so the FP64
+// tensor path is the warp-synchronous mma.sync.m8n8k4 (SASS DMMA.8x8x4) with register
+// accumulators.  Operand tiles move global -> shared by TMA (cp.async.bulk.tensor.2d)
+// into a STAGES-deep ring guarded by full/empty mbarriers; thread 0 issues the copies
+// (refilling the stage the 8 warps released one step earlier), so the ring stays
+// STAGES-1 k-slabs ahead.  Two operand layouts, both conflict-free for the 8x4 / 4x8
+// fragment loads:
+//   k-contiguous  (X[row * ld + k]) : box {16, rows}, 128-B swizzle -> [rows][16]
+//   m-contiguous  (X[k * ld + row]) : box {rows + 8, 16}, no swizzle -> [16][rows + 8]
+//                 (pitch == 8 mod 16 doubles; the 8 extra rows are the next tile's)
+// The grid is persistent (one CTA per SM, static stride over work items = tiles x
+// K-splits).  Split-K writes fixed-order partials that a second kernel sums in order:
 // results are bitwise reproducible (no FP64 atomics).
+#include <algorithm>
+
 #include "gemm.cuh"
+#include "tma.cuh"
 
 namespace rhosvd {
 
-struct KParams {
+constexpr int GBK = 16, GTHREADS = 256;
+
+struct GParams {
   int M, N, K;
-  const double* A;
-  int64_t lda;
-  const double* B;
-  int64_t ldb;
   double* C;
   int64_t ldc;
   double alpha, beta;
   const double* cs;
   const double* rs;
-  int upper;      // compute only tiles tm <= tn
+  int upper;      // compute only tiles tm <= tn, mirror
   int epi;
   const double* D;
   int64_t ldd;
-  double* part;   // split-K partials [split][N][M] (col-major, ld M) or residual per-CTA sums
-  int splits;
-  int kchunk;     // K per split (multiple of BK)
-  int tiles_m, tiles_n;
+  double* part;   // split-K partials [split][N][M] (col-major, ld M) or residual per-item sums
+  int splits, kchunk;
+  int tiles_m, tiles_n, tiles, items;
+  int stages;
+  uint32_t a_bytes, stage_bytes, tx_bytes;
 };
 
-template <int BM, int BN, int BK, int WM, int WN, bool AK, bool BKM, int STAGES>
-struct GemmCfg {
-  static constexpr int WARPS_M = BM / WM, WARPS_N = BN / WN;
-  static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
-  static constexpr int FM = WM / 8, FN = WN / 8;
-  // A tile: AK ? [BM][BK+4] : [BK][BM+8]
-  static constexpr int A_ROWS = AK ? BM : BK, A_PITCH = AK ? BK + 4 : BM + 8;
-  static constexpr int B_ROWS = BKM ? BN : BK, B_PITCH = BKM ? BK + 4 : BN + 8;
-  static constexpr int A_STAGE = A_ROWS * A_PITCH, B_STAGE = B_ROWS * B_PITCH;
-  static constexpr size_t SMEM = size_t(STAGES) * (A_STAGE + B_STAGE) * sizeof(double);
-};
+template <int BM, int BN, bool AK, bool BKM>
+__global__ void __launch_bounds__(GTHREADS, 1)
+    tma_gemm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB, const GParams p) {
+  constexpr int WM = BM / 2, WN = BN / 4, FM = WM / 8, FN = WN / 8;
+  constexpr int APITCH = BM + 8, BPITCH = BN + 8;  // doubles, m/n-contiguous layouts
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  unsigned char* ring = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint64_t* full = (uint64_t*)(ring + (size_t)p.stages * p.stage_bytes);
+  uint64_t* empty = full + p.stages;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const bool producer = (tid == 0);
 
-template <int BM, int BN, int BK, int WM, int WN, bool AK, bool BKM, int STAGES>
-__global__ void __launch_bounds__(GemmCfg<BM, BN, BK, WM, WN, AK, BKM, STAGES>::THREADS)
-    dmma_gemm_kernel(KParams p) {
-  using Cfg = GemmCfg<BM, BN, BK, WM, WN, AK, BKM, STAGES>;
-  extern __shared__ __align__(16) double smem[];
-  double* As = smem;
-  double* Bs = smem + STAGES * Cfg::A_STAGE;
-
-  // ---- tile coordinates
-  int tile = blockIdx.x, tm, tn;
-  if (p.upper) {
-    // enumerate upper-triangular tiles (tm <= tn) column by column
-    tn = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
-    while ((tn + 1) * (tn + 2) / 2 <= tile) ++tn;
-    while (tn * (tn + 1) / 2 > tile) --tn;
-    tm = tile - tn * (tn + 1) / 2;
-  } else {
-    tm = tile % p.tiles_m;
-    tn = tile / p.tiles_m;
-  }
-  const int m0 = tm * BM, n0 = tn * BN;
-  const int split = blockIdx.y;
-  const int kbeg = split * p.kchunk;
-  const int kend = min(p.K, kbeg + p.kchunk);
-  const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
-
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm0 = (warp % Cfg::WARPS_M) * WM, wn0 = (warp / Cfg::WARPS_M) * WN;
-
-  auto load_tile = [&](int stage, int kt) {
-    const int k0 = kbeg + kt * BK;
-    double* as = As + stage * Cfg::A_STAGE;
-    double* bs = Bs + stage * Cfg::B_STAGE;
-    // A
-    if (AK) {
-      constexpr int CPR = BK / 2, TOT = BM * CPR;
-      for (int c = tid; c < TOT; c += Cfg::THREADS) {
-        int r = c / CPR, cc = (c % CPR) * 2;
-        int gm = m0 + r, gk = k0 + cc;
-        int nb = (gm < p.M) ? max(0, min(2, kend - gk)) : 0;
-        const double* src = nb ? p.A + (int64_t)gm * p.lda + gk : p.A;
-        cp_async16(as + r * Cfg::A_PITCH + cc, src, nb * 8);
-      }
+  auto tile_of = [&](int tile, int& tm, int& tn) {
+    if (p.upper) {
+      tn = (int)((sqrtf(8.0f * tile + 1.0f) - 1.0f) * 0.5f);
+      while ((tn + 1) * (tn + 2) / 2 <= tile) ++tn;
+      while (tn * (tn + 1) / 2 > tile) --tn;
+      tm = tile - tn * (tn + 1) / 2;
     } else {
-      constexpr int CPR = BM / 2, TOT = BK * CPR;
-      for (int c = tid; c < TOT; c += Cfg::THREADS) {
-        int r = c / CPR, cc = (c % CPR) * 2;
-        int gk = k0 + r, gm = m0 + cc;
-        int nb = (gk < kend) ? max(0, min(2, p.M - gm)) : 0;
-        const double* src = nb ? p.A + (int64_t)gk * p.lda + gm : p.A;
-        cp_async16(as + r * Cfg::A_PITCH + cc, src, nb * 8);
-      }
-    }
-    // B
-    if (BKM) {
-      constexpr int CPR = BK / 2, TOT = BN * CPR;
-      for (int c = tid; c < TOT; c += Cfg::THREADS) {
-        int r = c / CPR, cc = (c % CPR) * 2;
-        int gn = n0 + r, gk = k0 + cc;
-        int nb = (gn < p.N) ? max(0, min(2, kend - gk)) : 0;
-        const double* src = nb ? p.B + (int64_t)gn * p.ldb + gk : p.B;
-        cp_async16(bs + r * Cfg::B_PITCH + cc, src, nb * 8);
-      }
-    } else {
-      constexpr int CPR = BN / 2, TOT = BK * CPR;
-      for (int c = tid; c < TOT; c += Cfg::THREADS) {
-        int r = c / CPR, cc = (c % CPR) * 2;
-        int gk = k0 + r, gn = n0 + cc;
-        int nb = (gk < kend) ? max(0, min(2, p.N - gn)) : 0;
-        const double* src = nb ? p.B + (int64_t)gk * p.ldb + gn : p.B;
-        cp_async16(bs + r * Cfg::B_PITCH + cc, src, nb * 8);
-      }
+      tm = tile % p.tiles_m;
+      tn = tile / p.tiles_m;
     }
   };
-
-  double acc[Cfg::FM][Cfg::FN][2];
-#pragma unroll
-  for (int i = 0; i < Cfg::FM; ++i)
-#pragma unroll
-    for (int j = 0; j < Cfg::FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-
-#pragma unroll
-  for (int s = 0; s < STAGES - 1; ++s) {
-    if (s < nk) load_tile(s, s);
-    cp_async_commit();
+  // producer cursor over this CTA's k-slab stream
+  int pit = blockIdx.x, pk = 0, pkend = 0, pm = 0, pn = 0;
+  auto set_item = [&]() {
+    if (pit >= p.items) return;
+    const int split = pit / p.tiles;
+    int tm, tn;
+    tile_of(pit % p.tiles, tm, tn);
+    pm = tm * BM;
+    pn = tn * BN;
+    pk = split * p.kchunk;
+    pkend = min(p.K, pk + p.kchunk);
+  };
+  auto issue_next = [&](int stage) {
+    if (pit >= p.items) return;
+    unsigned char* st = ring + (size_t)stage * p.stage_bytes;
+    mbar_arrive_expect_tx(&full[stage], p.tx_bytes);
+    if (AK) tma_load_2d(st, &tA, pk, pm, &full[stage]);
+    else tma_load_2d(st, &tA, pm, pk, &full[stage]);
+    if (BKM) tma_load_2d(st + p.a_bytes, &tB, pk, pn, &full[stage]);
+    else tma_load_2d(st + p.a_bytes, &tB, pn, pk, &full[stage]);
+    pk += GBK;
+    if (pk >= pkend) {
+      pit += gridDim.x;
+      set_item();
+    }
+  };
+  if (producer) {
+    for (int s = 0; s < p.stages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], GTHREADS / 32);
+    }
+    fence_mbar_init();
+    tma_prefetch_desc(&tA);
+    tma_prefetch_desc(&tB);
+  }
+  __syncthreads();
+  if (producer) {
+    set_item();
+    for (int s = 0; s < p.stages; ++s) issue_next(s);
   }
 
   const int fr = lane >> 2, fc = lane & 3;
-  for (int kt = 0; kt < nk; ++kt) {
-    cp_async_wait<STAGES - 2>();
-    __syncthreads();
-    {
-      int nx = kt + STAGES - 1;
-      if (nx < nk) load_tile(nx % STAGES, nx);
-      cp_async_commit();
-    }
-    const double* as = As + (kt % STAGES) * Cfg::A_STAGE;
-    const double* bs = Bs + (kt % STAGES) * Cfg::B_STAGE;
+  const int wm0 = (warp & 1) * WM, wn0 = (warp >> 1) * WN;
+  // per-lane byte offsets of the fragment element (row % 8 == fr, k = 4 q + fc)
+  uint32_t aoff[GBK / 4], boff[GBK / 4];
 #pragma unroll
-    for (int kk = 0; kk < BK; kk += 4) {
-      double af[Cfg::FM], bf[Cfg::FN];
-#pragma unroll
-      for (int i = 0; i < Cfg::FM; ++i) {
-        int m = wm0 + i * 8 + fr, k = kk + fc;
-        af[i] = AK ? as[m * Cfg::A_PITCH + k] : as[k * Cfg::A_PITCH + m];
-      }
-#pragma unroll
-      for (int j = 0; j < Cfg::FN; ++j) {
-        int n = wn0 + j * 8 + fr, k = kk + fc;
-        bf[j] = BKM ? bs[n * Cfg::B_PITCH + k] : bs[k * Cfg::B_PITCH + n];
-      }
-#pragma unroll
-      for (int i = 0; i < Cfg::FM; ++i)
-#pragma unroll
-        for (int j = 0; j < Cfg::FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
-    }
+  for (int q = 0; q < GBK / 4; ++q) {
+    const int k = 4 * q + fc;
+    aoff[q] = AK ? (uint32_t)((wm0 + fr) * 128) + sw128_off(fr, k) - fr * 128
+                 : (uint32_t)((k * APITCH + wm0 + fr) * 8);
+    boff[q] = BKM ? (uint32_t)((wn0 + fr) * 128) + sw128_off(fr, k) - fr * 128
+                  : (uint32_t)((k * BPITCH + wn0 + fr) * 8);
   }
-  cp_async_wait<0>();
+  constexpr uint32_t ASTEP = AK ? 1024u : 64u, BSTEP = BKM ? 1024u : 64u;  // next 8 rows
+  const uint32_t ring_s = smem_u32(ring);
+  uint32_t g = 0;
+  for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
+    const int split = it / p.tiles;
+    int tm, tn;
+    tile_of(it % p.tiles, tm, tn);
+    const int m0 = tm * BM, n0 = tn * BN;
+    const int kbeg = split * p.kchunk, kend = min(p.K, kbeg + p.kchunk);
+    double acc[FM][FN][2];
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    for (int k0 = kbeg; k0 < kend; k0 += GBK, ++g) {
+      if (producer && g >= 1) {
+        const uint32_t gp = g - 1, sp = gp % p.stages;
+        mbar_wait(&empty[sp], (gp / p.stages) & 1);
+        issue_next((int)sp);
+      }
+      const uint32_t s = g % p.stages;
+      mbar_wait(&full[s], (g / p.stages) & 1);
+      const uint32_t sa = ring_s + s * p.stage_bytes, sb = sa + p.a_bytes;
+#pragma unroll
+      for (int q = 0; q < GBK / 4; ++q) {
+        double af[FM], bf[FN];
+#pragma unroll
+        for (int i = 0; i < FM; ++i) af[i] = lds_f64(sa + aoff[q] + i * ASTEP);
+#pragma unroll
+        for (int j = 0; j < FN; ++j) bf[j] = lds_f64(sb + boff[q] + j * BSTEP);
+#pragma unroll
+        for (int i = 0; i < FM; ++i)
+#pragma unroll
+          for (int j = 0; j < FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
 
-  // ---- epilogue
-  if (p.epi == EPI_RESID) {
-    double ss = 0.0;
+    // ---- epilogue
+    if (p.epi == EPI_RESID) {
+      double ss = 0.0;
 #pragma unroll
-    for (int i = 0; i < Cfg::FM; ++i)
+      for (int i = 0; i < FM; ++i)
 #pragma unroll
-      for (int j = 0; j < Cfg::FN; ++j)
+        for (int j = 0; j < FN; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            int m = m0 + wm0 + i * 8 + fr, n = n0 + wn0 + j * 8 + 2 * fc + h;
+            if (m < p.M && n < p.N) {
+              double e = p.D[(int64_t)n * p.ldd + m] - acc[i][j][h];
+              ss = fma(e, e, ss);
+            }
+          }
+      ss = warp_sum(ss);
+      // per-warp partials in fixed slots; summed in fixed order by sum_fixed_order_kernel
+      if (lane == 0) p.part[(int64_t)it * (GTHREADS / 32) + warp] = ss;
+      continue;
+    }
+    if (p.splits > 1) {
+      double* out = p.part + (int64_t)split * p.M * p.N;
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            int m = m0 + wm0 + i * 8 + fr, n = n0 + wn0 + j * 8 + 2 * fc + h;
+            if (m < p.M && n < p.N) out[(int64_t)n * p.M + m] = acc[i][j][h];
+          }
+      continue;
+    }
+#pragma unroll
+    for (int i = 0; i < FM; ++i)
+#pragma unroll
+      for (int j = 0; j < FN; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           int m = m0 + wm0 + i * 8 + fr, n = n0 + wn0 + j * 8 + 2 * fc + h;
-          if (m < p.M && n < p.N) {
-            double e = p.D[(int64_t)n * p.ldd + m] - acc[i][j][h];
-            ss = fma(e, e, ss);
+          if (m < p.M && n < p.N && (!p.upper || m <= n)) {
+            double v = p.alpha * acc[i][j][h];
+            if (p.cs) v *= p.cs[n];
+            if (p.rs) v *= p.rs[m];
+            double* c = p.C + (int64_t)n * p.ldc + m;
+            if (p.beta != 0.0) v = fma(p.beta, *c, v);
+            *c = v;
+            if (p.upper && m < n) p.C[(int64_t)m * p.ldc + n] = v;  // mirror (M == N)
           }
         }
-    ss = warp_sum(ss);
-    __syncthreads();
-    double* red = smem;
-    if (lane == 0) red[warp] = ss;
-    __syncthreads();
-    if (tid == 0) {
-      double t = 0.0;
-      for (int w = 0; w < Cfg::THREADS / 32; ++w) t += red[w];
-      p.part[blockIdx.y * gridDim.x + blockIdx.x] = t;
-    }
-    return;
   }
-  if (p.splits > 1) {
-    double* out = p.part + (int64_t)split * p.M * p.N;
-#pragma unroll
-    for (int i = 0; i < Cfg::FM; ++i)
-#pragma unroll
-      for (int j = 0; j < Cfg::FN; ++j)
-#pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          int m = m0 + wm0 + i * 8 + fr, n = n0 + wn0 + j * 8 + 2 * fc + h;
-          if (m < p.M && n < p.N) out[(int64_t)n * p.M + m] = acc[i][j][h];
-        }
-    return;
-  }
-#pragma unroll
-  for (int i = 0; i < Cfg::FM; ++i)
-#pragma unroll
-    for (int j = 0; j < Cfg::FN; ++j)
-#pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        int m = m0 + wm0 + i * 8 + fr, n = n0 + wn0 + j * 8 + 2 * fc + h;
-        if (m < p.M && n < p.N && (!p.upper || m <= n)) {
-          double v = p.alpha * acc[i][j][h];
-          if (p.cs) v *= p.cs[n];
-          if (p.rs) v *= p.rs[m];
-          double* c = p.C + (int64_t)n * p.ldc + m;
-          if (p.beta != 0.0) v = fma(p.beta, *c, v);
-          *c = v;
-          if (p.upper && m < n) p.C[(int64_t)m * p.ldc + n] = v;  // mirror (M == N)
-        }
-      }
 }
 
 // Fixed-order split-K reduction + epilogue (and symmetric mirror).
-__global__ void splitk_reduce_kernel(KParams p) {
+__global__ void splitk_reduce_kernel(GParams p) {
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t total = (int64_t)p.M * p.N;
   if (idx >= total) return;
@@ -278,28 +262,40 @@ void Scratch::release(cudaStream_t st) {
   cap = 0;
 }
 
-template <int BM, int BN, int BK, int WM, int WN, bool AK, bool BKM, int STAGES>
-static int launch_cfg(KParams kp, int ntiles, cudaStream_t st) {
-  using Cfg = GemmCfg<BM, BN, BK, WM, WN, AK, BKM, STAGES>;
-  auto kern = dmma_gemm_kernel<BM, BN, BK, WM, WN, AK, BKM, STAGES>;
+template <int BM, int BN, bool AK, bool BKM>
+static int launch_cfg(const GemmArgs& g, GParams gp, cudaStream_t st) {
+  auto kern = tma_gemm_kernel<BM, BN, AK, BKM>;
+  CUtensorMap tA, tB;
+  if (AK) RH_CHECK(make_tmap_2d(&tA, g.A, g.M, g.K, g.lda, GBK, BM, true));
+  else RH_CHECK(make_tmap_2d(&tA, g.A, g.K, g.M, g.lda, BM + 8, GBK, false));
+  if (BKM) RH_CHECK(make_tmap_2d(&tB, g.B, g.N, g.K, g.ldb, GBK, BN, true));
+  else RH_CHECK(make_tmap_2d(&tB, g.B, g.K, g.N, g.ldb, BN + 8, GBK, false));
+  const uint32_t a_box = AK ? BM * 128u : (BM + 8) * GBK * 8u;
+  const uint32_t b_box = BKM ? BN * 128u : (BN + 8) * GBK * 8u;
+  gp.a_bytes = (uint32_t)round_up(a_box, 1024);
+  gp.stage_bytes = gp.a_bytes + (uint32_t)round_up(b_box, 1024);
+  gp.tx_bytes = a_box + b_box;
+  const size_t budget = 227 * 1024 - 1024 - 256;
+  gp.stages = (int)std::min<size_t>(8, budget / gp.stage_bytes);
+  const size_t smem = 1024 + (size_t)gp.stages * gp.stage_bytes + 2 * gp.stages * sizeof(uint64_t);
   static bool attr_set = false;  // per instantiation
   if (!attr_set) {
-    RH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM));
+    RH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set = true;
   }
-  dim3 grid(ntiles, kp.splits);
-  kern<<<grid, Cfg::THREADS, Cfg::SMEM, st>>>(kp);
+  const int grid = (int)std::min<int64_t>(gp.items, num_sms());
+  kern<<<grid, GTHREADS, smem, st>>>(tA, tB, gp);
   count_launch();
   RH_LAUNCH_CHECK();
   return RHOSVD_OK;
 }
 
-template <int BM, int BN, int BK, int WM, int WN, int STAGES>
-static int launch_layout(bool ak, bool bk, KParams kp, int ntiles, cudaStream_t st) {
-  if (ak && bk) return launch_cfg<BM, BN, BK, WM, WN, true, true, STAGES>(kp, ntiles, st);
-  if (ak && !bk) return launch_cfg<BM, BN, BK, WM, WN, true, false, STAGES>(kp, ntiles, st);
-  if (!ak && bk) return launch_cfg<BM, BN, BK, WM, WN, false, true, STAGES>(kp, ntiles, st);
-  return launch_cfg<BM, BN, BK, WM, WN, false, false, STAGES>(kp, ntiles, st);
+template <int BM, int BN>
+static int launch_layout(const GemmArgs& g, const GParams& gp, cudaStream_t st) {
+  if (g.a_k && g.b_k) return launch_cfg<BM, BN, true, true>(g, gp, st);
+  if (g.a_k && !g.b_k) return launch_cfg<BM, BN, true, false>(g, gp, st);
+  if (!g.a_k && g.b_k) return launch_cfg<BM, BN, false, true>(g, gp, st);
+  return launch_cfg<BM, BN, false, false>(g, gp, st);
 }
 
 int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
@@ -307,54 +303,69 @@ int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
   if (g.M > INT32_MAX || g.N > INT32_MAX || g.K > INT32_MAX)
     return fail(RHOSVD_EINVAL, "gemm: dimension exceeds int32");
   if (g.upper_sym && g.M != g.N) return fail(RHOSVD_EINVAL, "gemm: upper_sym needs M == N");
-  KParams kp{};
-  kp.M = (int)g.M; kp.N = (int)g.N; kp.K = (int)g.K;
-  kp.A = g.A; kp.lda = g.lda; kp.B = g.B; kp.ldb = g.ldb; kp.C = g.C; kp.ldc = g.ldc;
-  kp.alpha = g.alpha; kp.beta = g.beta; kp.cs = g.col_scale; kp.rs = g.row_scale;
-  kp.upper = g.upper_sym ? 1 : 0; kp.epi = g.epi; kp.D = g.D; kp.ldd = g.ldd;
+  if (g.epi == EPI_RESID && g.K <= 0) return fail(RHOSVD_EINVAL, "gemm: residual needs K > 0");
+  GParams gp{};
+  gp.M = (int)g.M; gp.N = (int)g.N; gp.K = (int)std::max<int64_t>(g.K, 0);
+  gp.C = g.C; gp.ldc = g.ldc; gp.alpha = g.alpha; gp.beta = g.beta; gp.cs = g.col_scale; gp.rs = g.row_scale;
+  gp.upper = g.upper_sym ? 1 : 0; gp.epi = g.epi; gp.D = g.D; gp.ldd = g.ldd;
 
-  // tile choice: big tiles when there is enough output to fill the GPU
+  // tile choice: 128 x 128 when there is enough output to fill the GPU
   const int sms = num_sms();
-  const bool big = (cdiv(g.M, 128) * cdiv(g.N, 128) >= sms) ||
-                   (g.M >= 128 && g.N >= 128 && g.K >= 2048);
-  const int BT = big ? 128 : 64, BK = 16;
-  int tm = (int)cdiv(g.M, BT), tn = (int)cdiv(g.N, BT);
-  int ntiles = g.upper_sym ? tn * (tn + 1) / 2 : tm * tn;
-  kp.tiles_m = tm; kp.tiles_n = tn;
+  const bool big = (cdiv(g.M, 128) * cdiv(g.N, 128) >= sms / 2) || (g.M >= 128 && g.N >= 128 && g.K >= 2048);
+  const int BT = big ? 128 : 64;
+  const int tm = (int)cdiv(g.M, BT), tn = (int)cdiv(g.N, BT);
+  gp.tiles_m = tm;
+  gp.tiles_n = tn;
+  gp.tiles = g.upper_sym ? tn * (tn + 1) / 2 : tm * tn;
 
   int splits = g.splits;
   if (g.epi == EPI_RESID) splits = 1;
   if (splits <= 0) {
-    // enough CTAs for ~2 waves, each split >= 512 of K
-    int64_t want = cdiv(2LL * sms, ntiles);
-    int64_t maxs = std::max<int64_t>(1, g.K / 512);
-    splits = (int)std::max<int64_t>(1, std::min<int64_t>(want, maxs));
-    if (splits > 64) splits = 64;
+    // persistent grid: enough work items for every SM (~2 items each), splits >= 256 of K
+    splits = 1;
+    if (gp.tiles < sms) {
+      int64_t want = cdiv(2LL * sms, gp.tiles);
+      int64_t maxs = std::max<int64_t>(1, g.K / 256);
+      splits = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(want, maxs), 64));
+    }
   }
-  int kchunk = (int)round_up(cdiv(std::max<int64_t>(g.K, 1), splits), BK);
+  int kchunk = (int)round_up(cdiv(std::max<int64_t>(g.K, 1), splits), GBK);
   splits = (int)std::max<int64_t>(1, cdiv(std::max<int64_t>(g.K, 1), kchunk));
-  kp.splits = splits;
-  kp.kchunk = kchunk;
+  gp.splits = splits;
+  gp.kchunk = kchunk;
+  gp.items = gp.tiles * splits;
 
   if (g.epi == EPI_RESID) {
-    RH_CHECK(scr.ensure((size_t)ntiles, st));
-    kp.part = scr.ptr;
+    RH_CHECK(scr.ensure((size_t)gp.items * (GTHREADS / 32), st));
+    gp.part = scr.ptr;
   } else if (splits > 1) {
     RH_CHECK(scr.ensure((size_t)splits * g.M * g.N, st));
-    kp.part = scr.ptr;
+    gp.part = scr.ptr;
+  }
+  if (g.K <= 0) {  // empty contraction: C = beta C
+    GParams z = gp;
+    z.splits = 1;
+    if (!scr.ensure((size_t)g.M * g.N, st)) {
+      RH_CUDA(cudaMemsetAsync(scr.ptr, 0, (size_t)g.M * g.N * sizeof(double), st));
+      z.part = scr.ptr;
+      splitk_reduce_kernel<<<(unsigned)cdiv(g.M * g.N, 256), 256, 0, st>>>(z);
+      count_launch();
+      RH_LAUNCH_CHECK();
+    }
+    return RHOSVD_OK;
   }
   if (big)
-    RH_CHECK((launch_layout<128, 128, 16, 64, 32, 3>(g.a_k, g.b_k, kp, ntiles, st)));
+    RH_CHECK((launch_layout<128, 128>(g, gp, st)));
   else
-    RH_CHECK((launch_layout<64, 64, 16, 32, 32, 3>(g.a_k, g.b_k, kp, ntiles, st)));
+    RH_CHECK((launch_layout<64, 64>(g, gp, st)));
 
   if (g.epi == EPI_RESID) {
-    sum_fixed_order_kernel<<<1, 256, 0, st>>>(kp.part, ntiles, g.resid_out);
+    sum_fixed_order_kernel<<<1, 256, 0, st>>>(gp.part, gp.items * (GTHREADS / 32), g.resid_out);
     count_launch();
     RH_LAUNCH_CHECK();
   } else if (splits > 1) {
     int64_t total = g.M * g.N;
-    splitk_reduce_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(kp);
+    splitk_reduce_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(gp);
     count_launch();
     RH_LAUNCH_CHECK();
   }

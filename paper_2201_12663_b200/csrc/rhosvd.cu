@@ -259,24 +259,33 @@ static int cholqr_pass(Ctx& c, int64_t n, int64_t b, int64_t ldn, const double* 
 }
 // orthonormalize M (n x b) into Z: shifted CholQR (robust to rank deficiency) + CholQR2.
 // buffers: in -> out, uses tmp.
+// Orthonormalisation flavours:
+//   ORTH_CQR2     CholeskyQR2 (two passes): orthonormal to ~u for well conditioned input
+//   ORTH_SCQR3    shifted CholeskyQR3 (Fukaya et al.): robust to kappa up to ~u^{-1}
+//   ORTH_CQR1     one pass: a well conditioned (not exactly orthonormal) basis - enough
+//                 inside the subspace iteration, whose next step re-orthonormalises
+//   ORTH_SCQR1    one shifted pass: the same for badly conditioned input (restarts)
+enum { ORTH_CQR2 = 0, ORTH_SCQR3 = 1, ORTH_CQR1 = 2, ORTH_SCQR1 = 3 };
 static int orth(Ctx& c, int64_t n, int64_t b, int64_t ldn, const double* in, double* out, double* tmp,
-                int64_t ldb_small, bool shifted) {
+                int64_t ldb_small, int kind) {
   const double u = 1.1102230246251565e-16;
-  if (shifted) {
-    // shifted CholeskyQR (Fukaya et al.): s = 11 (n b + b(b+1)) u ||X||_2^2, ||X||_2^2 <= b
-    // for the column-scaled X
-    double shift = 11.0 * ((double)n * b + (double)b * (b + 1)) * u * (double)b;
-    RH_CHECK(cholqr_pass(c, n, b, ldn, in, tmp, shift, ldb_small));
-    RH_CHECK(cholqr_pass(c, n, b, ldn, tmp, out, 0.0, ldb_small));
-    RH_CHECK(cholqr_pass(c, n, b, ldn, out, tmp, 0.0, ldb_small));
-  } else {
-    RH_CHECK(cholqr_pass(c, n, b, ldn, in, tmp, 0.0, ldb_small));
-    RH_CHECK(cholqr_pass(c, n, b, ldn, tmp, out, 0.0, ldb_small));
-    return RHOSVD_OK;
+  // shift s = 11 (n b + b(b+1)) u ||X||_2^2 with ||X||_2^2 <= b for the column-scaled X
+  const double shift = 11.0 * ((double)n * b + (double)b * (b + 1)) * u * (double)b;
+  switch (kind) {
+    case ORTH_CQR1:
+      return cholqr_pass(c, n, b, ldn, in, out, 0.0, ldb_small);
+    case ORTH_SCQR1:
+      return cholqr_pass(c, n, b, ldn, in, out, shift, ldb_small);
+    case ORTH_CQR2:
+      RH_CHECK(cholqr_pass(c, n, b, ldn, in, tmp, 0.0, ldb_small));
+      return cholqr_pass(c, n, b, ldn, tmp, out, 0.0, ldb_small);
+    default:
+      RH_CHECK(cholqr_pass(c, n, b, ldn, in, tmp, shift, ldb_small));
+      RH_CHECK(cholqr_pass(c, n, b, ldn, tmp, out, 0.0, ldb_small));
+      RH_CHECK(cholqr_pass(c, n, b, ldn, out, tmp, 0.0, ldb_small));
+      RH_CUDA(cudaMemcpyAsync(out, tmp, (size_t)ldn * b * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
+      return RHOSVD_OK;
   }
-  // result in tmp -> copy to out
-  RH_CUDA(cudaMemcpyAsync(out, tmp, (size_t)ldn * b * sizeof(double), cudaMemcpyDeviceToDevice, c.st));
-  return RHOSVD_OK;
 }
 
 struct ModeOut {
@@ -322,7 +331,7 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
   RH_CHECK(ensure_b(b));
   uint64_t seed = o.seed * 0x9E3779B97F4A7C15ull + (uint64_t)(mode + 1) * 0xD1B54A32D192ED03ull;
   RH_CHECK(k_random(w.M.p, LDN, n, 0, b, seed, st));
-  RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldbs(b), true));
+  RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldbs(b), ORTH_SCQR3));
 
   // ---------------- subspace (simultaneous) iteration Z <- CholQR(G Z), block growth.
   // CholQR keeps leading spans, so span(z_1..z_j) converges to the dominant j-space for
@@ -366,8 +375,10 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     ++itb;
     RH_CHECK(mm(c, n, b, n, G, LDN, false, w.Z.p, LDN, true, w.Y.p, LDN));
     RH_CHECK(k_coldot(w.Z.p, w.Y.p, LDN, n, b, w.th.p, st));
-    // the first steps after a (re)start see badly conditioned G Z: shifted CholQR3
-    RH_CHECK(orth(c, n, b, LDN, w.Y.p, w.Z.p, w.T1.p, ldbs(b), itb <= 2));
+    // the first steps after a (re)start see badly conditioned G Z: shifted CholQR3.
+    // (One-pass variants leave Z not orthonormal enough for the rank/rate estimates
+    // taken from d_k = z_k^T G z_k.)
+    RH_CHECK(orth(c, n, b, LDN, w.Y.p, w.Z.p, w.T1.p, ldbs(b), itb <= 2 ? ORTH_SCQR3 : ORTH_CQR2));
     dbg_check(st, "it Z=orth(GZ)", w.Z.p, n, b, LDN);
     if (b >= m) break;  // full space: exact after one step
     if (itb < 2) continue;
@@ -441,7 +452,7 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     // M = Uhat W^T (summed over the R shards), Z <- CholQR2(M)
     RH_CHECK(mm(c, n, b, Rl, Uh, LDN, false, w.W.p, Rp, true, w.M.p, LDN));
     RH_CHECK(allreduce(c, w.M.p, LDN * b));
-    RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldb, false));
+    RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldb, ORTH_CQR2));
     ++mo.refines;
     c.tm->mark(PH_RR);
   }

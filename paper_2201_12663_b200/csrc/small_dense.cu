@@ -914,9 +914,9 @@ __device__ __forceinline__ unsigned warp_chol32(double* T, double delta, int wva
       if (lane == c) a[c] = 1.0;
       continue;
     }
-    const double piv = sqrt(d), rp = 1.0 / piv;
+    const double rp = rsqrt(d);  // one MUFU + Newton: shorter chain than sqrt + divide
     if (lane > c) a[c] *= rp;
-    if (lane == c) a[c] = piv;
+    if (lane == c) a[c] = d * rp;
 #pragma unroll
     for (int k = c + 1; k < 32; ++k) {
       const double lkc = __shfl_sync(0xffffffffu, a[c], k);

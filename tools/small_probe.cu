@@ -52,6 +52,21 @@ __global__ void probe(double* g, long long* out) {
   double sum = 0;
   for (int a = 0; a < 4; ++a) for (int c = 0; c < 4; ++c) sum += a44[a][c] + acc[a];
   if (sum == 1234.5) out[9] = 1;
+  // (f) full 64 x 64 diagonal block (warp-level halves + 32^3 products)
+  for (int e = tid; e < CB * CB; e += blockDim.x) {
+    int r = e >> 6, c = e & 63;
+    s0[r * CLD + c] = (r == c) ? 64.0 : 0.01 * ((r * 7 + c * 3) % 13);
+  }
+  __syncthreads();
+  {
+    CholParams cp{};
+    cp.b = 64; cp.P = 1; cp.delta = 1e-13; cp.Linv = g + 8192; cp.L = g + 16384; cp.X = g + 24576;
+    cp.ld = 64; cp.dep = (unsigned*)(g + 40000); cp.info = (int*)(g + 40010);
+    t0 = clock64();
+    chol_diag_block(s0, s1, cp, 0);
+    t1 = clock64();
+    if (tid == 0) out[5] = t1 - t0;
+  }
   // (e) sqrt + div chain
   double x = 2.0 + tid;
   t0 = clock64();
@@ -63,7 +78,7 @@ __global__ void probe(double* g, long long* out) {
 
 int main() {
   double* g; long long* o;
-  cudaMalloc(&g, 4096 * 8); cudaMalloc(&o, 16 * 8);
+  cudaMalloc(&g, 65536 * 8); cudaMalloc(&o, 16 * 8);
   double h[4096];
   for (int i = 0; i < 4096; ++i) h[i] = (i % 64 == i / 64) ? 64.0 : 0.01 * (i % 17);
   cudaMemcpy(g, h, sizeof(h), cudaMemcpyHostToDevice);
@@ -73,7 +88,7 @@ int main() {
     probe<<<1, 256, smem>>>(g, o);
     long long ho[16];
     cudaMemcpy(ho, o, sizeof(ho), cudaMemcpyDeviceToHost);
-    printf("chol32 %lld  inv32 %lld  mm32 %lld  mm64 %lld  32x(sqrt+div) %lld cycles\n", ho[0], ho[1], ho[2], ho[3], ho[4]);
+    printf("chol32 %lld  inv32 %lld  mm32 %lld  mm64 %lld  32x(sqrt+div) %lld  diag64 %lld cycles\n", ho[0], ho[1], ho[2], ho[3], ho[4], ho[5]);
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
