@@ -387,7 +387,10 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     RH_CUDA(cudaStreamSynchronize(st));
     if (epsmode) r_est = predict_r(d_h, b);
     if (epsmode && r_est + p > b && guard < 12) {
+      // grow towards the predicted size, at most 2x per event (the log-linear tail
+      // extrapolation of a small block overshoots: 128 -> r_est 1093 on cfg 4)
       int64_t bn = std::min<int64_t>(m, std::min<int64_t>(2 * b, std::max<int64_t>((int64_t)(1.15 * r_est) + p, b + p)));
+      if (dbg_on()) fprintf(stderr, "[rhosvd dbg] mode %d grow b %lld -> %lld (r_est %lld)\n", mode, (long long)b, (long long)bn, (long long)r_est);
       RH_CHECK(ensure_b(bn));
       RH_CHECK(k_random(w.Z.p, LDN, n, b, bn, seed + 7919ull * (uint64_t)(it_total + 1), st));
       b = bn;
