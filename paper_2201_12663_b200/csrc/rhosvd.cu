@@ -264,8 +264,10 @@ static int cholqr_pass(Ctx& c, int64_t n, int64_t b, int64_t ldn, const double* 
 //   ORTH_SCQR3    shifted CholeskyQR3 (Fukaya et al.): robust to kappa up to ~u^{-1}
 //   ORTH_CQR1     one pass: a well conditioned (not exactly orthonormal) basis - enough
 //                 inside the subspace iteration, whose next step re-orthonormalises
-//   ORTH_SCQR1    one shifted pass: the same for badly conditioned input (restarts)
-enum { ORTH_CQR2 = 0, ORTH_SCQR3 = 1, ORTH_CQR1 = 2, ORTH_SCQR1 = 3 };
+//   ORTH_SCQR1    one shifted pass: the same for badly conditioned input
+//   ORTH_SCQR2    shifted pass + one plain pass: orthonormal to ~u kappa(Q1)^2 (kappa of the
+//                 shifted pass's output is small), enough for the subspace iteration
+enum { ORTH_CQR2 = 0, ORTH_SCQR3 = 1, ORTH_CQR1 = 2, ORTH_SCQR1 = 3, ORTH_SCQR2 = 4 };
 static int orth(Ctx& c, int64_t n, int64_t b, int64_t ldn, const double* in, double* out, double* tmp,
                 int64_t ldb_small, int kind) {
   const double u = 1.1102230246251565e-16;
@@ -276,6 +278,9 @@ static int orth(Ctx& c, int64_t n, int64_t b, int64_t ldn, const double* in, dou
       return cholqr_pass(c, n, b, ldn, in, out, 0.0, ldb_small);
     case ORTH_SCQR1:
       return cholqr_pass(c, n, b, ldn, in, out, shift, ldb_small);
+    case ORTH_SCQR2:
+      RH_CHECK(cholqr_pass(c, n, b, ldn, in, tmp, shift, ldb_small));
+      return cholqr_pass(c, n, b, ldn, tmp, out, 0.0, ldb_small);
     case ORTH_CQR2:
       RH_CHECK(cholqr_pass(c, n, b, ldn, in, tmp, 0.0, ldb_small));
       return cholqr_pass(c, n, b, ldn, tmp, out, 0.0, ldb_small);
@@ -330,8 +335,8 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
 
   RH_CHECK(ensure_b(b));
   uint64_t seed = o.seed * 0x9E3779B97F4A7C15ull + (uint64_t)(mode + 1) * 0xD1B54A32D192ED03ull;
-  RH_CHECK(k_random(w.M.p, LDN, n, 0, b, seed, st));
-  RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldbs(b), ORTH_SCQR3));
+  // random start block (Gaussian columns; the first step's G Omega is orthonormalised)
+  RH_CHECK(k_random(w.Z.p, LDN, n, 0, b, seed, st));
 
   // ---------------- subspace (simultaneous) iteration Z <- CholQR(G Z), block growth.
   // CholQR keeps leading spans, so span(z_1..z_j) converges to the dominant j-space for
@@ -375,10 +380,11 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     ++itb;
     RH_CHECK(mm(c, n, b, n, G, LDN, false, w.Z.p, LDN, true, w.Y.p, LDN));
     RH_CHECK(k_coldot(w.Z.p, w.Y.p, LDN, n, b, w.th.p, st));
-    // the first steps after a (re)start see badly conditioned G Z: shifted CholQR3.
-    // (One-pass variants leave Z not orthonormal enough for the rank/rate estimates
-    // taken from d_k = z_k^T G z_k.)
-    RH_CHECK(orth(c, n, b, LDN, w.Y.p, w.Z.p, w.T1.p, ldbs(b), itb <= 2 ? ORTH_SCQR3 : ORTH_CQR2));
+    // the first steps after a (re)start see badly conditioned G Z: shifted pass + plain
+    // pass; later steps (aligned Z, well conditioned G Z) one plain pass.  The estimates
+    // d_k are always taken on a Z produced by at least two passes or by one pass on a
+    // well conditioned input.
+    RH_CHECK(orth(c, n, b, LDN, w.Y.p, w.Z.p, w.T1.p, ldbs(b), itb <= 2 ? ORTH_SCQR2 : ORTH_CQR1));
     dbg_check(st, "it Z=orth(GZ)", w.Z.p, n, b, LDN);
     if (b >= m) break;  // full space: exact after one step
     if (itb < 2) continue;
