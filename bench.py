@@ -253,8 +253,18 @@ def run_ours(args):
     peak = fp64_peak() if rank == 0 else {}
     peak_tf = peak.get("dmma_tflops")
     achieved = fl / (kms * 1e-3) / 1e12 if kms > 0 else None
+    traffic, traffic_src = None, None
+    try:  # DRAM bytes per launch of the dominant kernel from the committed ncu capture
+        tj = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))
+        key = "core_kr_tma_kernel<96>" if dom.startswith("core") else "tma_gemm_kernel<128,128,0,0> (Gram)"
+        if key in tj and (args.config == 4 if dom.startswith("core") else args.config == 5):
+            traffic, traffic_src = tj[key]["bytes"], tj[key]["capture"]
+    except Exception:
+        pass
     roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
-            "frac": (achieved / peak_tf) if (achieved and peak_tf) else None, "traffic": None,
+            "frac": (achieved / peak_tf) if (achieved and peak_tf) else None, "traffic": traffic,
+            "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+            "traffic_source": traffic_src,
             "peak_source": "measured DMMA m8n8k4.f64 microbenchmark (tools/fp64_peak.cu) on this GPU; "
                            "MEASURED_PEAKS.json has no FP64 entry",
             "peak_detail": peak, "algorithmic_flop_per_launch": fl, "kernel_ms": kms,
