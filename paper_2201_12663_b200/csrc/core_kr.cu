@@ -29,6 +29,7 @@
 //    fixed order (deterministic, no FP64 atomics; reading A18).
 // Output beta[a,b,c] in C order (c fastest).
 #include <algorithm>
+#include <cstdlib>
 
 #include "tma.cuh"
 
@@ -47,7 +48,7 @@ struct CoreArgs {
   double* out;       // beta (splits == 1) or partials [split][r1 r2 r3]
 };
 
-template <int BN>
+template <int BN, int KSUB>
 __global__ void __launch_bounds__(CORE_THREADS, 1)
     core_kr_tma_kernel(const __grid_constant__ CUtensorMap tW1, const __grid_constant__ CUtensorMap tW2,
                        const __grid_constant__ CUtensorMap tW3, const CoreArgs p) {
@@ -62,6 +63,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1)
   const bool producer = (tid == 0);
   const int M = p.r1 * p.r2;
   const uint32_t w2_off = (uint32_t)p.A1pad * 128, w3_off = w2_off + CORE_BM * 128;
+  const uint32_t slab = p.stage_bytes / KSUB;  // one 16-wide k-slab of W1 | W2ext | W3
 
   // producer cursor over this CTA's k-tile stream (items strided by gridDim.x); the
   // item's box coordinates are recomputed only when the cursor moves to a new item
@@ -80,10 +82,13 @@ __global__ void __launch_bounds__(CORE_THREADS, 1)
     if (pit >= p.items) return;
     unsigned char* st = ring + (size_t)stage * p.stage_bytes;
     mbar_arrive_expect_tx(&full[stage], p.tx_bytes);
-    tma_load_2d(st, &tW1, pk, pa, &full[stage]);
-    tma_load_2d(st + w2_off, &tW2, pk, pb, &full[stage]);
-    tma_load_2d(st + w3_off, &tW3, pk, pn, &full[stage]);
-    pk += CORE_BK;
+#pragma unroll
+    for (int j = 0; j < KSUB; ++j) {
+      tma_load_2d(st + j * slab, &tW1, pk + 16 * j, pa, &full[stage]);
+      tma_load_2d(st + j * slab + w2_off, &tW2, pk + 16 * j, pb, &full[stage]);
+      tma_load_2d(st + j * slab + w3_off, &tW3, pk + 16 * j, pn, &full[stage]);
+    }
+    pk += CORE_BK * KSUB;
     if (pk >= pkend) {
       pit += gridDim.x;
       set_item();
@@ -135,7 +140,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1)
 #pragma unroll
       for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
 
-    for (int k0 = kbeg; k0 < kend; k0 += CORE_BK, ++g) {
+    for (int k0 = kbeg; k0 < kend; k0 += CORE_BK * KSUB, ++g) {
       // refill the stage released one step ago (its 8 warps are done with it)
       if (producer && g >= 1) {
         const uint32_t gp = g - 1, sp = gp % p.stages;
@@ -144,7 +149,9 @@ __global__ void __launch_bounds__(CORE_THREADS, 1)
       }
       const uint32_t s = g % p.stages;
       mbar_wait(&full[s], (g / p.stages) & 1);
-      const uint32_t w1 = ring_s + s * p.stage_bytes;
+#pragma unroll
+      for (int js = 0; js < KSUB; ++js) {
+      const uint32_t w1 = ring_s + s * p.stage_bytes + js * slab;
       const uint32_t w2 = w1 + w2_off + (wm0 + fr) * 128;
       const uint32_t w3 = w1 + w3_off + fr * 128;
 #pragma unroll
@@ -157,7 +164,8 @@ __global__ void __launch_bounds__(CORE_THREADS, 1)
 #pragma unroll
         for (int i = 0; i < FM; ++i)
 #pragma unroll
-          for (int j = 0; j < FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+          for (int jn = 0; jn < FN; ++jn) dmma_8x8x4(acc[i][jn][0], acc[i][jn][1], af[i], bf[jn]);
+      }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -244,10 +252,10 @@ size_t core_ws_doubles(int64_t r2, int64_t R, int64_t ldw) {
   return (size_t)(r2 + CORE_BM) * std::max<int64_t>(ldw, round_up(std::max<int64_t>(R, 2), 16));
 }
 
-template <int BN>
+template <int BN, int KSUB>
 static int launch_core(const CUtensorMap& t1, const CUtensorMap& t2, const CUtensorMap& t3, const CoreArgs& a,
                        size_t smem, int grid, cudaStream_t st) {
-  auto kern = core_kr_tma_kernel<BN>;
+  auto kern = core_kr_tma_kernel<BN, KSUB>;
   RH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   kern<<<grid, CORE_THREADS, smem, st>>>(t1, t2, t3, a);
   count_launch();
@@ -279,15 +287,20 @@ int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3,
   a.mt = (int)cdiv(M, CORE_BM);
   a.nt = (int)cdiv(r3, BN);
   a.tiles = a.mt * a.nt;
-  a.stage_bytes = (uint32_t)((a.A1pad + CORE_BM + BN) * 128);
-  a.tx_bytes = (uint32_t)((a.A1 + CORE_BM + BN) * 128);
+  static int ksub = -1;  // 16-wide k-slabs per pipeline stage (one mbarrier round trip each)
+  if (ksub < 0) {
+    const char* e = getenv("RHOSVD_CORE_KSUB");
+    ksub = (e && atoi(e) == 1) ? 1 : 2;
+  }
+  a.stage_bytes = (uint32_t)((a.A1pad + CORE_BM + BN) * 128 * ksub);
+  a.tx_bytes = (uint32_t)((a.A1 + CORE_BM + BN) * 128 * ksub);
   const size_t budget = 227 * 1024 - 1024 - 256;
   a.stages = (int)std::min<size_t>(8, budget / a.stage_bytes);
   if (a.stages < 2) return fail(RHOSVD_EINVAL, "core: tile does not fit shared memory");
   const int sms = num_sms();
   int splits = core_splits(r1, r2, r3, R, BN);
   while (splits > 1 && (size_t)splits * total > part_cap) --splits;
-  a.kchunk = (int)round_up(cdiv(R, splits), CORE_BK);
+  a.kchunk = (int)round_up(cdiv(R, splits), CORE_BK * ksub);
   splits = (int)cdiv(R, a.kchunk);
   a.splits = splits;
   a.items = a.tiles * splits;
@@ -307,12 +320,15 @@ int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3,
   RH_CHECK(make_tmap_2d(&t3, W3, r3, R, ldw, CORE_BK, BN, true));
   const size_t smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * a.stages * sizeof(uint64_t);
   const int grid = (int)std::min<int64_t>(a.items, sms);
-  if (BN == 128)
-    RH_CHECK(launch_core<128>(t1, t2, t3, a, smem, grid, st));
-  else if (BN == 96)
-    RH_CHECK(launch_core<96>(t1, t2, t3, a, smem, grid, st));
-  else
-    RH_CHECK(launch_core<64>(t1, t2, t3, a, smem, grid, st));
+  if (ksub == 2) {
+    if (BN == 128) RH_CHECK((launch_core<128, 2>(t1, t2, t3, a, smem, grid, st)));
+    else if (BN == 96) RH_CHECK((launch_core<96, 2>(t1, t2, t3, a, smem, grid, st)));
+    else RH_CHECK((launch_core<64, 2>(t1, t2, t3, a, smem, grid, st)));
+  } else {
+    if (BN == 128) RH_CHECK((launch_core<128, 1>(t1, t2, t3, a, smem, grid, st)));
+    else if (BN == 96) RH_CHECK((launch_core<96, 1>(t1, t2, t3, a, smem, grid, st)));
+    else RH_CHECK((launch_core<64, 1>(t1, t2, t3, a, smem, grid, st)));
+  }
   if (splits > 1) {
     core_splitk_reduce<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(part, splits, total, beta);
     count_launch();
