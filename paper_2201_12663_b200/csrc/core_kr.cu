@@ -287,11 +287,11 @@ int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3,
   a.mt = (int)cdiv(M, CORE_BM);
   a.nt = (int)cdiv(r3, BN);
   a.tiles = a.mt * a.nt;
-  static int ksub = -1;  // 16-wide k-slabs per pipeline stage (one mbarrier round trip each)
-  if (ksub < 0) {
+  // 16-wide k-slabs per pipeline stage (one mbarrier round trip each); thread-safe init
+  static const int ksub = [] {
     const char* e = getenv("RHOSVD_CORE_KSUB");
-    ksub = (e && atoi(e) == 1) ? 1 : 2;
-  }
+    return (e && atoi(e) == 1) ? 1 : 2;
+  }();
   a.stage_bytes = (uint32_t)((a.A1pad + CORE_BM + BN) * 128 * ksub);
   a.tx_bytes = (uint32_t)((a.A1 + CORE_BM + BN) * 128 * ksub);
   const size_t budget = 227 * 1024 - 1024 - 256;
@@ -354,14 +354,15 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 
 int make_tmap_2d(CUtensorMap* map, const double* base, int64_t rows, int64_t cols, int64_t ld, int box_cols,
                  int box_rows, bool swizzle128) {
-  static EncodeTiledFn enc = nullptr;
-  if (!enc) {
+  static const EncodeTiledFn enc = [] {
     void* fn = nullptr;
     cudaDriverEntryPointQueryResult q;
-    RH_CUDA(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q));
-    if (!fn || q != cudaDriverEntryPointSuccess) return fail(RHOSVD_ECUDA, "cuTensorMapEncodeTiled unavailable");
-    enc = (EncodeTiledFn)fn;
-  }
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      fn = nullptr;
+    return (EncodeTiledFn)fn;
+  }();
+  if (!enc) return fail(RHOSVD_ECUDA, "cuTensorMapEncodeTiled unavailable");
   if (((uintptr_t)base & 15) || ((ld * 8) & 15)) return fail(RHOSVD_EINVAL, "tensor map: 16-B alignment");
   cuuint64_t gdim[2] = {(cuuint64_t)std::max<int64_t>(cols, 1), (cuuint64_t)std::max<int64_t>(rows, 1)};
   cuuint64_t gstride[1] = {(cuuint64_t)(ld * 8)};

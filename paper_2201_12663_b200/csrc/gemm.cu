@@ -278,11 +278,9 @@ static int launch_cfg(const GemmArgs& g, GParams gp, cudaStream_t st) {
   const size_t budget = 227 * 1024 - 1024 - 256;
   gp.stages = (int)std::min<size_t>(8, budget / gp.stage_bytes);
   const size_t smem = 1024 + (size_t)gp.stages * gp.stage_bytes + 2 * gp.stages * sizeof(uint64_t);
-  static bool attr_set = false;  // per instantiation
-  if (!attr_set) {
-    RH_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr_set = true;
-  }
+  static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                        227 * 1024);  // per instantiation, thread-safe
+  RH_CUDA(attr);
   const int grid = (int)std::min<int64_t>(gp.items, num_sms());
   kern<<<grid, GTHREADS, smem, st>>>(tA, tB, gp);
   count_launch();

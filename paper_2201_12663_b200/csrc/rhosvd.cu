@@ -20,6 +20,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <thread>
+#include <array>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -41,13 +43,12 @@ int fail(int status, const std::string& msg) {
 }
 
 int num_sms() {
-  static int s = 0;
-  if (!s) {
-    int dev = 0;
+  static const int s = [] {
+    int dev = 0, v = 0;
     cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&s, cudaDevAttrMultiProcessorCount, dev);
-    if (s <= 0) s = 148;
-  }
+    cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev);
+    return v > 0 ? v : 148;
+  }();
   return s;
 }
 
@@ -78,13 +79,19 @@ struct DBuf {
   }
 };
 
-struct Workspace {
-  DBuf Uh, s, tcol, xip, xip2, scal, part;
-  DBuf G, Z, Y, M, T1;
+// per-mode buffers of the eigensolver (S3-S5): the three modes run concurrently
+struct ModeWs {
+  DBuf Z, Y, M, T1;
   DBuf H, V, S, Bp, th, inv, tail2, sgn;
-  DBuf W, X, W1x, W2x, corepart;
+  DBuf W, X;
   Scratch gsc;
   DenseWs dws;
+};
+struct Workspace {
+  DBuf Uh, s, tcol, xip, xip2, scal, part;
+  DBuf G, W1x, W2x, corepart;
+  Scratch gsc;
+  ModeWs mw[3];
   int* flag = nullptr;
 };
 // Output buffers (frames, CP factors, sigma, core) outlive the call: the result handle
@@ -148,6 +155,31 @@ static OutCache& OC() {
   return c;
 }
 
+// RHOSVD_SERIAL_MODES=1 runs the three per-mode eigensolves one after another
+static bool modes_concurrent() {
+  static const bool on = [] {
+    const char* e = getenv("RHOSVD_SERIAL_MODES");
+    return !(e && e[0] == '1');
+  }();
+  return on;
+}
+// one non-blocking stream per mode (created once per device)
+static cudaStream_t* mode_streams() {
+  static std::mutex mu;
+  static std::map<int, std::array<cudaStream_t, 3>> per_dev;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = per_dev.find(dev);
+  if (it == per_dev.end()) {
+    std::array<cudaStream_t, 3> a{};
+    for (auto& x : a)
+      if (cudaStreamCreateWithFlags(&x, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    it = per_dev.emplace(dev, a).first;
+  }
+  return it->second.data();
+}
+
 static Workspace& WS() {
   static Workspace w;
   return w;
@@ -192,6 +224,7 @@ struct Ctx {
   rhosvd_report* rep;
   PhaseTimer* tm;
   double flops = 0.0;
+  ModeWs* m = nullptr;  // per-mode buffers (S3-S5); GEMM scratch comes from here when set
 };
 
 // ------------------------------------------------------------------ GEMM shorthands
@@ -202,7 +235,7 @@ static int mm(Ctx& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
   GemmArgs g;
   g.M = M; g.N = N; g.K = K; g.A = A; g.lda = lda; g.a_k = ak; g.B = B; g.ldb = ldb; g.b_k = bk;
   g.C = C; g.ldc = ldc; g.col_scale = cs; g.row_scale = rs; g.upper_sym = upper;
-  return gemm(g, c.w.gsc, c.st, &c.flops);
+  return gemm(g, c.m ? c.m->gsc : c.w.gsc, c.st, &c.flops);
 }
 
 static int allreduce(Ctx& c, double* p, int64_t count) {
@@ -214,12 +247,11 @@ static int allreduce(Ctx& c, double* p, int64_t count) {
 
 // RHOSVD_DEBUG=1: synchronise and scan a device array for non-finite values (debug only)
 static bool dbg_on() {
-  static int on = -1;
-  if (on < 0) {
+  static const bool on = [] {
     const char* e = getenv("RHOSVD_DEBUG");
-    on = (e && e[0] == '1') ? 1 : 0;
-  }
-  return on == 1;
+    return e && e[0] == '1';
+  }();
+  return on;
 }
 static void dbg_check(cudaStream_t st, const char* tag, const double* p, int64_t rows, int64_t cols, int64_t ld) {
   if (!dbg_on() || !p) return;
@@ -249,7 +281,7 @@ static void dbg_check(cudaStream_t st, const char* tag, const double* p, int64_t
 // CholeskyQR pass: dst = src * D L^{-T}, L = chol(D src^T src D + shift I)
 static int cholqr_pass(Ctx& c, int64_t n, int64_t b, int64_t ldn, const double* src, double* dst, double shift,
                        int64_t ldb_small) {
-  Workspace& w = c.w;
+  ModeWs& w = *c.m;
   RH_CHECK(mm(c, b, b, n, src, ldn, true, src, ldn, true, w.S.p, ldb_small, nullptr, true));
   dbg_check(c.st, "chol S", w.S.p, b, b, ldb_small);
   RH_CHECK(chol_inv_scaled(b, w.S.p, ldb_small, shift, w.Bp.p, ldb_small, w.dws, c.st));
@@ -304,7 +336,8 @@ struct ModeOut {
 // eigensolver + one-sided RR + refinement + rank + projection for one mode
 static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int64_t Rp, int64_t Rg,
                       const double* Uh, const double* G, double T, const rhosvd_opts& o, ModeOut& mo) {
-  Workspace& w = c.w;
+  ModeWs& w = *c.m;
+  double* const scal = c.w.scal.p;  // shared scalar slots (mode-offset)
   cudaStream_t st = c.st;
   const int64_t m = std::min<int64_t>(n, Rg);
   const bool epsmode = o.rank_mode == RHOSVD_EPS;
@@ -478,21 +511,21 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
   {
     GemmArgs g;
     g.M = n; g.N = Rl; g.K = b; g.A = w.Z.p; g.lda = LDN; g.a_k = false; g.B = w.W.p; g.ldb = Rp; g.b_k = false;
-    g.epi = EPI_RESID; g.D = Uh; g.ldd = LDN; g.resid_out = w.scal.p + 16 + mode;
+    g.epi = EPI_RESID; g.D = Uh; g.ldd = LDN; g.resid_out = scal + 16 + mode;
     if (Rl > 0) {
       RH_CHECK(gemm(g, w.gsc, st, &c.flops));
     } else {
-      RH_CUDA(cudaMemsetAsync(w.scal.p + 16 + mode, 0, sizeof(double), st));
+      RH_CUDA(cudaMemsetAsync(scal + 16 + mode, 0, sizeof(double), st));
     }
-    RH_CHECK(allreduce(c, w.scal.p + 16 + mode, 1));
+    RH_CHECK(allreduce(c, scal + 16 + mode, 1));
     c.tm->mark(PH_RANK);
   }
   double sel[4];
-  RH_CHECK(k_select_rank(w.th.p, b, w.scal.p + 16 + mode, T, epsmode ? o.eps : 0.0, (int)rfix, 8, w.tail2.p,
-                         w.scal.p + 24 + 4 * mode, w.inv.p, st));
-  RH_CUDA(cudaMemcpyAsync(sel, w.scal.p + 24 + 4 * mode, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  RH_CHECK(k_select_rank(w.th.p, b, scal + 16 + mode, T, epsmode ? o.eps : 0.0, (int)rfix, 8, w.tail2.p,
+                         scal + 24 + 4 * mode, w.inv.p, st));
+  RH_CUDA(cudaMemcpyAsync(sel, scal + 24 + 4 * mode, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
   double rho_h = 0.0;
-  RH_CUDA(cudaMemcpyAsync(&rho_h, w.scal.p + 16 + mode, sizeof(double), cudaMemcpyDeviceToHost, st));
+  RH_CUDA(cudaMemcpyAsync(&rho_h, scal + 16 + mode, sizeof(double), cudaMemcpyDeviceToHost, st));
   RH_CUDA(cudaStreamSynchronize(st));
   int64_t r = (int64_t)sel[0];
   if (r < 0) {  // the block did not reach the threshold (should not happen after growth)
@@ -694,19 +727,83 @@ static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n
   RH_CHECK(allreduce(c, w.G.p, 3 * LDN * LDN));
   tm.mark(PH_EIG);
 
-  // ---- S3-S5 per mode
+  // ---- S3-S5 per mode.  The three modes are independent; on one GPU (no collectives
+  // inside) they run concurrently: one host thread and one stream per mode, so the
+  // latency-bound b x b kernels and host decisions of one mode overlap the GEMMs of
+  // the others.  With a communicator the modes run in order (one communicator must not
+  // be used by two threads at once).
   ModeOut mo[3];
+  int mst[3] = {RHOSVD_OK, RHOSVD_OK, RHOSVD_OK};
+  std::string merr[3];
+  const bool concurrent = (!comm || comm->world <= 1) && modes_concurrent();
+  if (concurrent) {
+    int dev = 0;
+    RH_CUDA(cudaGetDevice(&dev));
+    cudaStream_t* ms = mode_streams();
+    if (!ms) return fail(RHOSVD_ECUDA, "mode stream creation failed");
+    cudaEvent_t ev0;
+    RH_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
+    RH_CUDA(cudaEventRecord(ev0, st));
+    for (int l = 0; l < 3; ++l) RH_CUDA(cudaStreamWaitEvent(ms[l], ev0, 0));
+    double mflops[3] = {0, 0, 0};
+    int mlaunch[3] = {0, 0, 0};
+    double mphase[3][16] = {{0}};
+    auto run = [&](int l) {
+      cudaSetDevice(dev);
+      g_launches = 0;
+      PhaseTimer mtm(ms[l]);
+      mtm.mark(PH_EIG);
+      Ctx cl{ms[l], comm, w, &rep, &mtm};
+      cl.m = &w.mw[l];
+      mst[l] = solve_mode(cl, l, n, LDN, Rl, Rp, Rg, Uh[l], w.G.p + (size_t)l * LDN * LDN, rep.trace[l], o, mo[l]);
+      mtm.mark(-1);
+      if (mst[l] != RHOSVD_OK) merr[l] = g_err;
+      mtm.collect(mphase[l]);
+      mflops[l] = cl.flops;
+      mlaunch[l] = g_launches;
+    };
+    std::thread t1(run, 1), t2(run, 2);
+    run(0);
+    t1.join();
+    t2.join();
+    g_launches += mlaunch[0] + mlaunch[1] + mlaunch[2];
+    c.flops += mflops[0] + mflops[1] + mflops[2];
+    // per-phase device times of the concurrent region, summed over the modes (ms[9..13]:
+    // eigensolve, rr_refine, residual_rank, projection, collectives)
+    for (int l = 0; l < 3; ++l)
+      for (int ph = PH_EIG; ph <= PH_COMM; ++ph) rep.ms[9 + ph - PH_EIG] += mphase[l][ph];
+    cudaEvent_t ev[3];
+    for (int l = 0; l < 3; ++l) {
+      RH_CUDA(cudaEventCreateWithFlags(&ev[l], cudaEventDisableTiming));
+      RH_CUDA(cudaEventRecord(ev[l], ms[l]));
+      RH_CUDA(cudaStreamWaitEvent(st, ev[l], 0));
+    }
+    cudaEventDestroy(ev0);
+    for (int l = 0; l < 3; ++l) cudaEventDestroy(ev[l]);
+  } else {
+    for (int l = 0; l < 3; ++l) {
+      c.m = &w.mw[l];
+      mst[l] = solve_mode(c, l, n, LDN, Rl, Rp, Rg, Uh[l], w.G.p + (size_t)l * LDN * LDN, rep.trace[l], o, mo[l]);
+      c.m = nullptr;
+      if (mst[l] != RHOSVD_OK) {
+        merr[l] = g_err;
+        break;
+      }
+      tm.mark(PH_EIG);
+    }
+  }
   for (int l = 0; l < 3; ++l) {
-    int st_ = solve_mode(c, l, n, LDN, Rl, Rp, Rg, Uh[l], w.G.p + (size_t)l * LDN * LDN, rep.trace[l], o, mo[l]);
-    if (st_ != RHOSVD_OK) {
-      for (int q = 0; q <= l; ++q) {
-        cudaStreamSynchronize(st);
+    if (mst[l] != RHOSVD_OK) {
+      cudaDeviceSynchronize();
+      for (int q = 0; q < 3; ++q) {
         OC().put(mo[q].Z);
         OC().put(mo[q].W);
         OC().put(mo[q].sigma);
       }
-      return st_;
+      return fail(mst[l], merr[l]);
     }
+  }
+  for (int l = 0; l < 3; ++l) {
     res->Z[l] = mo[l].Z;
     res->W[l] = mo[l].W;
     res->sigma[l] = mo[l].sigma;
@@ -717,8 +814,8 @@ static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n
     rep.grow_events[l] = mo[l].grows;
     rep.rho[l] = mo[l].rho;
     rep.tail[l] = std::sqrt(std::max(0.0, mo[l].tail2));
-    tm.mark(PH_EIG);
   }
+  tm.mark(PH_EIG);
 
   // ---- S6 core (K7): beta = (W1 (.) W2)(xi' o W3)^T, then all-reduce
   tm.mark(PH_CORE);
@@ -869,7 +966,7 @@ int rhosvd_syevj(int64_t b, double* A, int64_t lda, double* lambda, double* V, i
   if (!A || !lambda || !V || b < 0 || lda < b || ldv < b) return fail(RHOSVD_EINVAL, "bad args");
   std::lock_guard<std::mutex> lk(g_mu);
   int sw = 0;
-  RH_CHECK(syevj(b, A, lda, lambda, V, ldv, tol > 0 ? tol : 1e-15, 1e-300, 80, WS().dws, (cudaStream_t)stream, &sw));
+  RH_CHECK(syevj(b, A, lda, lambda, V, ldv, tol > 0 ? tol : 1e-15, 1e-300, 80, WS().mw[0].dws, (cudaStream_t)stream, &sw));
   if (sweeps_out) *sweeps_out = sw;
   return RHOSVD_OK;
 }
@@ -878,7 +975,7 @@ int rhosvd_chol_inv(int64_t b, const double* S, int64_t lds, double shift, doubl
                     rhosvd_stream stream) {
   if (!S || !Bp || b < 0 || lds < b || ldb < b || !(shift >= 0.0)) return fail(RHOSVD_EINVAL, "bad args");
   std::lock_guard<std::mutex> lk(g_mu);
-  return chol_inv_scaled(b, S, lds, shift, Bp, ldb, WS().dws, (cudaStream_t)stream);
+  return chol_inv_scaled(b, S, lds, shift, Bp, ldb, WS().mw[0].dws, (cudaStream_t)stream);
 }
 
 int rhosvd_core(const double* W1, const double* W2, const double* W3, int64_t ldw, const double* xi, int64_t r1,

@@ -738,19 +738,16 @@ int syevj(int64_t b, const double* A, int64_t lda, double* lambda, double* Vout,
   jp.Ain = A; jp.lda = lda; jp.A0 = ws.A0; jp.A1 = ws.A1; jp.ld = ws.ld; jp.V = ws.V;
   jp.lam = ws.cs;  // unsorted eigenvalues staged in cs
   jp.tol = tol; jp.abstol = abstol; jp.max_sweeps = max_sweeps; jp.bar = ws.bar; jp.info = ws.info;
-  static int smem_maxb = -1;
-  if (smem_maxb < 0) {
+  static const int smem_maxb = [] {
     const char* e = getenv("RHOSVD_JAC_SMEM_MAXB");
-    smem_maxb = e ? std::max(0, std::min(atoi(e), JAC_SMEM_MAXB)) : 32;
-  }
+    return e ? std::max(0, std::min(atoi(e), JAC_SMEM_MAXB)) : 32;
+  }();
   if (b <= smem_maxb) {
     const int threads = 1024;
     size_t smem = (size_t)b * (b | 1) * sizeof(double) + (size_t)jp.h * (3 * sizeof(double) + 3 * sizeof(int)) + 64;
-    static bool attr_s = false;
-    if (!attr_s) {
-      RH_CUDA(cudaFuncSetAttribute(jacobi_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024));
-      attr_s = true;
-    }
+    static const cudaError_t attr_s =
+        cudaFuncSetAttribute(jacobi_smem_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    RH_CUDA(attr_s);
     jacobi_smem_kernel<<<1, threads, smem, st>>>(jp);
     count_launch();
     RH_LAUNCH_CHECK();
@@ -766,31 +763,27 @@ int syevj(int64_t b, const double* A, int64_t lda, double* lambda, double* Vout,
     bj.rotf = ws.rotf; bj.lam = ws.cs; bj.tol = tol; bj.abstol = abstol;
     bj.max_sweeps = std::min(max_sweeps, 250);
     {
-      static int inner = -1;
-      if (inner < 0) {
+      static const int inner = [] {
         const char* e = getenv("RHOSVD_JAC_INNER");
-        inner = e ? std::max(1, atoi(e)) : 1;
-      }
+        return e ? std::max(1, atoi(e)) : 1;
+      }();
       bj.inner_sweeps = inner;
     }
     bj.bar = ws.bar; bj.cnt = ws.cnt; bj.info = ws.info;
     const int threads = 256;
     const size_t smem = (size_t)(2 * BJ_P + 2 * BJ_VT) * BJ_LD * sizeof(double);
-    static bool attr_b = false;
-    if (!attr_b) {
-      RH_CUDA(cudaFuncSetAttribute(jacobi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      attr_b = true;
-    }
+    static const cudaError_t attr_b =
+        cudaFuncSetAttribute(jacobi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    RH_CUDA(attr_b);
     int64_t want = (int64_t)bj.h * (bj.h - 1) / 2 + cdiv(bj.bp, BJ_VT) * bj.h;
     int grid = (int)std::min<int64_t>(coop_grid((const void*)jacobi_block_kernel, threads, smem, want), num_sms());
-    static int tsm = -1;
-    static unsigned long long* tsb = nullptr;
-    if (tsm < 0) {
+    static const int tsm = [] {
       const char* e = getenv("RHOSVD_TS");
-      tsm = (e && e[0] == '1') ? 1 : 0;
-      if (tsm) cudaMalloc(&tsb, 64 * sizeof(unsigned long long));
-    }
-    bj.ts = tsm ? tsb : nullptr;
+      return (e && e[0] == '1') ? 1 : 0;
+    }();
+    unsigned long long* tsb = nullptr;
+    if (tsm) cudaMallocAsync((void**)&tsb, 64 * sizeof(unsigned long long), st);
+    bj.ts = tsb;
     void* args[] = {&bj};
     RH_CUDA(cudaLaunchCooperativeKernel((const void*)jacobi_block_kernel, dim3(grid), dim3(threads), args, smem, st));
     count_launch();
@@ -802,6 +795,7 @@ int syevj(int64_t b, const double* A, int64_t lda, double* lambda, double* Vout,
       cudaMemcpy(inf, ws.info, sizeof(inf), cudaMemcpyDeviceToHost);
       fprintf(stderr, "[jacobi ts] b=%d m=%d grid=%d sweeps=%d: phase1 %.1f bar1 %.1f phase2 %.1f bar2 %.1f us\n",
               (int)b, bj.m, grid, inf[0], h[0] * 1e-3, h[1] * 1e-3, h[2] * 1e-3, h[3] * 1e-3);
+      cudaFreeAsync(tsb, st);
     }
   }
   rank_sort_kernel<<<1, 1024, 0, st>>>((int)b, ws.cs, lambda, ws.perm);
@@ -1199,21 +1193,18 @@ int chol_inv_scaled(int64_t b, const double* S, int64_t lds, double shift_rel, d
   cp.Bp = Bp; cp.ldb = ldb; cp.ld = ws.ld; cp.bar = ws.bar; cp.info = ws.info;
   const int threads = 256;
   const size_t smem = (size_t)3 * CB * CLD * sizeof(double);
-  static bool attr = false;
-  if (!attr) {
-    RH_CUDA(cudaFuncSetAttribute(chol_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = true;
-  }
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(chol_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  RH_CUDA(attr);
   int64_t want = std::max<int64_t>(1, (int64_t)(P - 1) * P / 2);
   int grid = coop_grid((const void*)chol_blk_kernel, threads, smem, want);
-  static int tsmode = -1;
-  static unsigned long long* tsbuf = nullptr;
-  if (tsmode < 0) {
+  static const int tsmode = [] {
     const char* e = getenv("RHOSVD_TS");
-    tsmode = (e && e[0] == '1') ? 1 : 0;
-    if (tsmode) cudaMalloc(&tsbuf, 1024 * sizeof(unsigned long long));
-  }
-  cp.ts = tsmode ? tsbuf : nullptr;
+    return (e && e[0] == '1') ? 1 : 0;
+  }();
+  unsigned long long* tsbuf = nullptr;
+  if (tsmode) cudaMallocAsync((void**)&tsbuf, 1024 * sizeof(unsigned long long), st);
+  cp.ts = tsbuf;
   void* args[] = {&cp};
   RH_CUDA(cudaLaunchCooperativeKernel((const void*)chol_blk_kernel, dim3(grid), dim3(threads), args, smem, st));
   count_launch();
@@ -1225,6 +1216,7 @@ int chol_inv_scaled(int64_t b, const double* S, int64_t lds, double shift_rel, d
     fprintf(stderr, "[chol ts] b=%d P=%d grid=%d:", (int)b, P, grid);
     for (int i = 1; i < 3 + 2 * P - 1; ++i) fprintf(stderr, " %.1f", (h[i] - h[0]) * 1e-3);
     fprintf(stderr, " us\n");
+    cudaFreeAsync(tsbuf, st);
   }
   return RHOSVD_OK;
 }
