@@ -80,7 +80,10 @@ typedef struct {
 /* Per-call report (host struct).  ms[] holds per-phase device times:
  *   0 normalize, 1 gram, 2 eigensolve (subspace iteration), 3 one-sided RR +
  *   refinement, 4 residual + rank, 5 projection W_r, 6 core, 7 collectives,
- *   8 total (all in milliseconds, CUDA events on the call's stream). */
+ *   8 total (all in milliseconds, CUDA events on the call's stream).  When the three
+ *   per-mode eigensolves run concurrently (one GPU), ms[2] is the wall time of that
+ *   region and ms[9..13] hold the per-mode device times summed over the modes
+ *   (eigensolve, RR + refinement, residual + rank, projection, collectives). */
 typedef struct {
   double  trace[3];      /* T_l = ||Uhat_l||_F^2                                   */
   double  tail[3];       /* (sum_{k>r_l} sigma_{l,k}^2)^{1/2} (direct residual form) */

@@ -251,7 +251,10 @@ def _report_dict(rep: Report):
         bound_paper=rep.bound_paper, bound_ns=rep.bound_ns, beta_norm=rep.beta_norm,
         rho=list(rep.rho), ranks=list(rep.ranks), block=list(rep.block), iters=list(rep.iters),
         grow_events=list(rep.grow_events), R_global=rep.R_global,
-        ms={PHASES[i]: rep.ms[i] for i in range(len(PHASES))}, gemm_flops=rep.gemm_flops,
+        ms={PHASES[i]: rep.ms[i] for i in range(len(PHASES))},
+        ms_modes_summed={nm: rep.ms[9 + i] for i, nm in
+                         enumerate(["eigensolve", "rr_refine", "residual_rank", "projection", "collectives"])},
+        gemm_flops=rep.gemm_flops,
         core_ms=rep.core_ms, gram_ms=rep.gram_ms, launches=rep.launches)
 
 
