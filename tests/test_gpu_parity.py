@@ -189,3 +189,23 @@ def test_parity_full_size_fixture(rh, k):
     # tails within the threshold, consistent with the oracle's
     for l in range(3):
         assert abs(g.report["tail"][l] - fx["tail"][l]) <= 1e-6 * fx["tail"][l]
+    # sampled outputs computed one by one on the host from the GPU frames (independent of
+    # the GPU kernels): W_l[a, :] = z_a^T Uhat_l, ||W_l[a, :]|| = sigma_a (Def. 2.1:
+    # W = Z^T Uhat = D V^T) and beta[a,b,c] = sum_k xi'_k W1[a,k] W2[b,k] W3[c,k]
+    # (Prop. 2.1), at the first, last and a random retained index of every mode.
+    from oracle import normalize
+    Uh, xip, _, _ = normalize([U1, U2, U3], xi)
+    rng = np.random.default_rng(11)
+    Zg = [z.cpu().numpy() for z in g.Z]
+    idx = [np.array(sorted({0, g.ranks[l] - 1, int(rng.integers(g.ranks[l]))})) for l in range(3)]
+    Wt = [Uh[l] @ Zg[l][:, idx[l]] for l in range(3)]  # (R, |idx|) = W_l[idx, :]^T
+    for l in range(3):
+        s_host = np.linalg.norm(Wt[l], axis=0)
+        s_gpu = g.sigma[l].cpu().numpy()[idx[l]]
+        assert np.max(np.abs(s_host - s_gpu) / s_gpu) <= 1e-10
+    beta = g.beta.cpu().numpy()
+    for i, a in enumerate(idx[0]):
+        for j, b in enumerate(idx[1]):
+            for q, c in enumerate(idx[2]):
+                terms = xip * Wt[0][:, i] * Wt[1][:, j] * Wt[2][:, q]
+                assert abs(beta[a, b, c] - terms.sum()) <= 1e-9 * np.abs(terms).sum(), (a, b, c)
