@@ -325,6 +325,18 @@ int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
       int64_t want = cdiv(2LL * sms, gp.tiles);
       int64_t maxs = std::max<int64_t>(1, g.K / 256);
       splits = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(want, maxs), 64));
+    } else if (g.K >= 4 * 2048) {
+      // wave quantisation: with a few items per SM the last wave idles SMs (528 Gram tiles
+      // on 148 SMs run 4 waves for 3.57 of work); split K if that evens the waves out
+      double best = (double)cdiv(gp.tiles, sms) * sms / gp.tiles;
+      for (int s2 = 2; s2 <= 4; ++s2) {
+        if (g.K / s2 < 2048) break;
+        const double cost = (double)cdiv((int64_t)gp.tiles * s2, sms) * sms / ((double)gp.tiles * s2) * 1.01;
+        if (cost < best * 0.97) {
+          best = cost;
+          splits = s2;
+        }
+      }
     }
   }
   int kchunk = (int)round_up(cdiv(std::max<int64_t>(g.K, 1), splits), GBK);
