@@ -148,6 +148,27 @@ void rhosvd_result_free    (rhosvd_result* res);
 const char* rhosvd_last_error(void);
 const char* rhosvd_version(void);
 
+/* ---- Tucker-to-canonical (T2C) and canonical-to-canonical (C2C) rank reduction ----
+ * (Remark 2.1.)  The core beta of `res` is split
+ * into its r3 mode-3 slices B_m (r1 x r2); each is replaced by its truncated SVD keeping
+ * the singular values > thr = eps / (r3 sqrt(min(r1, r2)))  (eps / r^{3/2} for a cubic
+ * core), eps = eps_rel ||beta||_F, so that ||beta - beta_(R)||_F <= eps with
+ * R = p_1 + ... + p_r3 <= r3 min(r1, r2).  The result is lifted through the frames:
+ *   A ~ sum_j w_j F1[:, j] (x) F2[:, j] (x) F3[:, j],
+ *   F1 = Z1 u_j, F2 = Z2 v_j, F3 = Z3 e_{slice_j}   (unit columns, w_j = sigma_j).
+ * Signs: the largest-|.| entry of u_j is positive.  The slices are processed in shared
+ * memory (one CTA each): r1 (r2 + 1) must stay below ~27 000 doubles, else EINVAL.
+ * All output pointers are device pointers owned by the rhosvd_cp handle. */
+typedef struct rhosvd_cp rhosvd_cp;
+int  rhosvd_t2c(const rhosvd_result* res, double eps_rel, rhosvd_stream stream, rhosvd_cp** out);
+int  rhosvd_cp_rank(const rhosvd_cp* cp, int64_t* R);                                /* host out */
+int  rhosvd_cp_factor(const rhosvd_cp* cp, int mode, const double** F, int64_t* ld);  /* n x R col-major */
+int  rhosvd_cp_core_factor(const rhosvd_cp* cp, int mode, const double** F, int64_t* ld); /* mode 0: u (r1 x R), 1: v (r2 x R) */
+int  rhosvd_cp_weights(const rhosvd_cp* cp, const double** w, const int32_t** slice);   /* R each */
+int  rhosvd_cp_info(const rhosvd_cp* cp, double* eps_abs, double* thr, double* err2,
+                    int32_t* max_sweeps);                                          /* host out */
+void rhosvd_cp_free(rhosvd_cp* cp);
+
 /* ---- kernel-level entry points (used by the parity unit tests and bench) ----
  * Each runs ONE device kernel family on `stream`, all pointers device.     */
 

@@ -556,15 +556,7 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
 // ====================================================================== C ABI
 using namespace rhosvd;
 
-struct rhosvd_result {
-  int32_t ranks[3] = {0, 0, 0};
-  int64_t n = 0, ldz = 0, Rl = 0, Rp = 0;
-  double* Z[3] = {nullptr, nullptr, nullptr};
-  double* sigma[3] = {nullptr, nullptr, nullptr};
-  double* W[3] = {nullptr, nullptr, nullptr};
-  double* beta = nullptr;
-  rhosvd_report rep{};
-};
+#include "result.h"
 
 extern "C" {
 

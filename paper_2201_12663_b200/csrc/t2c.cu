@@ -1,0 +1,441 @@
+// t2c.cu - Tucker-to-canonical (T2C) of the RHOSVD core and its lift through the frames:
+// the canonical-to-canonical (C2C) rank reduction C2C = T2C o C2T.
+//
+// Remark 2.1: beta = sum_m B_m (x) z_m over the mode-3 slices B_m
+// (r1 x r2); each slice is replaced by its truncated SVD B_{p_m} keeping the singular values
+// above thr = eps / (r3 sqrt(min(r1, r2))) (eps / r^{3/2} for a cubic core; reading T2),
+// so that ||beta - beta_(R)|| <= eps with R = p_1 + ... + p_r3.  Lifting the core's CP
+// factors through the orthonormal frames (Lemma 2.1) gives
+//     A ~ sum_m sum_{k <= p_m} sigma_k^(m) (Z1 u_k) (x) (Z2 v_k) (x) (Z3 e_m).
+//
+// GPU design: one CTA per slice keeps the whole slice in shared memory and runs a
+// one-sided (Hestenes) Jacobi SVD on its columns - warp-parallel over the r2/2 disjoint
+// column pairs of a round-robin step, column dot products by warp reductions (fixed
+// order), one __syncthreads per step.  sigma_k = ||b_k||, u_k = b_k / sigma_k and
+// v_k = B^T u_k / sigma_k from the original slice (no V accumulation, so the slice alone
+// must fit in shared memory: r1 x r2 <= ~27 000 doubles).  The kept triplets are
+// compacted after a host prefix sum over the r3 counts; the lift is two DMMA GEMMs
+// (Z1 U, Z2 V) and a column gather of Z3.
+#include <algorithm>
+#include <cmath>
+#include <vector>
+
+#include "gemm.cuh"
+#include "result.h"
+
+namespace rhosvd {
+
+constexpr int T2C_THREADS = 256;
+constexpr int T2C_MAX_SWEEPS = 40;
+
+__device__ __forceinline__ int t2c_rr(int pos, int step, int m) {
+  return pos == 0 ? 0 : 1 + (pos - 1 + step) % (m - 1);
+}
+
+struct T2CParams {
+  const double* Bt;    // slice-major copy of beta: Bt[(m r1 + a) r2 + b] = beta[a][b][m]
+  int r1, r2, r3, ldb;  // ldb: smem column pitch (odd)
+  double thr, tol;
+  double* Us;     // per slice: r2 columns of length r1 (u_k, descending sigma)
+  double* Vs;     // per slice: r2 columns of length r2 (v_k)
+  double* sg;     // per slice: r2 sigma (descending)
+  int* cnt;       // per slice: kept count p_m
+  int* sweeps;    // per slice: sweeps used (-1: not converged)
+  double* drop;   // per slice: discarded energy sum_{k > p_m} sigma_k^2 (smallest first)
+};
+
+__global__ void __launch_bounds__(T2C_THREADS) t2c_slice_kernel(T2CParams p) {
+  extern __shared__ double sb[];  // B (col-major, pitch ldb) | sigma | order
+  const int r1 = p.r1, r2 = p.r2, ld = p.ldb;
+  const int m2 = r2 + (r2 & 1);  // even number of columns for the tournament
+  double* B = sb;
+  double* sig = B + (size_t)ld * m2;
+  int* ord = reinterpret_cast<int*>(sig + m2);
+  __shared__ int srot;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = T2C_THREADS / 32;
+  for (int m = blockIdx.x; m < p.r3; m += gridDim.x) {
+    // B_m[a][b] = beta[a][b][m], stored column b contiguous; padded column zero
+    const double* Bm = p.Bt + (size_t)m * r1 * r2;
+    for (int e = tid; e < ld * m2; e += T2C_THREADS) {
+      const int a = e % ld, b = e / ld;
+      B[e] = (a < r1 && b < r2) ? Bm[(size_t)a * r2 + b] : 0.0;
+    }
+    __syncthreads();
+    // ||B||_F^2 (fixed order): columns with ||b||^2 <= (16 u ||B||_F)^2 are numerically zero
+    // and never rotate (their pair cosines are rounding noise)
+    __shared__ double sfro;
+    if (warp == 0) {
+      double s = 0.0;
+      for (int e = lane; e < ld * m2; e += 32) s = fma(B[e], B[e], s);
+      s = warp_sum(s);
+      if (lane == 0) sfro = s;
+    }
+    __syncthreads();
+    const double tiny2 = 256.0 * 1.2325951644078309e-32 * sfro;
+    int sw = 0;
+    bool conv = false;
+    for (; sw < T2C_MAX_SWEEPS && !conv; ++sw) {
+      if (tid == 0) srot = 0;
+      __syncthreads();
+      for (int st = 0; st < m2 - 1; ++st) {
+        for (int k = warp; k < m2 / 2; k += nw) {
+          int c1 = t2c_rr(k, st, m2), c2 = t2c_rr(m2 - 1 - k, st, m2);
+          const int pc = min(c1, c2), qc = max(c1, c2);
+          double* bp = B + (size_t)pc * ld;
+          double* bq = B + (size_t)qc * ld;
+          double al = 0.0, be = 0.0, ga = 0.0;
+          for (int i = lane; i < r1; i += 32) {
+            const double x = bp[i], y = bq[i];
+            al = fma(x, x, al);
+            be = fma(y, y, be);
+            ga = fma(x, y, ga);
+          }
+          al = warp_sum(al);
+          be = warp_sum(be);
+          ga = warp_sum(ga);
+          if (al > tiny2 && be > tiny2 && fabs(ga) > p.tol * sqrt(al * be)) {
+            // Hestenes rotation annihilating b_p^T b_q
+            const double zeta = (be - al) / (2.0 * ga);
+            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double c = rsqrt(1.0 + t * t), s = c * t;
+            for (int i = lane; i < r1; i += 32) {
+              const double x = bp[i], y = bq[i];
+              bp[i] = c * x - s * y;
+              bq[i] = s * x + c * y;
+            }
+            if (lane == 0) atomicAdd(&srot, 1);
+          }
+        }
+        __syncthreads();
+      }
+      conv = (srot == 0);
+      __syncthreads();
+    }
+    // sigma_k = ||b_k|| (fixed-order warp reductions)
+    for (int k = warp; k < r2; k += nw) {
+      double s = 0.0;
+      for (int i = lane; i < r1; i += 32) s = fma(B[(size_t)k * ld + i], B[(size_t)k * ld + i], s);
+      s = warp_sum(s);
+      if (lane == 0) sig[k] = sqrt(s);
+    }
+    __syncthreads();
+    // descending order (ties: lower column first)
+    for (int k = tid; k < r2; k += T2C_THREADS) {
+      const double v = sig[k];
+      int r = 0;
+      for (int j = 0; j < r2; ++j) r += (sig[j] > v) || (sig[j] == v && j < k);
+      ord[r] = k;
+    }
+    __syncthreads();
+    double* Us = p.Us + (size_t)m * r2 * r1;
+    double* Vs = p.Vs + (size_t)m * r2 * r2;
+    double* sg = p.sg + (size_t)m * r2;
+    int keep = 0;
+    for (int j = 0; j < r2; ++j) keep += sig[ord[j]] > p.thr;  // same value in every thread
+    // kept triplets, one warp each: u = b / sigma with the sign rule (largest-|.| entry of u
+    // positive, lowest index on ties); v = B_orig^T u / sigma from the original slice
+    // (coalesced rows of Bt), renormalised (its direction error is ~u sigma_1 / sigma)
+    for (int j = warp; j < keep; j += nw) {
+      const int k = ord[j];
+      const double s = sig[k], inv = 1.0 / s;
+      const double* bk = B + (size_t)k * ld;
+      double best = -1.0;
+      int bi = 0x7fffffff;
+      for (int i = lane; i < r1; i += 32) {
+        const double a = fabs(bk[i]);
+        if (a > best || (a == best && i < bi)) {
+          best = a;
+          bi = i;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      const double sgn = (bk[bi] < 0.0) ? -inv : inv;
+      double* uo = Us + (size_t)j * r1;
+      for (int i = lane; i < r1; i += 32) uo[i] = sgn * bk[i];
+      double* vo = Vs + (size_t)j * r2;
+      double vn = 0.0;
+      for (int b = lane; b < r2; b += 32) {
+        double acc = 0.0;
+        for (int a = 0; a < r1; ++a) acc = fma(Bm[(size_t)a * r2 + b], bk[a], acc);
+        acc *= sgn * inv;  // B^T u / sigma with u = sgn * b_k
+        vo[b] = acc;
+        vn = fma(acc, acc, vn);
+      }
+      vn = warp_sum(vn);
+      const double rv = vn > 0.0 ? 1.0 / sqrt(vn) : 0.0;
+      __syncwarp();
+      for (int b = lane; b < r2; b += 32) vo[b] *= rv;
+      if (lane == 0) sg[j] = s;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      p.cnt[m] = keep;
+      p.sweeps[m] = conv ? sw : -1;
+      double d = 0.0;
+      for (int j = r2 - 1; j >= keep; --j) d = fma(sig[ord[j]], sig[ord[j]], d);
+      p.drop[m] = d;
+    }
+    __syncthreads();
+  }
+}
+
+// Bt[(m r1 + a) r2 + b] = beta[(a r2 + b) r3 + m]  (slice-major copy)
+__global__ void t2c_transpose_kernel(const double* beta, int r1, int r2, int r3, double* Bt) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tot = (int64_t)r1 * r2 * r3;
+  if (e >= tot) return;
+  const int64_t ab = e / r3;
+  const int m = (int)(e % r3);
+  Bt[(int64_t)m * r1 * r2 + ab] = beta[e];
+}
+
+// compaction: term t of slice m -> column off[m] + t
+__global__ void t2c_compact_kernel(const double* Us, const double* Vs, const double* sg, const int* cnt,
+                                   const int64_t* off, int r1, int r2, int r3, double* Uc, int64_t ldu,
+                                   double* Vc, int64_t ldv, double* w, int* slice) {
+  const int m = blockIdx.x;
+  if (m >= r3) return;
+  const int keep = cnt[m];
+  const int64_t o = off[m];
+  for (int e = threadIdx.x; e < keep * (r1 + r2 + 1); e += blockDim.x) {
+    const int j = e / (r1 + r2 + 1), i = e % (r1 + r2 + 1);
+    if (i < r1) Uc[(o + j) * ldu + i] = Us[((size_t)m * r2 + j) * r1 + i];
+    else if (i < r1 + r2) Vc[(o + j) * ldv + (i - r1)] = Vs[((size_t)m * r2 + j) * r2 + (i - r1)];
+    else {
+      w[o + j] = sg[(size_t)m * r2 + j];
+      slice[o + j] = m;
+    }
+  }
+}
+
+// F3[:, j] = Z3[:, slice[j]]
+__global__ void t2c_gather_kernel(const double* Z3, int64_t ldz, int n, const int* slice, int64_t R, double* F3,
+                                  int64_t ldf) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= (int64_t)n * R) return;
+  const int64_t j = e / n;
+  const int i = (int)(e % n);
+  F3[j * ldf + i] = Z3[(int64_t)slice[j] * ldz + i];
+}
+
+}  // namespace rhosvd
+
+using namespace rhosvd;
+
+struct rhosvd_cp {
+  int64_t R = 0, n = 0, ldf = 0;
+  int32_t r[3] = {0, 0, 0};
+  double* F[3] = {nullptr, nullptr, nullptr};   // n x R, col-major, ld ldf
+  double* Ucore = nullptr;                      // r1 x R (ld ldu)
+  double* Vcore = nullptr;                      // r2 x R (ld ldv)
+  int64_t ldu = 0, ldv = 0;
+  double* w = nullptr;
+  int* slice = nullptr;
+  double eps = 0, thr = 0, err2 = 0;
+  int max_sweeps = 0;
+};
+
+static void cp_release(rhosvd_cp* c) {
+  if (!c) return;
+  for (int l = 0; l < 3; ++l) cudaFree(c->F[l]);
+  cudaFree(c->Ucore);
+  cudaFree(c->Vcore);
+  cudaFree(c->w);
+  cudaFree(c->slice);
+  delete c;
+}
+
+extern "C" {
+
+int rhosvd_t2c(const rhosvd_result* res, double eps_rel, rhosvd_stream stream, rhosvd_cp** out) {
+  if (!out) return fail(RHOSVD_EINVAL, "out is null");
+  *out = nullptr;
+  if (!res || !(eps_rel >= 0.0 && eps_rel < 1.0)) return fail(RHOSVD_EINVAL, "t2c: need a result and 0 <= eps < 1");
+  cudaStream_t st = (cudaStream_t)stream;
+  const int r1 = res->ranks[0], r2 = res->ranks[1], r3 = res->ranks[2];
+  auto* cp = new rhosvd_cp();
+  cp->n = res->n;
+  cp->r[0] = r1; cp->r[1] = r2; cp->r[2] = r3;
+  cp->eps = eps_rel * res->rep.beta_norm;
+  const int q = std::min(r1, r2);
+  cp->thr = (r3 > 0 && q > 0) ? cp->eps / (r3 * std::sqrt((double)q)) : 0.0;
+  const int64_t ldf = round_up(std::max<int64_t>(res->n, 1), 16);
+  cp->ldf = ldf;
+  if ((int64_t)r1 * r2 * r3 == 0) {
+    *out = cp;
+    return RHOSVD_OK;
+  }
+  const int ldb = r1 | 1;
+  const int m2 = r2 + (r2 & 1);
+  const size_t smem = ((size_t)ldb * m2 + m2) * sizeof(double) + (size_t)m2 * sizeof(int) + 64;
+  if (smem > 220 * 1024) {
+    cp_release(cp);
+    return fail(RHOSVD_EINVAL, "t2c: core slices of " + std::to_string(r1) + " x " + std::to_string(r2) +
+                                   " do not fit the shared-memory slice kernel (r1 r2 <= ~27000)");
+  }
+  // per-slice scratch
+  double *Us = nullptr, *Vs = nullptr, *sg = nullptr, *drop = nullptr, *Bt = nullptr;
+  int *cnt = nullptr, *sweeps = nullptr;
+  int64_t* off = nullptr;
+  auto cleanup = [&]() {
+    cudaFree(Us); cudaFree(Vs); cudaFree(sg); cudaFree(cnt); cudaFree(sweeps); cudaFree(off); cudaFree(drop); cudaFree(Bt);
+  };
+  if (cudaMalloc(&Us, (size_t)r3 * r2 * r1 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&Vs, (size_t)r3 * r2 * r2 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&sg, (size_t)r3 * r2 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&cnt, (size_t)r3 * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&sweeps, (size_t)r3 * sizeof(int)) != cudaSuccess ||
+      cudaMalloc(&off, (size_t)r3 * sizeof(int64_t)) != cudaSuccess ||
+      cudaMalloc(&drop, (size_t)r3 * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&Bt, (size_t)r1 * r2 * r3 * sizeof(double)) != cudaSuccess) {
+    cudaGetLastError();
+    cleanup();
+    cp_release(cp);
+    return fail(RHOSVD_ENOMEM, "t2c scratch");
+  }
+  // one-sided Jacobi stopping rule |b_p^T b_q| <= tol ||b_p|| ||b_q||, tol = 4 sqrt(r1) u
+  const double tol = 4.0 * std::sqrt((double)std::max(r1, 1)) * 1.1102230246251565e-16;
+  {
+    const int64_t tot = (int64_t)r1 * r2 * r3;
+    t2c_transpose_kernel<<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(res->beta, r1, r2, r3, Bt);
+  }
+  T2CParams tp{Bt, r1, r2, r3, ldb, cp->thr, tol, Us, Vs, sg, cnt, sweeps, drop};
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(t2c_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+  (void)attr;
+  t2c_slice_kernel<<<std::min(r3, 4 * num_sms()), T2C_THREADS, smem, st>>>(tp);
+  cudaError_t e = cudaGetLastError();
+  std::vector<int> hc(r3), hs(r3);
+  std::vector<double> hd(r3);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hc.data(), cnt, r3 * sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hd.data(), drop, r3 * sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(hs.data(), sweeps, r3 * sizeof(int), cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) {
+    cleanup();
+    cp_release(cp);
+    return fail(RHOSVD_ECUDA, std::string("t2c slice kernel: ") + cudaGetErrorString(e));
+  }
+  std::vector<int64_t> ho(r3);
+  int64_t R = 0;
+  for (int m = 0; m < r3; ++m) {
+    ho[m] = R;
+    R += hc[m];
+    if (hs[m] < 0) {
+      cleanup();
+      cp_release(cp);
+      return fail(RHOSVD_ENOCONV, "t2c: one-sided Jacobi did not converge on slice " + std::to_string(m));
+    }
+    cp->max_sweeps = std::max(cp->max_sweeps, hs[m]);
+  }
+  cp->R = R;
+  // exact error^2 (the slices are orthogonal in mode 3): the discarded energy, summed in slice order
+  cp->err2 = 0.0;
+  for (int m = 0; m < r3; ++m) cp->err2 += hd[m];
+  cp->ldu = round_up(std::max(r1, 2), 2);
+  cp->ldv = round_up(std::max(r2, 2), 2);
+  const int64_t Rm = std::max<int64_t>(R, 1);
+  bool ok = cudaMalloc(&cp->Ucore, (size_t)cp->ldu * Rm * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&cp->Vcore, (size_t)cp->ldv * Rm * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&cp->w, (size_t)Rm * sizeof(double)) == cudaSuccess &&
+            cudaMalloc(&cp->slice, (size_t)Rm * sizeof(int)) == cudaSuccess;
+  for (int l = 0; l < 3 && ok; ++l) ok = cudaMalloc(&cp->F[l], (size_t)ldf * Rm * sizeof(double)) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    cleanup();
+    cp_release(cp);
+    return fail(RHOSVD_ENOMEM, "t2c outputs");
+  }
+  e = cudaMemsetAsync(cp->Ucore, 0, (size_t)cp->ldu * Rm * sizeof(double), st);
+  if (e == cudaSuccess) e = cudaMemsetAsync(cp->Vcore, 0, (size_t)cp->ldv * Rm * sizeof(double), st);
+  if (e == cudaSuccess) e = cudaMemcpyAsync(off, ho.data(), r3 * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+  if (e != cudaSuccess) {
+    cleanup();
+    cp_release(cp);
+    return fail(RHOSVD_ECUDA, cudaGetErrorString(e));
+  }
+  if (R > 0) {
+    t2c_compact_kernel<<<r3, 256, 0, st>>>(Us, Vs, sg, cnt, off, r1, r2, r3, cp->Ucore, cp->ldu, cp->Vcore,
+                                           cp->ldv, cp->w, cp->slice);
+    // lift: F1 = Z1 U, F2 = Z2 V (DMMA GEMMs), F3 = Z3[:, slice]
+    Scratch scr;
+    const int rr[2] = {r1, r2};
+    double* core_f[2] = {cp->Ucore, cp->Vcore};
+    const int64_t ldc[2] = {cp->ldu, cp->ldv};
+    for (int l = 0; l < 2; ++l) {
+      GemmArgs g;
+      g.M = res->n; g.N = R; g.K = rr[l];
+      g.A = res->Z[l]; g.lda = res->ldz; g.a_k = false;
+      g.B = core_f[l]; g.ldb = ldc[l]; g.b_k = true;
+      g.C = cp->F[l]; g.ldc = ldf;
+      int s = gemm(g, scr, st);
+      if (s != RHOSVD_OK) {
+        std::string msg = rhosvd_last_error();
+        scr.release(st);
+        cleanup();
+        cp_release(cp);
+        return fail(s, msg);
+      }
+    }
+    t2c_gather_kernel<<<(unsigned)cdiv(res->n * R, 256), 256, 0, st>>>(res->Z[2], res->ldz, (int)res->n, cp->slice,
+                                                                      R, cp->F[2], ldf);
+    e = cudaStreamSynchronize(st);
+    scr.release(st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      cleanup();
+      cp_release(cp);
+      return fail(RHOSVD_ECUDA, std::string("t2c lift: ") + cudaGetErrorString(e));
+    }
+  }
+  cudaStreamSynchronize(st);
+  cleanup();
+  *out = cp;
+  return RHOSVD_OK;
+}
+
+int rhosvd_cp_rank(const rhosvd_cp* cp, int64_t* R) {
+  if (!cp || !R) return fail(RHOSVD_EINVAL, "null");
+  *R = cp->R;
+  return RHOSVD_OK;
+}
+int rhosvd_cp_factor(const rhosvd_cp* cp, int mode, const double** F, int64_t* ld) {
+  if (!cp || !F || !ld || mode < 0 || mode > 2) return fail(RHOSVD_EINVAL, "bad args");
+  *F = cp->F[mode];
+  *ld = cp->ldf;
+  return RHOSVD_OK;
+}
+int rhosvd_cp_core_factor(const rhosvd_cp* cp, int mode, const double** F, int64_t* ld) {
+  if (!cp || !F || !ld || mode < 0 || mode > 1) return fail(RHOSVD_EINVAL, "bad args");
+  *F = mode == 0 ? cp->Ucore : cp->Vcore;
+  *ld = mode == 0 ? cp->ldu : cp->ldv;
+  return RHOSVD_OK;
+}
+int rhosvd_cp_weights(const rhosvd_cp* cp, const double** w, const int32_t** slice) {
+  if (!cp || !w || !slice) return fail(RHOSVD_EINVAL, "bad args");
+  *w = cp->w;
+  *slice = cp->slice;
+  return RHOSVD_OK;
+}
+int rhosvd_cp_info(const rhosvd_cp* cp, double* eps_abs, double* thr, double* err2, int32_t* max_sweeps) {
+  if (!cp || !eps_abs || !thr || !err2 || !max_sweeps) return fail(RHOSVD_EINVAL, "bad args");
+  *eps_abs = cp->eps;
+  *thr = cp->thr;
+  *err2 = cp->err2;
+  *max_sweeps = cp->max_sweeps;
+  return RHOSVD_OK;
+}
+void rhosvd_cp_free(rhosvd_cp* cp) {
+  cudaDeviceSynchronize();
+  cp_release(cp);
+}
+
+}  // extern "C"

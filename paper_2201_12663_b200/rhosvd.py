@@ -83,6 +83,13 @@ def lib():
         "rhosvd_syevj": (C.c_int, [I64, P, I64, P, P, I64, D, C.POINTER(I32), P]),
         "rhosvd_core": (C.c_int, [P, P, P, I64, P, I64, I64, I64, I64, P, P]),
         "rhosvd_chol_inv": (C.c_int, [I64, P, I64, D, P, I64, P]),
+        "rhosvd_t2c": (C.c_int, [P, D, P, C.POINTER(P)]),
+        "rhosvd_cp_rank": (C.c_int, [P, C.POINTER(I64)]),
+        "rhosvd_cp_factor": (C.c_int, [P, C.c_int, C.POINTER(P), C.POINTER(I64)]),
+        "rhosvd_cp_core_factor": (C.c_int, [P, C.c_int, C.POINTER(P), C.POINTER(I64)]),
+        "rhosvd_cp_weights": (C.c_int, [P, C.POINTER(P), C.POINTER(P)]),
+        "rhosvd_cp_info": (C.c_int, [P, C.POINTER(D), C.POINTER(D), C.POINTER(D), C.POINTER(I32)]),
+        "rhosvd_cp_free": (None, [P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -97,7 +104,8 @@ EXPORTED = ["rhosvd_opts_default", "rhosvd_c2t", "rhosvd_result_ranks", "rhosvd_
             "rhosvd_result_report", "rhosvd_result_free", "rhosvd_last_error", "rhosvd_version",
             "rhosvd_nccl_get_unique_id", "rhosvd_comm_init_nccl", "rhosvd_comm_init_callback",
             "rhosvd_comm_destroy", "rhosvd_gram", "rhosvd_dgemm", "rhosvd_syevj", "rhosvd_core",
-            "rhosvd_chol_inv"]
+            "rhosvd_chol_inv", "rhosvd_t2c", "rhosvd_cp_rank", "rhosvd_cp_factor", "rhosvd_cp_core_factor",
+            "rhosvd_cp_weights", "rhosvd_cp_info", "rhosvd_cp_free"]
 
 
 def _check(status):
@@ -330,6 +338,71 @@ def c2t(U, xi, eps=None, ranks=None, comm: Comm | None = None, stream=None, keep
         return Result(ranks=ranks_, Z=Zs, sigma=sig, beta=beta, W=Ws if keep_w else None,
                       report=_report_dict(rep))
     finally:
+        L.rhosvd_result_free(h)
+
+
+@dataclass
+class CPResult:
+    """C2C output: A ~ sum_j w_j F1[:, j] (x) F2[:, j] (x) F3[:, j] (unit factor columns)."""
+    R: int
+    F: list            # torch (n, R) x 3
+    w: object          # torch (R,)
+    slice_of: object   # torch (R,) int32: mode-3 slice of each term
+    U: object          # torch (r1, R) core-space left factors u_j
+    V: object          # torch (r2, R) core-space right factors v_j
+    eps: float         # absolute eps = eps_rel ||beta||
+    thr: float         # singular-value threshold eps / (r3 sqrt(min(r1, r2)))
+    err2: float        # ||beta - beta_(R)||^2 (discarded energy)
+    sweeps: int        # largest one-sided Jacobi sweep count over the slices
+    c2t: Result = None
+
+
+def c2c(U, xi, t2c_eps, eps=None, ranks=None, comm: Comm | None = None, stream=None, **kw):
+    """Canonical-to-canonical rank reduction C2C = T2C o C2T (PAPER.md 2.3, Remark 2.1):
+    rhosvd_c2t, then rhosvd_t2c of its core within t2c_eps * ||beta||_F, lifted through
+    the frames."""
+    import torch
+    opts = make_opts(eps=eps, ranks=ranks, **kw)
+    L = lib()
+    h = c2t_raw(U, xi, opts, comm, stream)
+    cp = C.c_void_p()
+    dev = U[0].device
+    try:
+        with torch.cuda.device(dev):
+            _check(L.rhosvd_t2c(h, float(t2c_eps), _stream_ptr(stream), C.byref(cp)))
+        torch.cuda.synchronize(dev)
+        R = C.c_int64()
+        _check(L.rhosvd_cp_rank(cp, C.byref(R)))
+        R = int(R.value)
+        n = U[0].shape[1]
+        F = []
+        for l in range(3):
+            fp, ld = C.c_void_p(), C.c_int64()
+            _check(L.rhosvd_cp_factor(cp, l, C.byref(fp), C.byref(ld)))
+            F.append(_wrap_dev(fp.value, int(ld.value) * R, dev).view(R, int(ld.value))[:, :n].t() if R
+                     else torch.empty(n, 0, dtype=torch.float64, device=dev))
+        core = []
+        r = (C.c_int32 * 3)()
+        _check(L.rhosvd_result_ranks(h, r))
+        for l in range(2):
+            fp, ld = C.c_void_p(), C.c_int64()
+            _check(L.rhosvd_cp_core_factor(cp, l, C.byref(fp), C.byref(ld)))
+            rl = int(r[l])
+            core.append(_wrap_dev(fp.value, int(ld.value) * R, dev).view(R, int(ld.value))[:, :rl].t() if R
+                        else torch.empty(rl, 0, dtype=torch.float64, device=dev))
+        wp, sp = C.c_void_p(), C.c_void_p()
+        _check(L.rhosvd_cp_weights(cp, C.byref(wp), C.byref(sp)))
+        w = _wrap_dev(wp.value, R, dev)
+        sl = torch.empty(R, dtype=torch.int32, device=dev)
+        if R:
+            _memcpy(sl.data_ptr(), sp.value, R * 4, 3)
+        e, t, e2, sw = C.c_double(), C.c_double(), C.c_double(), C.c_int32()
+        _check(L.rhosvd_cp_info(cp, C.byref(e), C.byref(t), C.byref(e2), C.byref(sw)))
+        return CPResult(R=R, F=F, w=w, slice_of=sl, U=core[0], V=core[1], eps=e.value, thr=t.value,
+                        err2=e2.value, sweeps=int(sw.value))
+    finally:
+        if cp.value:
+            L.rhosvd_cp_free(cp)
         L.rhosvd_result_free(h)
 
 

@@ -1,0 +1,108 @@
+"""T2C / C2C on the GPU (rhosvd_t2c through the C ABI) against the T2C oracle
+(oracle/t2c_oracle.py, Remark 2.1) applied to the SAME core beta
+(the library is deterministic: rhosvd.c2t and rhosvd.c2c return bitwise-identical
+cores), so the comparison isolates the T2C step:
+  * identical per-slice kept counts p_m and total rank R (integer, exact) unless the
+    oracle flags a singular value within 1e-8 of the threshold;
+  * kept sigma within 1e-12 sigma_1(B_m) + 1e-10 sigma (one-sided Jacobi vs LAPACK);
+  * beta_(R) from the GPU factors equal to the oracle's within 1e-11 ||beta||;
+  * ||beta - beta_(R)|| <= eps and err2 equal to the oracle's discarded energy;
+  * lifted factors: unit columns, F1 = Z1 u, F2 = Z2 v, F3 = Z3 e_slice.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+from oracle.t2c_oracle import t2c as oracle_t2c, t2c_dense  # noqa: E402
+from workloads import make_config, make_params, make_random_params  # noqa: E402
+
+
+@pytest.fixture(scope="module")
+def rh():
+    from paper_2201_12663_b200 import rhosvd
+    rhosvd.lib()
+    return rhosvd
+
+
+def dev_inputs(p):
+    U1, U2, U3, xi = make_config(p, backend="torch", device=torch.device("cuda"))
+    return [U1, U2, U3], xi
+
+
+def beta_from_gpu(cp, shape):
+    r1, r2, r3 = shape
+    U = cp.U.cpu().numpy()
+    V = cp.V.cpu().numpy()
+    w = cp.w.cpu().numpy()
+    sl = cp.slice_of.cpu().numpy()
+    out = np.zeros(shape)
+    for j in range(cp.R):
+        out[:, :, sl[j]] += w[j] * np.outer(U[:, j], V[:, j])
+    return out
+
+
+def check_case(rh, Us, xi, eps, ranks, t2c_eps):
+    g = rh.c2t(Us, xi, eps=eps, ranks=ranks, keep_w=False)
+    beta = g.beta.cpu().numpy()
+    cp = rh.c2c(Us, xi, t2c_eps, eps=eps, ranks=ranks)
+    o = oracle_t2c(beta, t2c_eps * np.linalg.norm(beta))
+    assert abs(cp.thr - o.thr) <= 1e-12 * o.thr
+    if not o.near_tie:
+        assert cp.R == o.sigma.shape[0]
+        sl = cp.slice_of.cpu().numpy()
+        assert np.array_equal(np.bincount(sl, minlength=beta.shape[2]), o.p)
+        w = cp.w.cpu().numpy()
+        for m in range(beta.shape[2]):
+            s1 = np.linalg.norm(beta[:, :, m], 2)
+            wg, wo = w[sl == m], o.sigma[o.slice_of == m]
+            assert np.all(np.abs(wg - wo) <= 1e-12 * s1 + 1e-10 * wo)
+    bR = beta_from_gpu(cp, beta.shape)
+    nb = np.linalg.norm(beta)
+    assert np.linalg.norm(bR - t2c_dense(o, beta.shape)) <= 1e-11 * nb
+    err = np.linalg.norm(beta - bR)
+    assert err <= cp.eps * (1 + 1e-12) + 1e-12 * nb  # + rounding (columns below 16 u ||B|| are zero)
+    assert abs(cp.err2 - o.err2) <= 1e-10 * o.err2 + 1e-13 * nb ** 2
+    # lifted factors
+    Z = [z.cpu().numpy() for z in g.Z]
+    F = [f.cpu().numpy() for f in cp.F]
+    sl = cp.slice_of.cpu().numpy()
+    assert np.allclose(F[0], Z[0] @ cp.U.cpu().numpy(), atol=1e-13)
+    assert np.allclose(F[1], Z[1] @ cp.V.cpu().numpy(), atol=1e-13)
+    assert np.array_equal(F[2], Z[2][:, sl])
+    for f in F:
+        if f.shape[1]:
+            assert np.max(np.abs(np.linalg.norm(f, axis=0) - 1.0)) <= 1e-12
+    return cp, o
+
+
+@pytest.mark.parametrize("n,R,seed,eps,ranks,t2c_eps", [
+    (30, 200, 1, None, (8, 9, 7), 1e-4),
+    (48, 300, 2, 1e-6, None, 1e-6),
+    (40, 257, 3, 1e-5, None, 0.0),
+    (64, 500, 4, None, (33, 17, 40), 1e-3),
+])
+def test_t2c_random(rh, n, R, seed, eps, ranks, t2c_eps):
+    p = make_random_params(n, R, seed=seed, eps=eps, ranks=ranks)
+    Us, xi = dev_inputs(p)
+    cp, o = check_case(rh, Us, xi, p.eps, p.ranks, t2c_eps)
+    if t2c_eps == 0.0:  # exact: every slice keeps its numerical rank
+        assert cp.err2 <= 1e-20 * np.sum(o.sigma ** 2) + 1e-300
+
+
+@pytest.mark.parametrize("k,t2c_eps", [(1, 1e-6), (3, 1e-6), (5, 1e-5)])
+def test_t2c_baseline_configs(rh, k, t2c_eps):
+    """cfg 1 (r = 10), cfg 3 (r ~ 130), cfg 5 (r = 108): slices fit shared memory."""
+    p = make_params(k)
+    Us, xi = dev_inputs(p)
+    cp, o = check_case(rh, Us, xi, p.eps, p.ranks, t2c_eps)
+    r1, r2, r3 = cp.U.shape[0], cp.V.shape[0], len(o.p)
+    assert cp.R <= r3 * min(r1, r2)
+
+
+def test_t2c_rejects_slices_too_large(rh):
+    p = make_random_params(400, 600, seed=5, ranks=(170, 170, 4))
+    Us, xi = dev_inputs(p)
+    with pytest.raises(Exception, match="shared-memory"):
+        rh.c2c(Us, xi, 1e-6, ranks=p.ranks)
