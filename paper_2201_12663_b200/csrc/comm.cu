@@ -64,6 +64,11 @@ int comm_allreduce(rhosvd_comm* c, double* p, int64_t count, cudaStream_t st) {
   if (e != cudaSuccess) return fail(RHOSVD_ECUDA, cudaGetErrorString(e));
   int r = c->fn(p, count, (rhosvd_stream)st, c->user);
   if (r != 0) return fail(RHOSVD_ENCCL, "callback all-reduce failed: " + std::to_string(r));
+  // the callback may copy back with a synchronous cudaMemcpy from pageable memory, which can
+  // return before the DMA lands and is ordered only on the legacy stream: make the result
+  // visible to work queued on `st` (a non-blocking stream) before continuing
+  e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return fail(RHOSVD_ECUDA, cudaGetErrorString(e));
   return RHOSVD_OK;
 }
 

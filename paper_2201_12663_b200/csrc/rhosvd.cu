@@ -20,6 +20,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <memory>
+#include <condition_variable>
 #include <thread>
 #include <array>
 #include <mutex>
@@ -217,6 +219,77 @@ struct PhaseTimer {
 };
 enum { PH_NORM = 0, PH_GRAM = 1, PH_EIG = 2, PH_RR = 3, PH_RANK = 4, PH_PROJ = 5, PH_CORE = 6, PH_COMM = 7 };
 
+// Collective scheduler for the concurrent per-mode eigensolves on a multi-rank
+// communicator.  One communicator must not be driven by two threads, and the ranks must
+// issue their collectives in the same order; so the mode threads post their all-reduces
+// here and ONE comm thread executes them in a fixed round-robin order over the modes
+// (mode 0's k-th, mode 1's k-th, mode 2's k-th, mode 0's (k+1)-th, ...; a finished mode
+// is skipped).  Every rank runs the same deterministic sequence of collectives per mode
+// (identical reduced inputs), so the global order is identical on all ranks.
+static bool comm_trace() {
+  static const bool on = [] {
+    const char* e = getenv("RHOSVD_COMM_TRACE");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
+struct CommSched {
+  rhosvd_comm* comm = nullptr;
+  std::mutex mu;
+  std::condition_variable cv;
+  struct Req {
+    double* p = nullptr;
+    int64_t count = 0;
+    cudaStream_t st = nullptr;
+    bool posted = false, done = false, finished = false;
+    int status = RHOSVD_OK;
+    std::string err;
+  } req[3];
+  int dev = 0;
+  // mode thread: run one all-reduce through the comm thread (blocks until done)
+  int post(int mode, double* p, int64_t count, cudaStream_t st) {
+    std::unique_lock<std::mutex> lk(mu);
+    Req& r = req[mode];
+    r.p = p; r.count = count; r.st = st; r.done = false; r.posted = true;
+    cv.notify_all();
+    cv.wait(lk, [&] { return r.done; });
+    if (r.status != RHOSVD_OK) set_error(r.err);
+    return r.status;
+  }
+  void finish(int mode) {
+    std::lock_guard<std::mutex> lk(mu);
+    req[mode].finished = true;
+    cv.notify_all();
+  }
+  // comm thread
+  void run() {
+    cudaSetDevice(dev);
+    int l = 0;
+    std::unique_lock<std::mutex> lk(mu);
+    while (true) {
+      if (req[0].finished && req[1].finished && req[2].finished) break;
+      Req& r = req[l];
+      if (!r.finished) {
+        cv.wait(lk, [&] { return r.posted || r.finished; });
+        if (r.posted) {
+          r.posted = false;
+          if (comm_trace()) fprintf(stderr, "[rhosvd comm exec] rank %d mode %d count %lld\n", comm->rank, l, (long long)r.count);
+          lk.unlock();
+          int s = comm_allreduce(comm, r.p, r.count, r.st);
+          std::string e = s != RHOSVD_OK ? std::string(rhosvd_last_error()) : std::string();
+          lk.lock();
+          r.status = s;
+          r.err = e;
+          r.done = true;
+          cv.notify_all();
+        }
+      }
+      l = (l + 1) % 3;
+    }
+  }
+};
+
 struct Ctx {
   cudaStream_t st;
   rhosvd_comm* comm;
@@ -225,6 +298,8 @@ struct Ctx {
   PhaseTimer* tm;
   double flops = 0.0;
   ModeWs* m = nullptr;  // per-mode buffers (S3-S5); GEMM scratch comes from here when set
+  CommSched* sched = nullptr;  // concurrent modes on a multi-rank communicator
+  int mode = 0;
 };
 
 // ------------------------------------------------------------------ GEMM shorthands
@@ -240,9 +315,10 @@ static int mm(Ctx& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
 
 static int allreduce(Ctx& c, double* p, int64_t count) {
   if (!c.comm || c.comm->world <= 1) return RHOSVD_OK;
+  if (comm_trace()) fprintf(stderr, "[rhosvd comm] rank %d mode %d count %lld\n", c.comm->rank, c.m ? c.mode : -1, (long long)count);
   c.tm->mark(PH_COMM);
-  int r = comm_allreduce(c.comm, p, count, c.st);
-  return r;
+  if (c.sched) return c.sched->post(c.mode, p, count, c.st);
+  return comm_allreduce(c.comm, p, count, c.st);
 }
 
 // RHOSVD_DEBUG=1: synchronise and scan a device array for non-finite values (debug only)
@@ -727,10 +803,18 @@ static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n
   ModeOut mo[3];
   int mst[3] = {RHOSVD_OK, RHOSVD_OK, RHOSVD_OK};
   std::string merr[3];
-  const bool concurrent = (!comm || comm->world <= 1) && modes_concurrent();
+  const bool concurrent = modes_concurrent();
   if (concurrent) {
     int dev = 0;
     RH_CUDA(cudaGetDevice(&dev));
+    std::unique_ptr<CommSched> sched;
+    std::thread comm_thread;
+    if (comm && comm->world > 1) {
+      sched.reset(new CommSched());
+      sched->comm = comm;
+      sched->dev = dev;
+      comm_thread = std::thread([&] { sched->run(); });
+    }
     cudaStream_t* ms = mode_streams();
     if (!ms) return fail(RHOSVD_ECUDA, "mode stream creation failed");
     cudaEvent_t ev0;
@@ -747,7 +831,10 @@ static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n
       mtm.mark(PH_EIG);
       Ctx cl{ms[l], comm, w, &rep, &mtm};
       cl.m = &w.mw[l];
+      cl.sched = sched.get();
+      cl.mode = l;
       mst[l] = solve_mode(cl, l, n, LDN, Rl, Rp, Rg, Uh[l], w.G.p + (size_t)l * LDN * LDN, rep.trace[l], o, mo[l]);
+      if (cl.sched) cl.sched->finish(l);
       mtm.mark(-1);
       if (mst[l] != RHOSVD_OK) merr[l] = g_err;
       mtm.collect(mphase[l]);
@@ -758,6 +845,7 @@ static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n
     run(0);
     t1.join();
     t2.join();
+    if (comm_thread.joinable()) comm_thread.join();
     g_launches += mlaunch[0] + mlaunch[1] + mlaunch[2];
     c.flops += mflops[0] + mflops[1] + mflops[2];
     // per-phase device times of the concurrent region, summed over the modes (ms[9..13]:
