@@ -54,17 +54,23 @@ def normalize(Us, xi):
 
     Us: list of d arrays of shape (R, n) (row k = u_k^(l)); xi: (R,).
     Returns (Uhat list, xi' (R,), s (d, R) column norms, T (d,) = ||Uhat_l||_F^2).
-    Zero columns stay zero and get xi'_k = 0 (reading A3).
+    Zero columns stay zero and get xi'_k = 0 (reading A3).  The 2-norm is evaluated
+    as m ||u / m||_2 with m = max_i |u_i| (the plain definition without the underflow
+    of sum u_i^2: a column with entries ~1e-200 is NOT zero).
     """
     d = len(Us)
     R = xi.shape[0]
     s = np.zeros((d, R))
     Uh = []
     for l, U in enumerate(Us):
-        sl = np.linalg.norm(U, axis=1)              # ||u_k^(l)||_2
+        mx = np.max(np.abs(U), axis=1) if U.shape[1] else np.zeros(U.shape[0])
+        safe = np.where(mx > 0, mx, 1.0)
+        Us_ = U / safe[:, None]                     # entries in [-1, 1]
+        nr = np.linalg.norm(Us_, axis=1)
+        sl = np.where(mx > 0, mx * nr, 0.0)         # ||u_k^(l)||_2
         s[l] = sl
-        inv = np.where(sl > 0, 1.0 / np.where(sl > 0, sl, 1.0), 0.0)
-        Uh.append(U * inv[:, None])
+        inv = np.where(mx > 0, 1.0 / np.where(nr > 0, nr, 1.0), 0.0)
+        Uh.append(Us_ * inv[:, None])
     xip = xi * np.prod(s, axis=0)                  # xi'_k = xi_k prod_l s_{l,k}
     T = np.array([np.sum(u * u) for u in Uh])      # T_l (reading A19)
     return Uh, xip, s, T

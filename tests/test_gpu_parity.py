@@ -209,3 +209,35 @@ def test_parity_full_size_fixture(rh, k):
             for q, c in enumerate(idx[2]):
                 terms = xip * Wt[0][:, i] * Wt[1][:, j] * Wt[2][:, q]
                 assert abs(beta[a, b, c] - terms.sum()) <= 1e-9 * np.abs(terms).sum(), (a, b, c)
+
+
+# ------------------------------------------------------------------ seeded stress sweep
+def _stress_cases():
+    rng = np.random.default_rng(20261019)
+    ns = [1, 2, 5, 17, 63, 64, 65, 127, 129, 200, 300]
+    Rs = [1, 3, 8, 50, 200, 777, 1500]
+    cases = []
+    for i in range(24):
+        n, R = int(rng.choice(ns)), int(rng.choice(Rs))
+        if rng.random() < 0.6:
+            eps, ranks = float(rng.choice([1e-2, 1e-4, 1e-7, 1e-10])), None
+        else:
+            m = min(n, R)
+            eps, ranks = None, tuple(int(x) for x in rng.integers(1, m + 3, size=3))
+        wide = bool(rng.random() < 0.5)
+        cases.append((i, n, R, eps, ranks, wide))
+    return cases
+
+
+@pytest.mark.parametrize("i,n,R,eps,ranks,wide", _stress_cases())
+def test_parity_stress(rh, i, n, R, eps, ranks, wide):
+    """24 seeded random shapes (n from 1 to 300, R from 1 to 1500, eps and fixed modes,
+    clamped ranks, narrow and wide Gaussian exponents): the same three criteria."""
+    p = make_random_params(n, R, seed=7000 + i, eps=eps, ranks=ranks,
+                           a_range=(0.05, 400.0) if wide else (0.5, 20.0), signed=bool(i % 2))
+    U1, U2, U3, xi = make_config(p)
+    o = oracle_rhosvd([U1, U2, U3], xi, eps=eps, ranks=ranks)
+    g = run_gpu(rh, [U1, U2, U3], xi, eps=eps, ranks=ranks)
+    if any(o.report["near_tie"]):
+        pytest.skip(f"oracle flags a near-tie at the cut: {o.report['margins']}")
+    compare(g, o)

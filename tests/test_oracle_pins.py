@@ -286,3 +286,15 @@ def test_empty_R():
     Us = [np.zeros((0, 5)) for _ in range(3)]
     res = rhosvd(Us, np.zeros(0), eps=1e-3)
     assert res.ranks == (0, 0, 0) and res.beta.size == 0
+
+
+def test_normalization_no_underflow():
+    """A column with entries ~1e-200 has norm ~1e-200, not 0: it is normalized to a unit
+    column and xi' = xi ||u|| (closed form; the naive sum of squares underflows)."""
+    from oracle import normalize
+    u = np.array([[3e-200, 4e-200, 0.0], [1.0, 2.0, 2.0]])
+    Uh, xip, s, T = normalize([u, u, u], np.array([1.0, 1.0]))
+    assert np.allclose(s[0], [5e-200, 3.0], rtol=1e-15)
+    assert np.allclose(Uh[0][0], [0.6, 0.8, 0.0], rtol=1e-15)
+    assert np.allclose(T, [2.0, 2.0, 2.0], rtol=1e-15)
+    assert xip[0] == 0.0 or xip[0] > 0  # (5e-200)^3 underflows to 0: the weight, not the column
