@@ -38,21 +38,37 @@ def run_gpu(rh, Us, xi, eps=None, ranks=None, **kw):
     return rh.c2t(Ud, xd, eps=eps, ranks=ranks, **kw)
 
 
-def compare(g, o, check_W=True):
+def compare(g, o, check_W=True, sig_floor=False):
+    """Ranks exact; sigma within SIG_TOL relative (with sig_floor: or 16 u sigma_1 / sigma_k,
+    the accuracy floor of ANY fp64 SVD including the oracle's - used only by the stress
+    sweep, whose eps = 1e-10 cases keep sigma_k ~ 1e-9 sigma_1); Tucker tensor within
+    TUCKER_TOL unless a cut falls inside a degenerate cluster (relative gap < 1e-8: the
+    rank-r subspace, hence the Tucker tensor, is not unique - reading A10: only the unique
+    quantities are compared and the frames are checked for validity)."""
     assert tuple(g.ranks) == tuple(o.ranks), (g.ranks, o.ranks, o.report["margins"])
+    degenerate = False
     for l in range(3):
         r = o.ranks[l]
         sg = g.sigma[l].cpu().numpy()
-        assert sigma_rel_err(sg, o.sigma[l][:r]) <= SIG_TOL, (l, sigma_rel_err(sg, o.sigma[l][:r]))
+        so = o.sigma[l][:r]
+        if sig_floor and r:
+            tol = np.maximum(SIG_TOL, 16 * 1.1102230246251565e-16 * so[0] / so)
+            assert np.all(np.abs(sg - so) <= tol * so), (l, np.max(np.abs(sg - so) / so))
+        else:
+            assert sigma_rel_err(sg, so) <= SIG_TOL, (l, sigma_rel_err(sg, so))
         Z = g.Z[l].cpu().numpy()
         assert orth_error(Z) <= ORTH_TOL, orth_error(Z)
-    Zg = [z.cpu().numpy() for z in g.Z]
-    d, nrm = tucker_diff(g.beta.cpu().numpy(), Zg, o.beta, o.Z)
-    assert d <= TUCKER_TOL * max(nrm, 1e-300), d / nrm
+        if 0 < r < o.sigma[l].shape[0] and (o.sigma[l][r - 1] - o.sigma[l][r]) <= 1e-8 * o.sigma[l][r - 1]:
+            degenerate = True
     rep = g.report
     for l in range(3):
         assert abs(rep["trace"][l] - o.T[l]) <= 1e-12 * o.T[l]
     assert abs(rep["xi_norm"] - o.report["xi_norm"]) <= 1e-12 * o.report["xi_norm"]
+    if degenerate:
+        return 0.0
+    Zg = [z.cpu().numpy() for z in g.Z]
+    d, nrm = tucker_diff(g.beta.cpu().numpy(), Zg, o.beta, o.Z)
+    assert d <= TUCKER_TOL * max(nrm, 1e-300), d / nrm
     assert abs(rep["beta_norm"] - o.report["beta_norm"]) <= 1e-12 * o.report["beta_norm"]
     if check_W and g.W is not None:
         # the CP factors of the core are Z_l^T Uhat_l (Prop. 2.1) - sign-aligned with the frames
@@ -240,4 +256,4 @@ def test_parity_stress(rh, i, n, R, eps, ranks, wide):
     g = run_gpu(rh, [U1, U2, U3], xi, eps=eps, ranks=ranks)
     if any(o.report["near_tie"]):
         pytest.skip(f"oracle flags a near-tie at the cut: {o.report['margins']}")
-    compare(g, o)
+    compare(g, o, sig_floor=True)
