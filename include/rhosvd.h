@@ -70,7 +70,7 @@ typedef struct {
   int32_t  r[3];         /* fixed mode: requested r_l >= 1 (clamped to min(n, R_global))      */
   double   eps;          /* eps mode: 0 < eps < 1, relative Frobenius tail per mode (A1)     */
   int32_t  oversample;   /* p: block size b = r + p (default 16)                             */
-  int32_t  block0;       /* eps mode: first block size (default 128); grows adaptively       */
+  int32_t  block0;       /* eps mode: first block size (0 = default 128); grows adaptively    */
   int32_t  max_iters;    /* subspace-iteration cap per block size (default 30)               */
   int32_t  refine_steps; /* non-squared refinement steps (default 1)                         */
   uint64_t seed;         /* start-block seed                                                 */

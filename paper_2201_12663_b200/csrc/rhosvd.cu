@@ -419,7 +419,11 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
   const bool epsmode = o.rank_mode == RHOSVD_EPS;
   const int64_t rfix = epsmode ? 0 : std::min<int64_t>(o.r[mode], m);
   const int p = std::max(1, o.oversample);
-  int64_t b = epsmode ? std::min<int64_t>(m, std::max(o.block0, 2 * p)) : std::min<int64_t>(m, rfix + p);
+  // eps mode: first block block0 (<= 0: 128); it grows adaptively.  (Starting at n/4 saves
+  // growth restarts but leaves the trailing Rayleigh quotients too rough to truncate the
+  // block before the non-squared steps: cfg 3/5 got slower.)
+  const int64_t b0 = o.block0 > 0 ? o.block0 : 128;
+  int64_t b = epsmode ? std::min<int64_t>(m, std::max<int64_t>(b0, 2 * p)) : std::min<int64_t>(m, rfix + p);
   const double u = 1.1102230246251565e-16;
   const double tau = 1e-13;  // Ritz-value floor relative to theta_1
   mo.T = T;
@@ -524,10 +528,14 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
   mo.iters = it_total;
   // block truncation: smallest b' >= r + p with d_b' <= 0.05 d_r (leading columns carry
   // the dominant subspaces)
+  static const double trunc_ratio = [] {
+    const char* e = getenv("RHOSVD_TRUNC_RATIO");
+    return e ? atof(e) : 0.05;
+  }();
   if (!d_h.empty() && r_est > 0 && r_est + p < b) {
     const double tr = d_h[r_est - 1];
     for (int64_t j = r_est + p; j <= b; ++j)
-      if (d_h[j - 1] <= 0.05 * tr) {
+      if (d_h[j - 1] <= trunc_ratio * tr) {
         b = j;
         break;
       }
@@ -554,7 +562,8 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
       const int64_t rr = std::min<int64_t>(r_est, b);
       const double dr = std::max(d_h[rr - 1], 1e-300), d1 = std::max(d_h[0], dr);
       const double e0 = 10.0 * u * d1 / dr;
-      const double rho = std::min(0.9, std::max(d_h[b - 1], 1e-300) / dr);
+      // d_b below the Gram-domain noise (~u d_1) says nothing about lambda_{b+1}: floor it
+      const double rho = std::min(0.9, std::max(d_h[b - 1], 64.0 * u * d1) / dr);
       int need = e0 <= 1e-11 ? 0 : (int)std::ceil(std::log(1e-11 / e0) / std::log(rho * rho));
       nref = std::max(o.refine_steps, std::min(need, o.refine_steps + 3));
       if (dbg_on())
@@ -646,7 +655,7 @@ void rhosvd_opts_default(rhosvd_opts* o) {
   o->r[0] = o->r[1] = o->r[2] = 10;
   o->eps = 1e-6;
   o->oversample = 16;
-  o->block0 = 128;
+  o->block0 = 0;  // 0: default first block (128)
   o->max_iters = 30;
   o->refine_steps = 1;
   o->seed = 12345;

@@ -716,11 +716,18 @@ void DenseWs::release(cudaStream_t st) {
   cap_b = 0;
 }
 
+// Cooperative grid size: at most the co-resident CTAs, further capped by
+// RHOSVD_COOP_MAX (the three per-mode solves run concurrently, and a cooperative kernel
+// that asks for every SM waits for all of them to be free).
 static int coop_grid(const void* kern, int threads, size_t smem, int64_t want_blocks) {
+  static const int cap = [] {
+    const char* e = getenv("RHOSVD_COOP_MAX");
+    return e ? std::max(1, atoi(e)) : 1 << 30;
+  }();
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
   if (occ < 1) occ = 1;
-  int64_t maxb = (int64_t)occ * num_sms();
+  int64_t maxb = std::min<int64_t>((int64_t)occ * num_sms(), cap);
   int64_t g = std::min<int64_t>(maxb, std::max<int64_t>(1, want_blocks));
   return (int)g;
 }
@@ -776,7 +783,7 @@ int syevj(int64_t b, const double* A, int64_t lda, double* lambda, double* Vout,
         cudaFuncSetAttribute(jacobi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     RH_CUDA(attr_b);
     int64_t want = (int64_t)bj.h * (bj.h - 1) / 2 + cdiv(bj.bp, BJ_VT) * bj.h;
-    int grid = (int)std::min<int64_t>(coop_grid((const void*)jacobi_block_kernel, threads, smem, want), num_sms());
+    int grid = coop_grid((const void*)jacobi_block_kernel, threads, smem, want);
     static const int tsm = [] {
       const char* e = getenv("RHOSVD_TS");
       return (e && e[0] == '1') ? 1 : 0;

@@ -129,7 +129,7 @@ def _need_cuda_f64(t, name):
         raise TypeError(f"{name} must be a torch.float64 CUDA tensor")
 
 
-def make_opts(eps=None, ranks=None, oversample=16, block0=128, max_iters=30, refine_steps=1,
+def make_opts(eps=None, ranks=None, oversample=16, block0=0, max_iters=30, refine_steps=1,
               seed=12345, sign_fix=True):
     o = Opts()
     lib().rhosvd_opts_default(C.byref(o))

@@ -39,7 +39,7 @@ def test_opts_default_and_struct_layout(lib):
     from paper_2201_12663_b200 import rhosvd
     o = rhosvd.Opts()
     lib.rhosvd_opts_default(ctypes.byref(o))
-    assert o.rank_mode == rhosvd.RHOSVD_EPS and o.oversample == 16 and o.block0 == 128
+    assert o.rank_mode == rhosvd.RHOSVD_EPS and o.oversample == 16 and o.block0 == 0
     assert o.refine_steps == 1 and o.flags == rhosvd.RHOSVD_F_SIGN_FIX
     assert ctypes.sizeof(rhosvd.Opts) == 56
     o2 = rhosvd.make_opts(ranks=(3, 4, 5))

@@ -17,7 +17,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--reps", type=int, default=2)
-    ap.add_argument("--block0", type=int, default=128)
+    ap.add_argument("--block0", type=int, default=0)
     ap.add_argument("--oversample", type=int, default=16)
     ap.add_argument("--t2c", type=float, default=None, help="also time rhosvd_t2c with this eps_rel")
     args = ap.parse_args()

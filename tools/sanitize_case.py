@@ -1,0 +1,29 @@
+"""Small end-to-end run for compute-sanitizer: one C2T (eps mode, ragged sizes), one T2C,
+and the kernel-level entry points."""
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+import numpy as np
+import torch
+from paper_2201_12663_b200 import rhosvd
+from workloads import make_config, make_random_params
+
+dev = torch.device("cuda")
+p = make_random_params(70, 333, seed=5, eps=1e-6)
+U1, U2, U3, xi = make_config(p, backend="torch", device=dev)
+g = rhosvd.c2t([U1, U2, U3], xi, eps=p.eps)
+cp = rhosvd.c2c([U1, U2, U3], xi, 1e-6, eps=p.eps)
+rng = np.random.default_rng(1)
+A = torch.as_tensor(rng.normal(size=(130, 67)), device=dev)
+B = torch.as_tensor(rng.normal(size=(67, 45)), device=dev)
+rhosvd.dgemm(A, B)
+S = torch.as_tensor(rng.normal(size=(200, 200)), device=dev)
+rhosvd.syevj(S + S.t())
+M = torch.as_tensor(rng.normal(size=(300, 97)), device=dev)
+rhosvd.chol_inv(M.t() @ M)
+W = [torch.as_tensor(rng.normal(size=(r, 500)), device=dev) for r in (5, 130, 97)]
+rhosvd.core(W[0], W[1], W[2], torch.as_tensor(rng.normal(size=500), device=dev))
+torch.cuda.synchronize()
+print("ok", g.ranks, cp.R)
