@@ -1,17 +1,13 @@
 // small_dense.cu - the b x b kernels of the RHOSVD eigensolver on sm_100a.
 //
-//  * syevj: parallel cyclic two-sided Jacobi (round-robin pair ordering,
-//    b/2 disjoint rotations per step) as ONE cooperative persistent kernel:
-//    every CTA recomputes all rotation parameters of a step from the current
-//    matrix (so a step needs a single grid barrier), the 2x2 block updates of
-//    A (double-buffered) and the column rotations of V are spread over the
-//    whole GPU.  Stopping rule |a_pq| <= tol sqrt(|a_pp a_qq|) (Demmel-Veselic
-//    relative criterion) gives eigenvalues of scaled-diagonally-dominant
-//    positive definite matrices to high relative accuracy - which is what the
-//    one-sided Rayleigh-Ritz on W W^T needs.
-//  * chol_inv_scaled: column-scaled (optionally shifted) Cholesky of a b x b
-//    Gram as a cooperative blocked right-looking kernel (32-wide panels, one
-//    grid barrier per panel), then the inverse of L one warp per column; the
+//  * syevj: two-sided Jacobi - a single-CTA shared-memory kernel for small b and a
+//    cooperative block Jacobi (see below) otherwise.  Stopping rule
+//    |a_pq| <= tol sqrt(|a_pp a_qq|) (Demmel-Veselic relative criterion) gives
+//    eigenvalues of scaled-diagonally-dominant positive definite matrices to high
+//    relative accuracy - which is what the one-sided Rayleigh-Ritz on W W^T needs
+//    (DESIGN.md).
+//  * chol_inv_scaled: column-scaled (optionally shifted) Cholesky of a b x b Gram and
+//    the inverse of its factor as one cooperative blocked kernel (see below); the
 //    output D L^{-T} turns M into Q = M D L^{-T} (CholeskyQR).
 #include <cooperative_groups.h>
 #include <cstdio>
@@ -48,175 +44,6 @@ struct JacParams {
   unsigned* bar;
   int* info;
 };
-
-__global__ void __launch_bounds__(512) jacobi_kernel(JacParams p) {
-  extern __shared__ double sh[];
-  const int h = p.h, b = p.b, m = p.m;
-  double* c_ = sh;
-  double* s_ = sh + h;
-  double* t_ = sh + 2 * h;
-  int* act_ = reinterpret_cast<int*>(sh + 3 * h);
-  int* pp_ = act_ + h;
-  int* qq_ = pp_ + h;
-  __shared__ int red[32];
-
-  const int64_t gtid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t gthreads = (int64_t)gridDim.x * blockDim.x;
-  const int64_t ld = p.ld;
-
-  // absolute floor relative to the largest diagonal entry (every CTA, same value)
-  __shared__ double sdmax[32];
-  {
-    double dm = 0.0;
-    for (int i = threadIdx.x; i < b; i += blockDim.x) dm = fmax(dm, fabs(p.Ain[i * p.lda + i]));
-    for (int o = 16; o > 0; o >>= 1) dm = fmax(dm, __shfl_xor_sync(0xffffffffu, dm, o));
-    if ((threadIdx.x & 31) == 0) sdmax[threadIdx.x >> 5] = dm;
-    __syncthreads();
-    dm = 0.0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) dm = fmax(dm, sdmax[w]);
-    __syncthreads();
-    if (threadIdx.x == 0) sdmax[0] = dm;
-    __syncthreads();
-  }
-  const double abstol = p.abstol * sdmax[0];
-  // init: A0 = Ain, V = I
-  for (int64_t e = gtid; e < (int64_t)b * b; e += gthreads) {
-    int i = (int)(e % b), j = (int)(e / b);
-    p.A0[j * ld + i] = p.Ain[j * p.lda + i];
-    p.V[j * ld + i] = (i == j) ? 1.0 : 0.0;
-  }
-  grid_barrier(p.bar);
-
-  double* cur = p.A0;
-  double* nxt = p.A1;
-  const int64_t nblk = (int64_t)h * (h + 1) / 2;
-  const int64_t items = nblk + (int64_t)b * h;
-  int sweeps = 0;
-  bool converged = false;
-  for (int sw = 0; sw < p.max_sweeps; ++sw) {
-    int mycount = 0;
-    for (int step = 0; step < m - 1; ++step) {
-      // ---- phase 1: every CTA computes all rotations of this step
-      for (int k = threadIdx.x; k < h; k += blockDim.x) {
-        int i1 = rr_index(k, step, m), i2 = rr_index(m - 1 - k, step, m);
-        int pq = min(i1, i2), qq = max(i1, i2);
-        pp_[k] = pq;
-        qq_[k] = qq;
-        double c = 1.0, s = 0.0, t = 0.0;
-        int act = 0;
-        if (qq < b) {
-          double app = cur[pq * ld + pq], aqq = cur[qq * ld + qq], apq = cur[qq * ld + pq];
-          double thr = fmax(abstol, p.tol * sqrt(fabs(app * aqq)));
-          if (fabs(apq) > thr) {
-            act = 1;
-            double theta = (aqq - app) / (2.0 * apq);
-            if (fabs(theta) > 1e150)
-              t = 0.5 / theta;
-            else
-              t = copysign(1.0 / (fabs(theta) + sqrt(1.0 + theta * theta)), theta);
-            if (theta == 0.0) t = 1.0;
-            c = 1.0 / sqrt(1.0 + t * t);
-            s = t * c;
-          }
-        }
-        c_[k] = c;
-        s_[k] = s;
-        t_[k] = t;
-        act_[k] = act;
-        mycount += act;
-      }
-      __syncthreads();
-      // ---- phase 2: 2x2 block updates (upper blocks, mirrored) and V rotations
-      for (int64_t it = gtid; it < items; it += gthreads) {
-        if (it < nblk) {
-          int Q = (int)((sqrt(8.0 * (double)it + 1.0) - 1.0) * 0.5);
-          while ((int64_t)(Q + 1) * (Q + 2) / 2 <= it) ++Q;
-          while ((int64_t)Q * (Q + 1) / 2 > it) --Q;
-          int P = (int)(it - (int64_t)Q * (Q + 1) / 2);  // P <= Q
-          int p1 = pp_[P], q1 = qq_[P];
-          if (P == Q) {
-            if (q1 >= b) {
-              nxt[p1 * ld + p1] = cur[p1 * ld + p1];
-            } else if (act_[P]) {
-              double app = cur[p1 * ld + p1], aqq = cur[q1 * ld + q1], apq = cur[q1 * ld + p1];
-              double t = t_[P];
-              nxt[p1 * ld + p1] = app - t * apq;
-              nxt[q1 * ld + q1] = aqq + t * apq;
-              nxt[q1 * ld + p1] = 0.0;
-              nxt[p1 * ld + q1] = 0.0;
-            } else {
-              nxt[p1 * ld + p1] = cur[p1 * ld + p1];
-              nxt[q1 * ld + q1] = cur[q1 * ld + q1];
-              double apq = cur[q1 * ld + p1];
-              nxt[q1 * ld + p1] = apq;
-              nxt[p1 * ld + q1] = apq;
-            }
-          } else {
-            int p2 = pp_[Q], q2 = qq_[Q];
-            bool vq1 = q1 < b, vq2 = q2 < b;
-            double a11 = cur[p2 * ld + p1];
-            double a12 = vq2 ? cur[q2 * ld + p1] : 0.0;
-            double a21 = vq1 ? cur[p2 * ld + q1] : 0.0;
-            double a22 = (vq1 && vq2) ? cur[q2 * ld + q1] : 0.0;
-            double c1 = c_[P], s1 = s_[P], c2 = c_[Q], s2 = s_[Q];
-            // columns (p2,q2) rotated by (c2,s2)
-            double b11 = c2 * a11 - s2 * a12, b12 = s2 * a11 + c2 * a12;
-            double b21 = c2 * a21 - s2 * a22, b22 = s2 * a21 + c2 * a22;
-            // rows (p1,q1) rotated by (c1,s1)
-            double n11 = c1 * b11 - s1 * b21, n21 = s1 * b11 + c1 * b21;
-            double n12 = c1 * b12 - s1 * b22, n22 = s1 * b12 + c1 * b22;
-            nxt[p2 * ld + p1] = n11;
-            nxt[p1 * ld + p2] = n11;
-            if (vq2) {
-              nxt[q2 * ld + p1] = n12;
-              nxt[p1 * ld + q2] = n12;
-            }
-            if (vq1) {
-              nxt[p2 * ld + q1] = n21;
-              nxt[q1 * ld + p2] = n21;
-            }
-            if (vq1 && vq2) {
-              nxt[q2 * ld + q1] = n22;
-              nxt[q1 * ld + q2] = n22;
-            }
-          }
-        } else {
-          int64_t j = it - nblk;
-          int i = (int)(j % b), P = (int)(j / b);
-          if (act_[P]) {
-            int pc = pp_[P], qc = qq_[P];
-            double vp = p.V[pc * ld + i], vq = p.V[qc * ld + i];
-            double c = c_[P], s = s_[P];
-            p.V[pc * ld + i] = c * vp - s * vq;
-            p.V[qc * ld + i] = s * vp + c * vq;
-          }
-        }
-      }
-      grid_barrier(p.bar);
-      double* tmp = cur;
-      cur = nxt;
-      nxt = tmp;
-    }
-    ++sweeps;
-    // block-reduce the rotation count (identical in every CTA)
-    int v = mycount;
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
-    __syncthreads();
-    int tot = 0;
-    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) tot += red[w];
-    __syncthreads();
-    if (tot == 0) {
-      converged = true;
-      break;
-    }
-  }
-  for (int64_t i = gtid; i < b; i += gthreads) p.lam[i] = cur[i * ld + i];
-  if (gtid == 0) {
-    p.info[0] = sweeps;
-    p.info[2] = converged ? 0 : 1;
-  }
-}
 
 // Single-CTA variant for b <= 160: A lives in shared memory and is updated in
 // place (each 2x2 block (P,Q), P <= Q, is read and written by one thread, its
