@@ -191,8 +191,9 @@ __global__ void __launch_bounds__(1024) jacobi_smem_kernel(JacParams p) {
 //   phase 1  one CTA per pair diagonalises the 32 x 32 sub-matrix A[I u J, I u J] in
 //            shared memory with cyclic two-sided Jacobi (relative stopping rule),
 //            accumulating Q_k; it writes Q_k and the rotated diagonal block;
-//   phase 2  every off-diagonal pair block A'[k, l] = Q_k^T A[k, l] Q_l (double
-//            buffered) and V[:, l] <- V[:, l] Q_l, spread over the whole grid.
+//   phase 2  every off-diagonal pair block A'[k, l] = Q_k^T A[k, l] Q_l (in place; the
+//            blocks of two unrotated pairs are skipped) and V[:, l] <- V[:, l] Q_l,
+//            spread over the whole grid.
 // Two grid barriers per round instead of one per rotation step.  Plane rotations
 // inside the pairs keep the relative accuracy of graded (scaled diagonally dominant)
 // matrices; the off-pair blocks see only orthogonal transformations.
@@ -265,8 +266,7 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(BJParams p) {
   for (int64_t e = gtid; e < p.max_sweeps; e += gthreads) p.cnt[e] = 0;
   grid_barrier(p.bar);
 
-  double* cur = p.A0;
-  double* nxt = p.A1;
+  double* cur = p.A0;  // updated in place: blocks of unrotated pairs are never touched
   const int m = p.m, h = p.h;
   const int vt = (int)cdiv_d(bp, BJ_VT);
   const int nkl = h * (h - 1) / 2;
@@ -366,11 +366,12 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(BJParams p) {
         }
         // write Q_k, the flag and the rotated diagonal block
         double* Qk = p.Qb + (int64_t)k * BJ_P * BJ_P;
-        for (int e = tid; e < BJ_P * BJ_P; e += nth) {
-          int r = e >> 5, c = e & 31;
-          Qk[r * BJ_P + c] = Q[r * BJ_LD + c];
-          nxt[(int64_t)bj_g(c, I, J) * ld + bj_g(r, I, J)] = S[r * BJ_LD + c];
-        }
+        if (rot_total)  // in place: the pair's diagonal block belongs to this CTA alone
+          for (int e = tid; e < BJ_P * BJ_P; e += nth) {
+            int r = e >> 5, c = e & 31;
+            Qk[r * BJ_P + c] = Q[r * BJ_LD + c];
+            cur[(int64_t)bj_g(c, I, J) * ld + bj_g(r, I, J)] = S[r * BJ_LD + c];
+          }
         if (tid == 0) {
           p.rotf[k] = rot_total > 0;
           if (rot_total) atomicAdd(&p.cnt[sw], rot_total);
@@ -399,7 +400,7 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(BJParams p) {
         bj_pair(l, step, m, Il, Jl);
         const bool rk = t < 0 && p.rotf[k], rl = p.rotf[l];
         const int rows = t < 0 ? BJ_P : min(BJ_VT, bp - t * BJ_VT);
-        if (t >= 0 && !rl) continue;  // V tile unchanged
+        if (!rk && !rl) continue;  // identity on both sides: the block (or V tile) is unchanged
         const double* Qk = p.Qb + (int64_t)k * BJ_P * BJ_P;
         const double* Ql = p.Qb + (int64_t)l * BJ_P * BJ_P;
         for (int e = tid; e < rows * BJ_P; e += nth) {
@@ -449,8 +450,8 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(BJParams p) {
             const int gc = bj_g(cc, Il, Jl);
             if (t < 0) {
               const int gr = bj_g(r, Ik, Jk);
-              nxt[(int64_t)gc * ld + gr] = a4[c];
-              nxt[(int64_t)gr * ld + gc] = a4[c];
+              cur[(int64_t)gc * ld + gr] = a4[c];  // in place: block (k, l) and its mirror
+              cur[(int64_t)gr * ld + gc] = a4[c];  // belong to this item alone
             } else {
               p.V[(int64_t)gc * ld + t * BJ_VT + r] = a4[c];
             }
@@ -464,9 +465,6 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(BJParams p) {
       { unsigned long long t = gtimer(); tacc[2] += t - tq; tq = t; }
       grid_barrier(p.bar);
       { unsigned long long t = gtimer(); tacc[3] += t - tq; tq = t; }
-      double* tmp = cur;
-      cur = nxt;
-      nxt = tmp;
     }
     ++sweeps;
     if (*(volatile int*)(p.cnt + sw) == 0) {  // read after the barrier: identical in every CTA

@@ -18,6 +18,7 @@
 // (Z1 U, Z2 V) and a column gather of Z3.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <vector>
 
 #include "gemm.cuh"
@@ -302,7 +303,11 @@ int rhosvd_t2c(const rhosvd_result* res, double eps_rel, rhosvd_stream stream, r
     return fail(RHOSVD_ENOMEM, "t2c scratch");
   }
   // one-sided Jacobi stopping rule |b_p^T b_q| <= tol ||b_p|| ||b_q||, tol = 4 sqrt(r1) u
-  const double tol = 4.0 * std::sqrt((double)std::max(r1, 1)) * 1.1102230246251565e-16;
+  static const double tol_mult = [] {
+    const char* e = getenv("RHOSVD_T2C_TOL");
+    return e ? atof(e) : 4.0;
+  }();
+  const double tol = tol_mult * std::sqrt((double)std::max(r1, 1)) * 1.1102230246251565e-16;
   {
     const int64_t tot = (int64_t)r1 * r2 * r3;
     t2c_transpose_kernel<<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(res->beta, r1, r2, r3, Bt);
