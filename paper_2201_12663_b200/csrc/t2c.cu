@@ -188,6 +188,207 @@ __global__ void __launch_bounds__(T2C_THREADS) t2c_slice_kernel(T2CParams p) {
   }
 }
 
+// ---------------------------------------------------------------- large slices
+// Slices too large for shared memory: block one-sided Jacobi with the slice in global
+// memory (column-major per slice, L2-resident working set).  One-sided rotations only
+// mix the two columns involved, so a block pair (I, J) of CB columns each is loaded
+// into shared memory, swept once with the in-CTA one-sided Jacobi, and written back;
+// the blocks meet in round-robin order, an outer sweep covers every column pair.
+struct T2CBlockParams {
+  const double* Bo;  // original slices, column-major: Bo[(m r2 + b) r1 + a] = beta[a][b][m]
+  double* Bw;        // working copy (rotated in place), same layout
+  int r1, r2, r3, ldp, CB, nb;  // ldp: smem column pitch (odd); nb: even block count
+  double thr, tol;
+  double* Us;
+  double* Vs;
+  double* sg;
+  int* cnt;
+  int* sweeps;
+  double* drop;
+};
+
+__global__ void __launch_bounds__(T2C_THREADS) t2c_slice_block_kernel(T2CBlockParams p) {
+  extern __shared__ double sbk[];
+  const int r1 = p.r1, r2 = p.r2, ld = p.ldp, CB = p.CB, nb = p.nb;
+  double* P = sbk;                              // 2 CB columns, pitch ld
+  double* sig = P + (size_t)2 * CB * ld;        // r2
+  int* ord = reinterpret_cast<int*>(sig + r2);  // r2
+  __shared__ int srot;
+  __shared__ double sfro;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = T2C_THREADS / 32;
+  for (int m = blockIdx.x; m < p.r3; m += gridDim.x) {
+    const double* Bo = p.Bo + (size_t)m * r2 * r1;
+    double* Bw = p.Bw + (size_t)m * r2 * r1;
+    for (int e = tid; e < r1 * r2; e += T2C_THREADS) Bw[e] = Bo[e];
+    if (warp == 0) {  // ||B||_F^2 (fixed order)
+      double s = 0.0;
+      for (int e = lane; e < r1 * r2; e += 32) s = fma(Bo[e], Bo[e], s);
+      s = warp_sum(s);
+      if (lane == 0) sfro = s;
+    }
+    __syncthreads();
+    const double tiny2 = 256.0 * 1.2325951644078309e-32 * sfro;
+    int sw = 0;
+    bool conv = false;
+    for (; sw < T2C_MAX_SWEEPS && !conv; ++sw) {
+      if (tid == 0) srot = 0;
+      __syncthreads();
+      for (int rd = 0; rd < nb - 1; ++rd) {
+        for (int k = 0; k < nb / 2; ++k) {
+          const int b1 = t2c_rr(k, rd, nb), b2 = t2c_rr(nb - 1 - k, rd, nb);
+          const int I = min(b1, b2), J = max(b1, b2);
+          // local column l < CB -> global I CB + l, else J CB + (l - CB); beyond r2 -> zero
+          for (int e = tid; e < 2 * CB * ld; e += T2C_THREADS) {
+            const int l = e / ld, a = e % ld;
+            const int gcol = l < CB ? I * CB + l : J * CB + (l - CB);
+            P[e] = (a < r1 && gcol < r2) ? Bw[(size_t)gcol * r1 + a] : 0.0;
+          }
+          __syncthreads();
+          const int m2 = 2 * CB;
+          for (int st = 0; st < m2 - 1; ++st) {
+            for (int q = warp; q < CB; q += nw) {
+              const int c1 = t2c_rr(q, st, m2), c2 = t2c_rr(m2 - 1 - q, st, m2);
+              double* bp = P + (size_t)min(c1, c2) * ld;
+              double* bq = P + (size_t)max(c1, c2) * ld;
+              double al = 0.0, be = 0.0, ga = 0.0;
+              for (int i = lane; i < r1; i += 32) {
+                const double x = bp[i], y = bq[i];
+                al = fma(x, x, al);
+                be = fma(y, y, be);
+                ga = fma(x, y, ga);
+              }
+              al = warp_sum(al);
+              be = warp_sum(be);
+              ga = warp_sum(ga);
+              if (al > tiny2 && be > tiny2 && fabs(ga) > p.tol * sqrt(al * be)) {
+                const double zeta = (be - al) / (2.0 * ga);
+                const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                const double c = rsqrt(1.0 + t * t), s = c * t;
+                for (int i = lane; i < r1; i += 32) {
+                  const double x = bp[i], y = bq[i];
+                  bp[i] = c * x - s * y;
+                  bq[i] = s * x + c * y;
+                }
+                if (lane == 0) atomicAdd(&srot, 1);
+              }
+            }
+            __syncthreads();
+          }
+          for (int e = tid; e < 2 * CB * ld; e += T2C_THREADS) {
+            const int l = e / ld, a = e % ld;
+            const int gcol = l < CB ? I * CB + l : J * CB + (l - CB);
+            if (a < r1 && gcol < r2) Bw[(size_t)gcol * r1 + a] = P[e];
+          }
+          __syncthreads();
+        }
+      }
+      conv = (srot == 0);
+      __syncthreads();
+    }
+    // sigma_k = ||b_k||, descending order, kept count (as in the shared-memory kernel)
+    for (int k = warp; k < r2; k += nw) {
+      double s = 0.0;
+      for (int i = lane; i < r1; i += 32) s = fma(Bw[(size_t)k * r1 + i], Bw[(size_t)k * r1 + i], s);
+      s = warp_sum(s);
+      if (lane == 0) sig[k] = sqrt(s);
+    }
+    __syncthreads();
+    for (int k = tid; k < r2; k += T2C_THREADS) {
+      const double v = sig[k];
+      int r = 0;
+      for (int j = 0; j < r2; ++j) r += (sig[j] > v) || (sig[j] == v && j < k);
+      ord[r] = k;
+    }
+    __syncthreads();
+    int keep = 0;
+    for (int j = 0; j < r2; ++j) keep += sig[ord[j]] > p.thr;
+    double* Us = p.Us + (size_t)m * r2 * r1;
+    double* Vs = p.Vs + (size_t)m * r2 * r2;
+    double* sg = p.sg + (size_t)m * r2;
+    // u_j = sgn b_k / sigma (largest-|.| entry positive, lowest index on ties)
+    for (int j = warp; j < keep; j += nw) {
+      const int k = ord[j];
+      const double* bk = Bw + (size_t)k * r1;
+      double best = -1.0;
+      int bi = 0x7fffffff;
+      for (int i = lane; i < r1; i += 32) {
+        const double a = fabs(bk[i]);
+        if (a > best || (a == best && i < bi)) {
+          best = a;
+          bi = i;
+        }
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) {
+          best = ob;
+          bi = oi;
+        }
+      }
+      const double sc = ((bk[bi] < 0.0) ? -1.0 : 1.0) / sig[k];
+      for (int i = lane; i < r1; i += 32) Us[(size_t)j * r1 + i] = sc * bk[i];
+      if (lane == 0) sg[j] = sig[k];
+    }
+    __syncthreads();
+    // v_j = B_orig^T u_j / sigma_j, 8 u's per pass staged in shared memory (the pair buffer),
+    // one warp per column b of the original slice (coalesced), renormalised at the end
+    const int JT = min(8, 2 * CB * ld / max(r1, 1));
+    for (int j0 = 0; j0 < keep; j0 += JT) {
+      const int jn = min(JT, keep - j0);
+      for (int e = tid; e < jn * r1; e += T2C_THREADS) P[e] = Us[(size_t)j0 * r1 + e];
+      __syncthreads();
+      for (int b = warp; b < r2; b += nw) {
+        const double* ob = Bo + (size_t)b * r1;
+        double acc[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[j] = 0.0;
+        for (int i = lane; i < r1; i += 32) {
+          const double x = ob[i];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (j < jn) acc[j] = fma(x, P[(size_t)j * r1 + i], acc[j]);
+        }
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const double v = warp_sum(acc[j]);
+          if (lane == 0 && j < jn) Vs[(size_t)(j0 + j) * r2 + b] = v / sg[j0 + j];
+        }
+      }
+      __syncthreads();
+    }
+    for (int j = warp; j < keep; j += nw) {
+      double* vo = Vs + (size_t)j * r2;
+      double vn = 0.0;
+      for (int b = lane; b < r2; b += 32) vn = fma(vo[b], vo[b], vn);
+      vn = warp_sum(vn);
+      const double rv = vn > 0.0 ? 1.0 / sqrt(vn) : 0.0;
+      __syncwarp();
+      for (int b = lane; b < r2; b += 32) vo[b] *= rv;
+    }
+    if (tid == 0) {
+      p.cnt[m] = keep;
+      p.sweeps[m] = conv ? sw : -1;
+      double d = 0.0;
+      for (int j = r2 - 1; j >= keep; --j) d = fma(sig[ord[j]], sig[ord[j]], d);
+      p.drop[m] = d;
+    }
+    __syncthreads();
+  }
+}
+
+// Bc[(m r2 + b) r1 + a] = beta[(a r2 + b) r3 + m]  (slice-major, column-major copy)
+__global__ void t2c_transpose_cm_kernel(const double* beta, int r1, int r2, int r3, double* Bc) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tot = (int64_t)r1 * r2 * r3;
+  if (e >= tot) return;
+  const int m = (int)(e % r3);
+  const int64_t ab = e / r3;
+  const int a = (int)(ab / r2), b = (int)(ab % r2);
+  Bc[((int64_t)m * r2 + b) * r1 + a] = beta[e];
+}
+
 // Bt[(m r1 + a) r2 + b] = beta[(a r2 + b) r3 + m]  (slice-major copy)
 __global__ void t2c_transpose_kernel(const double* beta, int r1, int r2, int r3, double* Bt) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -277,10 +478,15 @@ int rhosvd_t2c(const rhosvd_result* res, double eps_rel, rhosvd_stream stream, r
   const int ldb = r1 | 1;
   const int m2 = r2 + (r2 & 1);
   const size_t smem = ((size_t)ldb * m2 + m2) * sizeof(double) + (size_t)m2 * sizeof(int) + 64;
-  if (smem > 220 * 1024) {
+  const bool small = smem <= 220 * 1024;
+  // large slices: block width CB with a 2 CB-column pair buffer in shared memory
+  int CB = 32;
+  while (CB > 4 && (size_t)2 * CB * ldb * sizeof(double) + (size_t)r2 * 12 + 64 > 200 * 1024) CB /= 2;
+  const size_t smem_blk = (size_t)2 * CB * ldb * sizeof(double) + (size_t)r2 * (sizeof(double) + sizeof(int)) + 64;
+  if (!small && (smem_blk > 220 * 1024 || r1 * 8 > 2 * CB * ldb)) {
     cp_release(cp);
     return fail(RHOSVD_EINVAL, "t2c: core slices of " + std::to_string(r1) + " x " + std::to_string(r2) +
-                                   " do not fit the shared-memory slice kernel (r1 r2 <= ~27000)");
+                                   " are too large (r1 > ~3000)");
   }
   // per-slice scratch
   double *Us = nullptr, *Vs = nullptr, *sg = nullptr, *drop = nullptr, *Bt = nullptr;
@@ -308,16 +514,38 @@ int rhosvd_t2c(const rhosvd_result* res, double eps_rel, rhosvd_stream stream, r
     return e ? atof(e) : 4.0;
   }();
   const double tol = tol_mult * std::sqrt((double)std::max(r1, 1)) * 1.1102230246251565e-16;
-  {
+  if (small) {
     const int64_t tot = (int64_t)r1 * r2 * r3;
     t2c_transpose_kernel<<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(res->beta, r1, r2, r3, Bt);
   }
-  T2CParams tp{Bt, r1, r2, r3, ldb, cp->thr, tol, Us, Vs, sg, cnt, sweeps, drop};
-  static const cudaError_t attr =
-      cudaFuncSetAttribute(t2c_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-  (void)attr;
-  t2c_slice_kernel<<<std::min(r3, 4 * num_sms()), T2C_THREADS, smem, st>>>(tp);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = cudaSuccess;
+  if (small) {
+    T2CParams tp{Bt, r1, r2, r3, ldb, cp->thr, tol, Us, Vs, sg, cnt, sweeps, drop};
+    static const cudaError_t attr =
+        cudaFuncSetAttribute(t2c_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    (void)attr;
+    t2c_slice_kernel<<<std::min(r3, 4 * num_sms()), T2C_THREADS, smem, st>>>(tp);
+    e = cudaGetLastError();
+  } else {
+    // column-major slice copies: the original (for v = B^T u / sigma) and the working copy
+    double* Bw = nullptr;
+    e = cudaMalloc(&Bw, (size_t)r1 * r2 * r3 * sizeof(double));
+    if (e == cudaSuccess) {
+      const int64_t tot = (int64_t)r1 * r2 * r3;
+      t2c_transpose_cm_kernel<<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(res->beta, r1, r2, r3, Bt);
+      const int nbk = (int)cdiv(r2, CB);
+      T2CBlockParams bp{Bt, Bw, r1, r2, r3, ldb, CB, nbk + (nbk & 1), cp->thr, tol, Us, Vs, sg, cnt, sweeps, drop};
+      static const cudaError_t attr2 =
+          cudaFuncSetAttribute(t2c_slice_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      (void)attr2;
+      t2c_slice_block_kernel<<<std::min(r3, num_sms()), T2C_THREADS, smem_blk, st>>>(bp);
+      e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      cudaFree(Bw);
+    } else {
+      cudaGetLastError();
+    }
+  }
   std::vector<int> hc(r3), hs(r3);
   std::vector<double> hd(r3);
   if (e == cudaSuccess) e = cudaMemcpyAsync(hc.data(), cnt, r3 * sizeof(int), cudaMemcpyDeviceToHost, st);

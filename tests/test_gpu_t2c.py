@@ -101,8 +101,16 @@ def test_t2c_baseline_configs(rh, k, t2c_eps):
     assert cp.R <= r3 * min(r1, r2)
 
 
-def test_t2c_rejects_slices_too_large(rh):
-    p = make_random_params(400, 600, seed=5, ranks=(170, 170, 4))
+@pytest.mark.parametrize("n,R,ranks,t2c_eps", [(400, 600, (170, 170, 4), 1e-6), (300, 900, (257, 190, 9), 1e-5)])
+def test_t2c_large_slices_block_kernel(rh, n, R, ranks, t2c_eps):
+    """Slices too large for shared memory take the block one-sided Jacobi path."""
+    p = make_random_params(n, R, seed=5, ranks=ranks)
     Us, xi = dev_inputs(p)
-    with pytest.raises(Exception, match="shared-memory"):
-        rh.c2c(Us, xi, 1e-6, ranks=p.ranks)
+    check_case(rh, Us, xi, None, p.ranks, t2c_eps)
+
+
+def test_t2c_cfg2(rh):
+    """cfg 2 (r = 278 / 282 / 282): 282 slices of 278 x 282 through the block path."""
+    p = make_params(2)
+    Us, xi = dev_inputs(p)
+    check_case(rh, Us, xi, p.eps, p.ranks, 1e-6)
