@@ -76,12 +76,27 @@ __global__ void __launch_bounds__(T2C_THREADS) t2c_slice_kernel(T2CParams p) {
     int sw = 0;
     bool conv = false;
     for (; sw < T2C_MAX_SWEEPS && !conv; ++sw) {
+      // de Rijk pivoting: visit the columns in decreasing-norm order this sweep (the
+      // position -> column map lives in ord; any visiting order is a valid cyclic sweep)
+      for (int k = warp; k < r2; k += nw) {
+        double s = 0.0;
+        for (int i = lane; i < r1; i += 32) s = fma(B[(size_t)k * ld + i], B[(size_t)k * ld + i], s);
+        s = warp_sum(s);
+        if (lane == 0) sig[k] = s;
+      }
       if (tid == 0) srot = 0;
+      __syncthreads();
+      for (int k = tid; k < r2; k += T2C_THREADS) {
+        const double v = sig[k];
+        int r = 0;
+        for (int j = 0; j < r2; ++j) r += (sig[j] > v) || (sig[j] == v && j < k);
+        ord[r] = k;
+      }
+      if (tid == 0 && m2 > r2) ord[r2] = r2;  // the zero padding column
       __syncthreads();
       for (int st = 0; st < m2 - 1; ++st) {
         for (int k = warp; k < m2 / 2; k += nw) {
-          int c1 = t2c_rr(k, st, m2), c2 = t2c_rr(m2 - 1 - k, st, m2);
-          const int pc = min(c1, c2), qc = max(c1, c2);
+          const int pc = ord[t2c_rr(k, st, m2)], qc = ord[t2c_rr(m2 - 1 - k, st, m2)];
           double* bp = B + (size_t)pc * ld;
           double* bq = B + (size_t)qc * ld;
           double al = 0.0, be = 0.0, ga = 0.0;
@@ -231,7 +246,21 @@ __global__ void __launch_bounds__(T2C_THREADS) t2c_slice_block_kernel(T2CBlockPa
     int sw = 0;
     bool conv = false;
     for (; sw < T2C_MAX_SWEEPS && !conv; ++sw) {
+      // de Rijk pivoting: blocks are formed over the columns in decreasing-norm order
+      for (int k = warp; k < r2; k += nw) {
+        double s = 0.0;
+        for (int i = lane; i < r1; i += 32) s = fma(Bw[(size_t)k * r1 + i], Bw[(size_t)k * r1 + i], s);
+        s = warp_sum(s);
+        if (lane == 0) sig[k] = s;
+      }
       if (tid == 0) srot = 0;
+      __syncthreads();
+      for (int k = tid; k < r2; k += T2C_THREADS) {
+        const double v = sig[k];
+        int r = 0;
+        for (int j = 0; j < r2; ++j) r += (sig[j] > v) || (sig[j] == v && j < k);
+        ord[r] = k;
+      }
       __syncthreads();
       for (int rd = 0; rd < nb - 1; ++rd) {
         for (int k = 0; k < nb / 2; ++k) {
@@ -240,8 +269,8 @@ __global__ void __launch_bounds__(T2C_THREADS) t2c_slice_block_kernel(T2CBlockPa
           // local column l < CB -> global I CB + l, else J CB + (l - CB); beyond r2 -> zero
           for (int e = tid; e < 2 * CB * ld; e += T2C_THREADS) {
             const int l = e / ld, a = e % ld;
-            const int gcol = l < CB ? I * CB + l : J * CB + (l - CB);
-            P[e] = (a < r1 && gcol < r2) ? Bw[(size_t)gcol * r1 + a] : 0.0;
+            const int pos = l < CB ? I * CB + l : J * CB + (l - CB);
+            P[e] = (a < r1 && pos < r2) ? Bw[(size_t)ord[pos] * r1 + a] : 0.0;
           }
           __syncthreads();
           const int m2 = 2 * CB;
@@ -276,8 +305,8 @@ __global__ void __launch_bounds__(T2C_THREADS) t2c_slice_block_kernel(T2CBlockPa
           }
           for (int e = tid; e < 2 * CB * ld; e += T2C_THREADS) {
             const int l = e / ld, a = e % ld;
-            const int gcol = l < CB ? I * CB + l : J * CB + (l - CB);
-            if (a < r1 && gcol < r2) Bw[(size_t)gcol * r1 + a] = P[e];
+            const int pos = l < CB ? I * CB + l : J * CB + (l - CB);
+            if (a < r1 && pos < r2) Bw[(size_t)ord[pos] * r1 + a] = P[e];
           }
           __syncthreads();
         }
