@@ -790,67 +790,94 @@ __device__ __forceinline__ void mm32(const double* A, const double* B, double ac
 }
 
 // Factor the (already updated) diagonal block in sm (64 x 64, lower used) in place into
-// L_jj as 2 x 2 blocks of 32 (warp-level Cholesky / inverse of the diagonal halves,
-// CTA-wide 32^3 products for the off-diagonal half), write L_jj to L, its inverse to
-// Linv[j] and X, and the dependent-column mask.
+// L_jj, write it to L, its inverse to Linv[j] and X, and the dependent-column mask.
+// Register-resident right-looking Cholesky: thread t owns row i = t / 4, columns
+// k = t % 4 + 4 s (s = 0..15); at step c the owners of column c publish it to a
+// double-buffered shared vector, ONE __syncthreads, and every thread applies
+// a_ik -= a_ic a_kc / d_c to its elements (unscaled; columns scaled at the end).  The
+// inverse is row-sequential forward substitution, 4 threads per column j (all inside
+// one warp: __syncwarp only).  Dependent columns (pivot <= delta, or padding): unit
+// pivot, zero sub-column.
+#ifndef RHOSVD_PROBE_STAMP
+#define RHOSVD_PROBE_STAMP(i)
+#endif
 __device__ void chol_diag_block(double* sm, double* inv, const CholParams& p, int j) {
-  const int tid = threadIdx.x, warp = tid >> 5;
+  const int tid = threadIdx.x;
   const int w = min(CB, p.b - j * CB);
-  const int r = tid >> 3, c0 = tid & 7;
-  __shared__ unsigned depw[2];
-  double* A11 = sm;
-  double* A21 = sm + 32 * CLD;
-  double* A22 = sm + 32 * CLD + 32;
-  double* I11 = inv;
-  double* I21 = inv + 32 * CLD;
-  double* I12 = inv + 32;  // scratch, zero at the end
-  double* I22 = inv + 32 * CLD + 32;
-  double acc[4];
-  if (warp == 0) {
-    unsigned d1 = warp_chol32(A11, p.delta, min(w, 32));
-    warp_inv32(A11, I11);
-    if ((tid & 31) == 0) depw[0] = d1;
+  RHOSVD_PROBE_STAMP(0);
+  const int i = tid >> 2, kq = tid & 3;
+  __shared__ double colbuf[2][CB];
+  __shared__ double dd[CB];
+  __shared__ unsigned long long depm;
+  double a[16];
+#pragma unroll
+  for (int s = 0; s < 16; ++s) {
+    const int k = kq + 4 * s;
+    a[s] = (k <= i) ? sm[i * CLD + k] : 0.0;
+  }
+  unsigned long long dep = 0ull;
+#pragma unroll
+  for (int s = 0; s < 16; ++s) {
+    for (int q = 0; q < 4; ++q) {
+      const int c = 4 * s + q;
+      double* cb = colbuf[c & 1];
+      if (kq == q && i >= c) cb[i] = a[s];  // publish column c (final from now on)
+      __syncthreads();
+      const double d = cb[c];
+      const bool skip = (c >= w) || !(d > p.delta);
+      dep |= (skip ? 1ull : 0ull) << c;
+      if (tid == 0) dd[c] = d;
+      if (!skip && i > c) {
+        const double rs = rsqrt(d);
+        const double f = cb[i] * (rs * rs);
+#pragma unroll
+        for (int s2 = 0; s2 < 16; ++s2) {
+          const int k = kq + 4 * s2;
+          if (k > c && k <= i) a[s2] = fma(-f, cb[k], a[s2]);
+        }
+      }
+    }
   }
   __syncthreads();
-  const unsigned d1 = depw[0];
-  // L21 = A21 L11^{-T} (dependent columns of the first half zero)
-  mm32<true>(A21, I11, acc);
-  __syncthreads();
+  RHOSVD_PROBE_STAMP(1);
+  // scale: L(i, k) = a_ik / sqrt(d_k) (k < i), L(i, i) = sqrt(d_i); dependent: 1 / 0
 #pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    const int c = c0 + 8 * q;
-    A21[r * CLD + c] = ((d1 >> c) & 1u) ? 0.0 : acc[q];
+  for (int s = 0; s < 16; ++s) {
+    const int k = kq + 4 * s;
+    double v = 0.0;
+    if (k <= i) {
+      const bool dk = (dep >> k) & 1ull;
+      if (k == i) v = dk ? 1.0 : sqrt(dd[k]);
+      else v = dk ? 0.0 : a[s] * rsqrt(dd[k]);
+    }
+    sm[i * CLD + k] = v;  // upper part (k > i) zeroed
+  }
+  if (tid == 0) depm = dep;
+  __syncthreads();
+  // inverse by 2 x 2 blocks of 32: warps 0 and 1 invert the diagonal halves at the same
+  // time (warp-level, registers), then Linv21 = -Linv22 L21 Linv11 (two 32^3 products)
+  {
+    const int warp = tid >> 5;
+    if (warp == 0) warp_inv32(sm, inv);
+    if (warp == 1) warp_inv32(sm + 32 * CLD + 32, inv + 32 * CLD + 32);
+    __syncthreads();
+    const int r = tid >> 3, c0 = tid & 7;
+    double acc[4];
+    mm32<false>(sm + 32 * CLD, inv, acc);  // T = L21 Linv11 -> scratch in inv's upper right
+#pragma unroll
+    for (int q = 0; q < 4; ++q) inv[r * CLD + 32 + c0 + 8 * q] = acc[q];
+    __syncthreads();
+    mm32<false>(inv + 32 * CLD + 32, inv + 32, acc);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) inv[(32 + r) * CLD + c0 + 8 * q] = -acc[q];
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) inv[r * CLD + 32 + c0 + 8 * q] = 0.0;
   }
   __syncthreads();
-  // A22 -= L21 L21^T
-  mm32<true>(A21, A21, acc);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) A22[r * CLD + c0 + 8 * q] -= acc[q];
-  __syncthreads();
-  if (warp == 0) {
-    unsigned d2 = warp_chol32(A22, p.delta, max(0, min(w - 32, 32)));
-    warp_inv32(A22, I22);
-    if ((tid & 31) == 0) depw[1] = d2;
-  }
-  __syncthreads();
-  // Linv21 = -L22^{-1} L21 L11^{-1}
-  mm32<false>(A21, I11, acc);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) I12[r * CLD + c0 + 8 * q] = acc[q];
-  __syncthreads();
-  mm32<false>(I22, I12, acc);
-#pragma unroll
-  for (int q = 0; q < 4; ++q) I21[r * CLD + c0 + 8 * q] = -acc[q];
-  __syncthreads();
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    I12[r * CLD + c0 + 8 * q] = 0.0;
-    sm[r * CLD + 32 + c0 + 8 * q] = 0.0;  // upper-right of L
-  }
-  __syncthreads();
-  const unsigned long long dep = (unsigned long long)depw[0] | ((unsigned long long)depw[1] << 32);
+  RHOSVD_PROBE_STAMP(2);
   const unsigned long long valid = (w >= 64) ? ~0ull : ((1ull << w) - 1ull);
-  if (tid == 0 && (dep & valid)) atomicOr(p.info + 1, 1);
+  if (tid == 0 && (depm & valid)) atomicOr(p.info + 1, 1);
   double* Lg = p.Linv + (int64_t)j * CB * CB;
   for (int e = tid; e < CB * CB; e += blockDim.x) {
     int rr = e >> 6, c = e & 63;
@@ -859,10 +886,11 @@ __device__ void chol_diag_block(double* sm, double* inv, const CholParams& p, in
     p.X[(int64_t)(j * CB + c) * p.ld + j * CB + rr] = inv[rr * CLD + c];
   }
   if (tid == 0) {
-    p.dep[2 * j] = (unsigned)(dep & 0xffffffffu);
-    p.dep[2 * j + 1] = (unsigned)(dep >> 32);
+    p.dep[2 * j] = (unsigned)(depm & 0xffffffffu);
+    p.dep[2 * j + 1] = (unsigned)(depm >> 32);
   }
   __syncthreads();
+  RHOSVD_PROBE_STAMP(3);
 }
 
 __global__ void __launch_bounds__(256) chol_blk_kernel(CholParams p) {

@@ -1,4 +1,6 @@
 // small_probe.cu - single-CTA timing of the b x b building blocks (clock64 cycles).
+__device__ long long g_stamp[8];
+#define RHOSVD_PROBE_STAMP(i) do { __syncthreads(); if (threadIdx.x == 0) g_stamp[i] = clock64(); } while (0)
 #include "../paper_2201_12663_b200/csrc/small_dense.cu"
 
 namespace rhosvd {
@@ -88,6 +90,9 @@ int main() {
     probe<<<1, 256, smem>>>(g, o);
     long long ho[16];
     cudaMemcpy(ho, o, sizeof(ho), cudaMemcpyDeviceToHost);
+    long long st[8];
+    cudaMemcpyFromSymbol(st, g_stamp, sizeof(st));
+    printf("diag parts: chol %lld, scale %lld, inverse+writes %lld\n", st[1] - st[0], st[2] - st[1], st[3] - st[2]);
     printf("chol32 %lld  inv32 %lld  mm32 %lld  mm64 %lld  32x(sqrt+div) %lld  diag64 %lld cycles\n", ho[0], ho[1], ho[2], ho[3], ho[4], ho[5]);
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
