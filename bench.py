@@ -292,14 +292,21 @@ def run_ours(args):
             h.copy_(t, non_blocking=True)
             return h
 
+        dbg = os.environ.get("RHOSVD_E2E_DEBUG") == "1"
+
         def e2e_step():
             nonlocal d2h
+            t0 = time.perf_counter()
             dU = [u.to(dev, non_blocking=True) for u in hU]
             dx = hx.to(dev, non_blocking=True)
             res = rhosvd.c2t(dU, dx, eps=p.eps, ranks=p.ranks, comm=comm, keep_w=False)
+            t1 = time.perf_counter()
             outs = [to_host(res.beta, "beta")] + [to_host(z, f"Z{i}") for i, z in enumerate(res.Z)] + \
                    [to_host(s, f"s{i}") for i, s in enumerate(res.sigma)]
             torch.cuda.current_stream(dev).synchronize()
+            if dbg:
+                print(f"[e2e] h2d+c2t {1e3 * (t1 - t0):.1f} ms, d2h {1e3 * (time.perf_counter() - t1):.1f} ms",
+                      file=sys.stderr)
             d2h = sum(o.numel() * 8 for o in outs)
             return outs
 

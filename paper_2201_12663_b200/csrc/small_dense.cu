@@ -280,42 +280,62 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(BJParams p) {
       for (int k = blockIdx.x; k < h; k += gridDim.x) {
         int I, J;
         bj_pair(k, step, m, I, J);
-        for (int e = tid; e < BJ_P * BJ_P; e += nth) {
-          int r = e & 31, c = e >> 5;
-          S[r * BJ_LD + c] = cur[(int64_t)bj_g(c, I, J) * ld + bj_g(r, I, J)];
-          Q[r * BJ_LD + c] = (r == c) ? 1.0 : 0.0;
+        {  // 256 threads: 4 loads each, all in flight before the stores
+          double v4[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int e = tid + 256 * q, r = e & 31, c = e >> 5;
+            v4[q] = cur[(int64_t)bj_g(c, I, J) * ld + bj_g(r, I, J)];
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int e = tid + 256 * q, r = e & 31, c = e >> 5;
+            S[r * BJ_LD + c] = v4[q];
+            Q[r * BJ_LD + c] = (r == c) ? 1.0 : 0.0;
+          }
         }
         __syncthreads();
+        // early exit: no off-diagonal entry of the pair block above its threshold means
+        // the inner sweep would rotate nothing (converged sweeps, nearly diagonal input)
+        bool any = false;
+        for (int e = tid; e < BJ_P * BJ_P; e += nth) {
+          const int r = e & 31, c = e >> 5;
+          if (r < c) {
+            const double apq = S[r * BJ_LD + c];
+            any |= fabs(apq) > fmax(abstol, p.tol * sqrt(fabs(S[r * BJ_LD + r] * S[c * BJ_LD + c])));
+          }
+        }
         int rot_total = 0;
+        if (__syncthreads_or(any))
         for (int isw = 0; isw < p.inner_sweeps; ++isw) {
           int rot_sw = 0;
           for (int st = 0; st < BJ_P - 1; ++st) {
             // rotation parameters of the 16 disjoint pairs of this step (t = tan of the
-            // angle; the standard formulas keep high relative accuracy on the diagonal)
+            // angle; the standard formulas keep high relative accuracy on the diagonal).
+            // The threshold test and t are evaluated side by side (no branch between the
+            // two square roots).
             if (tid < 32) {
               int act = 0;
               if (tid < BJ_W) {
                 int a1 = rr_index(tid, st, BJ_P), a2 = rr_index(BJ_P - 1 - tid, st, BJ_P);
                 int pq = min(a1, a2), qq = max(a1, a2);
                 double app = S[pq * BJ_LD + pq], aqq = S[qq * BJ_LD + qq], apq = S[pq * BJ_LD + qq];
-                double c = 1.0, s = 0.0;
-                if (fabs(apq) > fmax(abstol, p.tol * sqrt(fabs(app * aqq)))) {
-                  act = 1;
-                  const double zeta = aqq - app, two = 2.0 * apq;
-                  // t = 2 apq sgn(zeta) / (|zeta| + sqrt(zeta^2 + 4 apq^2))
-                  double t = (zeta >= 0.0 ? two : -two) / (fabs(zeta) + sqrt(fma(zeta, zeta, two * two)));
-                  if (!isfinite(t)) t = copysign(1.0, two);
-                  c = rsqrt(fma(t, t, 1.0));
-                  s = t * c;
-                  // exact diagonal / annihilated entries, written in pass B
-                  c_[tid] = c; s_[tid] = s;
-                  dA_[tid] = app - t * apq;
-                  dB_[tid] = aqq + t * apq;
-                }
+                const double zeta = aqq - app, two = 2.0 * apq;
+                // t = 2 apq sgn(zeta) / (|zeta| + sqrt(zeta^2 + 4 apq^2))
+                double t = (zeta >= 0.0 ? two : -two) / (fabs(zeta) + sqrt(fma(zeta, zeta, two * two)));
+                const double thr = fmax(abstol, p.tol * sqrt(fabs(app * aqq)));
+                act = fabs(apq) > thr;
+                if (!isfinite(t)) t = copysign(1.0, two);
+                double c = rsqrt(fma(t, t, 1.0));
+                double s = t * c;
+                if (!act) { c = 1.0; s = 0.0; }
+                c_[tid] = c; s_[tid] = s;
+                // exact diagonal / annihilated entries
+                dA_[tid] = act ? app - t * apq : app;
+                dB_[tid] = act ? aqq + t * apq : aqq;
                 pp_[tid] = pq;
                 qq_[tid] = qq;
                 act_[tid] = act;
-                if (!act) { c_[tid] = 1.0; s_[tid] = 0.0; }
               }
               unsigned bal = __ballot_sync(0xffffffffu, act);
               if (tid == 0) srot = __popc(bal);
@@ -324,38 +344,43 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(BJParams p) {
             const int nrot = srot;
             rot_sw += nrot;
             if (nrot) {
-              // pass A: rows p, q of S (S <- J^T S) and columns p, q of Q (Q <- Q J);
-              // thread: pair k = tid / 16, index j = tid % 16 and j + 16
-              const int k = tid >> 4, j0 = tid & 15;
-              if (act_[k]) {
-                const int pk = pp_[k], qk = qq_[k];
+              // one pass: thread (k, l) = (tid / 16, tid % 16) owns the 2 x 2 block
+              // rows {p_k, q_k} x cols {p_l, q_l} of S and applies J_k^T (.) J_l (rows
+              // first, then columns); diagonal blocks (k == l) of rotated pairs get the
+              // exact values.  Q <- Q J: pair k, rows tid % 16 and + 16.
+              const int k = tid >> 4, l = tid & 15;
+              const int pk = pp_[k], qk = qq_[k], pl = pp_[l], ql = qq_[l];
+              const bool ak = act_[k], al = act_[l];
+              if (ak || al) {
+                double x00 = S[pk * BJ_LD + pl], x01 = S[pk * BJ_LD + ql];
+                double x10 = S[qk * BJ_LD + pl], x11 = S[qk * BJ_LD + ql];
+                if (k == l) {
+                  x00 = dA_[k]; x01 = 0.0; x10 = 0.0; x11 = dB_[k];
+                } else {
+                  if (ak) {
+                    const double c = c_[k], s = s_[k];
+                    const double y00 = c * x00 - s * x10, y01 = c * x01 - s * x11;
+                    const double y10 = s * x00 + c * x10, y11 = s * x01 + c * x11;
+                    x00 = y00; x01 = y01; x10 = y10; x11 = y11;
+                  }
+                  if (al) {
+                    const double c = c_[l], s = s_[l];
+                    const double y00 = c * x00 - s * x01, y01 = s * x00 + c * x01;
+                    const double y10 = c * x10 - s * x11, y11 = s * x10 + c * x11;
+                    x00 = y00; x01 = y01; x10 = y10; x11 = y11;
+                  }
+                }
+                S[pk * BJ_LD + pl] = x00; S[pk * BJ_LD + ql] = x01;
+                S[qk * BJ_LD + pl] = x10; S[qk * BJ_LD + ql] = x11;
+              }
+              if (ak) {
                 const double c = c_[k], s = s_[k];
 #pragma unroll
                 for (int h2 = 0; h2 < 2; ++h2) {
-                  const int j = j0 + 16 * h2;
-                  double xp = S[pk * BJ_LD + j], xq = S[qk * BJ_LD + j];
-                  S[pk * BJ_LD + j] = c * xp - s * xq;
-                  S[qk * BJ_LD + j] = s * xp + c * xq;
+                  const int j = l + 16 * h2;
                   double vp = Q[j * BJ_LD + pk], vq = Q[j * BJ_LD + qk];
                   Q[j * BJ_LD + pk] = c * vp - s * vq;
                   Q[j * BJ_LD + qk] = s * vp + c * vq;
-                }
-              }
-              __syncthreads();
-              // pass B: columns p, q of S (S <- S J); the 2x2 diagonal block of each
-              // rotated pair gets the exact values
-              if (act_[k]) {
-                const int pk = pp_[k], qk = qq_[k];
-                const double c = c_[k], s = s_[k];
-#pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2) {
-                  const int j = j0 + 16 * h2;
-                  double xp = S[j * BJ_LD + pk], xq = S[j * BJ_LD + qk];
-                  double np = c * xp - s * xq, nq = s * xp + c * xq;
-                  if (j == pk) { np = dA_[k]; nq = 0.0; }
-                  if (j == qk) { np = 0.0; nq = dB_[k]; }
-                  S[j * BJ_LD + pk] = np;
-                  S[j * BJ_LD + qk] = nq;
                 }
               }
             }
@@ -627,6 +652,13 @@ int syevj(int64_t b, const double* A, int64_t lda, double* lambda, double* Vout,
       cudaMemcpy(inf, ws.info, sizeof(inf), cudaMemcpyDeviceToHost);
       fprintf(stderr, "[jacobi ts] b=%d m=%d grid=%d sweeps=%d: phase1 %.1f bar1 %.1f phase2 %.1f bar2 %.1f us\n",
               (int)b, bj.m, grid, inf[0], h[0] * 1e-3, h[1] * 1e-3, h[2] * 1e-3, h[3] * 1e-3);
+      {
+        int cnt[16] = {0};
+        cudaMemcpy(cnt, ws.cnt, sizeof(int) * std::min(16, bj.max_sweeps), cudaMemcpyDeviceToHost);
+        fprintf(stderr, "[jacobi ts] rotations per sweep:");
+        for (int i = 0; i < std::min(inf[0], 16); ++i) fprintf(stderr, " %d", cnt[i]);
+        fprintf(stderr, "\n");
+      }
       cudaFreeAsync(tsb, st);
     }
   }
@@ -714,11 +746,24 @@ __device__ __forceinline__ void zero44(double acc[4][4]) {
     for (int c = 0; c < 4; ++c) acc[a][c] = 0.0;
 }
 // global col-major block (I, J) of M (ld) <-> smem [r][c] (pitch CLD)
+// (blockDim.x == 256: all 16 loads of a thread are issued before the first store)
 __device__ __forceinline__ void ld_blk(double* sm, const double* M, int64_t ld, int I, int J) {
-  for (int e = threadIdx.x; e < CB * CB; e += blockDim.x) {
-    int r = e & 63, c = e >> 6;
-    sm[r * CLD + c] = M[(int64_t)(J * CB + c) * ld + I * CB + r];
-  }
+  const int r = threadIdx.x & 63, c0 = threadIdx.x >> 6;
+  const double* src = M + (int64_t)(J * CB + c0) * ld + I * CB + r;
+  double v[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] = src[(int64_t)(4 * q) * ld];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) sm[r * CLD + c0 + 4 * q] = v[q];
+}
+// row-major 64 x 64 (pitch 64) -> smem [r][c] (pitch CLD)
+__device__ __forceinline__ void ld_rm(double* sm, const double* G) {
+  const int c = threadIdx.x & 63, r0 = threadIdx.x >> 6;
+  double v[16];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) v[q] = G[(r0 + 4 * q) * CB + c];
+#pragma unroll
+  for (int q = 0; q < 16; ++q) sm[(r0 + 4 * q) * CLD + c] = v[q];
 }
 
 // ---- warp-level 32 x 32 building blocks (lane i holds row i in registers; all loops
@@ -880,10 +925,11 @@ __device__ void chol_diag_block(double* sm, double* inv, const CholParams& p, in
   if (tid == 0 && (depm & valid)) atomicOr(p.info + 1, 1);
   double* Lg = p.Linv + (int64_t)j * CB * CB;
   for (int e = tid; e < CB * CB; e += blockDim.x) {
-    int rr = e >> 6, c = e & 63;
+    const int rr = e >> 6, c = e & 63;  // row-major Linv: consecutive threads, consecutive c
     Lg[rr * CB + c] = inv[rr * CLD + c];
-    p.L[(int64_t)(j * CB + c) * p.ld + j * CB + rr] = sm[rr * CLD + c];
-    p.X[(int64_t)(j * CB + c) * p.ld + j * CB + rr] = inv[rr * CLD + c];
+    const int r2 = e & 63, c2 = e >> 6;  // column-major L, X: consecutive threads, consecutive rows
+    p.L[(int64_t)(j * CB + c2) * p.ld + j * CB + r2] = sm[r2 * CLD + c2];
+    p.X[(int64_t)(j * CB + c2) * p.ld + j * CB + r2] = inv[r2 * CLD + c2];
   }
   if (tid == 0) {
     p.dep[2 * j] = (unsigned)(depm & 0xffffffffu);
@@ -913,10 +959,8 @@ __global__ void __launch_bounds__(256) chol_blk_kernel(CholParams p) {
     double v = 0.0;
     if (i < b && j < b) v = p.S[(int64_t)j * p.lds + i] * p.d[i] * p.d[j];
     if (i == j) v += (i < b) ? p.shift : 1.0;
-    p.A[(int64_t)j * ld + i] = v;
-    p.L[(int64_t)j * ld + i] = 0.0;
-    p.X[(int64_t)j * ld + i] = 0.0;
-  }
+    p.A[(int64_t)j * ld + i] = v;  // (L and X: only their lower blocks are ever read,
+  }                                 //  and every one of those is written below)
   grid_barrier(p.bar);
   stamp(p.ts, 0);
   if (blockIdx.x == 0) {
@@ -940,10 +984,7 @@ __global__ void __launch_bounds__(256) chol_blk_kernel(CholParams p) {
       I += j + 1;
       K += j + 1;
       // s2 = Linv_jj ; s0 = L_Ij = A_Ij Linv^T ; s1 = L_Kj
-      {
-        const double* Lg = p.Linv + (int64_t)j * CB * CB;
-        for (int e = tid; e < CB * CB; e += blockDim.x) s2[(e >> 6) * CLD + (e & 63)] = Lg[e];
-      }
+      ld_rm(s2, p.Linv + (int64_t)j * CB * CB);
       ld_blk(s0, p.A, ld, I, j);
       if (K != I) ld_blk(s1, p.A, ld, K, j);
       __syncthreads();
@@ -986,14 +1027,19 @@ __global__ void __launch_bounds__(256) chol_blk_kernel(CholParams p) {
           for (int c = 0; c < 4; ++c) s2[(ty + 16 * a) * CLD + tx + 16 * c] -= acc[a][c];
         __syncthreads();
         chol_diag_block(s2, s1, p, j + 1);
-      } else {
+      } else {  // stage through smem so the global read-modify-write is coalesced
+        __syncthreads();
 #pragma unroll
         for (int a = 0; a < 4; ++a)
 #pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const int r = ty + 16 * a, cc = tx + 16 * c;
-            p.A[(int64_t)(K * CB + cc) * ld + I * CB + r] -= acc[a][c];
-          }
+          for (int c = 0; c < 4; ++c) s2[(ty + 16 * a) * CLD + tx + 16 * c] = acc[a][c];
+        __syncthreads();
+        {
+          const int r = tid & 63, c0 = tid >> 6;
+          double* dst = p.A + (int64_t)(K * CB + c0) * ld + I * CB + r;
+#pragma unroll
+          for (int q = 0; q < 16; ++q) dst[(int64_t)(4 * q) * ld] -= s2[r * CLD + c0 + 4 * q];
+        }
       }
       __syncthreads();
     }
@@ -1017,28 +1063,43 @@ __global__ void __launch_bounds__(256) chol_blk_kernel(CholParams p) {
       for (int a = 0; a < 4; ++a)
 #pragma unroll
         for (int c = 0; c < 4; ++c) s1[(ty + 16 * a) * CLD + tx + 16 * c] = acc[a][c];
-      {
-        const double* Lg = p.Linv + (int64_t)i * CB * CB;
-        for (int e = tid; e < CB * CB; e += blockDim.x) s2[(e >> 6) * CLD + (e & 63)] = Lg[e];
-      }
+      ld_rm(s2, p.Linv + (int64_t)i * CB * CB);
       __syncthreads();
       zero44(acc);
       mm64<false, false>(s2, s1, acc, ty, tx);
+      __syncthreads();
 #pragma unroll
       for (int a = 0; a < 4; ++a)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          const int r = ty + 16 * a, cc = tx + 16 * c;
-          p.X[(int64_t)(j * CB + cc) * ld + i * CB + r] = -acc[a][c];
-        }
+        for (int c = 0; c < 4; ++c) s0[(ty + 16 * a) * CLD + tx + 16 * c] = -acc[a][c];
+      __syncthreads();
+      {
+        const int r = tid & 63, c0 = tid >> 6;
+        double* dst = p.X + (int64_t)(j * CB + c0) * ld + i * CB + r;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) dst[(int64_t)(4 * q) * ld] = s0[r * CLD + c0 + 4 * q];
+      }
     }
     grid_barrier(p.bar);
     stamp(p.ts, 3 + P + dd);
   }
-  // ---------------- Bp(c, i) = d_c X(i, c)
-  for (int64_t e = gtid; e < (int64_t)b * b; e += gthreads) {
-    int c = (int)(e % b), i = (int)(e / b);
-    p.Bp[(int64_t)i * p.ldb + c] = (i >= c) ? p.d[c] * p.X[(int64_t)c * ld + i] : 0.0;
+  // ---------------- Bp(c, i) = d_c X(i, c) (i >= c), 0 above: 64 x 64 tiles transposed
+  // through smem (coalesced on both sides)
+  for (int t = blockIdx.x; t < P * P; t += gridDim.x) {
+    const int I = t % P, J = t / P;  // X block (I, J) -> Bp block (J, I)
+    const int c = tid & 63, r0 = tid >> 6;
+    __syncthreads();
+    if (I >= J) ld_blk(s0, p.X, ld, I, J);  // s0[r][c] = X(I*64 + r, J*64 + c)
+    __syncthreads();
+    const int gc = J * CB + c;
+    if (gc < b) {
+      const double dc = p.d[gc];
+#pragma unroll 4
+      for (int q = 0; q < 16; ++q) {
+        const int r = r0 + 4 * q, gi = I * CB + r;
+        if (gi < b) p.Bp[(int64_t)gi * p.ldb + gc] = (I >= J) ? dc * s0[r * CLD + c] : 0.0;
+      }
+    }
   }
 }
 
