@@ -137,6 +137,25 @@ int  rhosvd_c2t(const double* U1, const double* U2, const double* U3, int64_t ld
                 const double* xi, int64_t n, int64_t R_local, const rhosvd_opts* opts,
                 rhosvd_comm* comm, rhosvd_stream stream, rhosvd_result** out);
 
+/* The same with HOST buffers (the end-to-end entry point bench.py's "e2e" times).
+ *   U1,U2,U3 : host, n x R_local column-major (ld ldu; elements (R_local-1) ldu + n are
+ *              read); xi : host, R_local.  Pinned memory (cudaHostAlloc / torch
+ *              pin_memory) gives full PCIe bandwidth; pageable memory works, slower.
+ *              The buffers must stay valid until the call returns (it never writes them).
+ *   Inputs go H2D on a library copy stream, one side matrix at a time, and mode l's
+ *   normalize + Gram start as soon as U_l has arrived.  Outputs (frames, sigma, core)
+ *   are copied back into library-owned pinned host buffers while the core contraction
+ *   still runs (single GPU: beta row chunk by row chunk), read with the
+ *   rhosvd_result_host_* accessors below; the device accessors stay valid too.
+ *   Errors, collectives, blocking and ownership as rhosvd_c2t. */
+int  rhosvd_c2t_host(const double* U1, const double* U2, const double* U3, int64_t ldu,
+                     const double* xi, int64_t n, int64_t R_local, const rhosvd_opts* opts,
+                     rhosvd_comm* comm, rhosvd_stream stream, rhosvd_result** out);
+/* Host copies (owned by the handle; EINVAL for a result of rhosvd_c2t). */
+int  rhosvd_result_host_frame(const rhosvd_result* res, int mode, const double** Z, int64_t* ldz);
+int  rhosvd_result_host_sigma(const rhosvd_result* res, int mode, const double** s, int64_t* count);
+int  rhosvd_result_host_core (const rhosvd_result* res, const double** beta);
+
 /* Result accessors (device pointers stay owned by the handle). */
 int  rhosvd_result_ranks   (const rhosvd_result* res, int32_t r[3]);               /* host out */
 int  rhosvd_result_frame   (const rhosvd_result* res, int mode, const double** Z, int64_t* ldz); /* n x r_l col-major */

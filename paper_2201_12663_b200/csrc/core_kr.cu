@@ -31,6 +31,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include "kernels.h"
 #include "tma.cuh"
 
 namespace rhosvd {
@@ -43,6 +44,7 @@ struct CoreArgs {
   int A1;            // W1 rows per box
   int A1pad;         // rounded to 8 (1024-B aligned sub-tiles)
   int mt, nt, tiles, splits, kchunk, items;
+  int tm0;           // first row tile of this launch (row-chunked launches)
   int stages;
   uint32_t stage_bytes, tx_bytes;
   double* out;       // beta (splits == 1) or partials [split][r1 r2 r3]
@@ -71,7 +73,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1)
   auto set_item = [&]() {
     if (pit >= p.items) return;
     const int split = pit / p.tiles, tile = pit % p.tiles;
-    const int m0 = (tile % p.mt) * CORE_BM;
+    const int m0 = (p.tm0 + tile % p.mt) * CORE_BM;
     pk = split * p.kchunk;
     pkend = min(p.R, pk + p.kchunk);
     pa = m0 / p.r2;
@@ -121,7 +123,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1)
   uint32_t g = 0;  // k-tiles consumed by this CTA
   for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
     const int split = it / p.tiles, tile = it % p.tiles;
-    const int tm = tile % p.mt, tn = tile / p.mt;
+    const int tm = p.tm0 + tile % p.mt, tn = tile / p.mt;
     const int m0 = tm * CORE_BM, n0 = tn * BN;
     const int a_lo = m0 / p.r2;
     const int kbeg = split * p.kchunk, kend = min(p.R, kbeg + p.kchunk);
@@ -269,13 +271,14 @@ static int launch_core(const CUtensorMap& t1, const CUtensorMap& t2, const CUten
 // (W2ext); part: split-K scratch of part_cap doubles (may be 0).
 int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3, int64_t ldw, int64_t r1,
             int64_t r2, int64_t r3, int64_t R, double* beta, double* ws, double* part, size_t part_cap,
-            cudaStream_t st, double* flops_acc) {
+            cudaStream_t st, double* flops_acc, const CoreChunks* chunks) {
   if (r1 <= 0 || r2 <= 0 || r3 <= 0) return RHOSVD_OK;
   const int64_t M = r1 * r2, total = M * r3;
   if (M > INT32_MAX || total > ((int64_t)1 << 40) || R > INT32_MAX)
     return fail(RHOSVD_EINVAL, "core: problem too large");
   if (R == 0) {
     RH_CUDA(cudaMemsetAsync(beta, 0, (size_t)total * sizeof(double), st));
+    if (chunks && chunks->done) RH_CHECK(chunks->done(chunks->ctx, 0, 0, total, st));
     return RHOSVD_OK;
   }
   const int BN = pick_bn(r3);
@@ -319,20 +322,51 @@ int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3,
   RH_CHECK(make_tmap_2d(&t2, ws, r2 + CORE_BM, R, ldx, CORE_BK, CORE_BM, true));
   RH_CHECK(make_tmap_2d(&t3, W3, r3, R, ldw, CORE_BK, BN, true));
   const size_t smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * a.stages * sizeof(uint64_t);
-  const int grid = (int)std::min<int64_t>(a.items, sms);
-  if (ksub == 2) {
-    if (BN == 128) RH_CHECK((launch_core<128, 2>(t1, t2, t3, a, smem, grid, st)));
-    else if (BN == 96) RH_CHECK((launch_core<96, 2>(t1, t2, t3, a, smem, grid, st)));
-    else RH_CHECK((launch_core<64, 2>(t1, t2, t3, a, smem, grid, st)));
+  auto launch = [&](const CoreArgs& aa, cudaStream_t s) -> int {
+    const int grid = (int)std::min<int64_t>(aa.items, sms);
+    if (ksub == 2) {
+      if (BN == 128) RH_CHECK((launch_core<128, 2>(t1, t2, t3, aa, smem, grid, s)));
+      else if (BN == 96) RH_CHECK((launch_core<96, 2>(t1, t2, t3, aa, smem, grid, s)));
+      else RH_CHECK((launch_core<64, 2>(t1, t2, t3, aa, smem, grid, s)));
+    } else {
+      if (BN == 128) RH_CHECK((launch_core<128, 1>(t1, t2, t3, aa, smem, grid, s)));
+      else if (BN == 96) RH_CHECK((launch_core<96, 1>(t1, t2, t3, aa, smem, grid, s)));
+      else RH_CHECK((launch_core<64, 1>(t1, t2, t3, aa, smem, grid, s)));
+    }
+    return RHOSVD_OK;
+  };
+  const int nch = (chunks && chunks->side && splits == 1) ? std::max(1, std::min(chunks->count, a.mt)) : 1;
+  if (nch > 1) {
+    // independent launches over disjoint row ranges, alternating between two streams
+    cudaEvent_t e0, e1;
+    RH_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+    RH_CUDA(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+    RH_CUDA(cudaEventRecord(e0, st));
+    RH_CUDA(cudaStreamWaitEvent(chunks->side, e0, 0));
+    for (int c = 0; c < nch; ++c) {
+      CoreArgs ac = a;
+      ac.tm0 = (int)((int64_t)a.mt * c / nch);
+      const int tm1 = (int)((int64_t)a.mt * (c + 1) / nch);
+      ac.mt = tm1 - ac.tm0;
+      ac.tiles = ac.mt * a.nt;
+      ac.items = ac.tiles;
+      cudaStream_t s = (c & 1) ? chunks->side : st;
+      RH_CHECK(launch(ac, s));
+      const int64_t m_lo = (int64_t)ac.tm0 * CORE_BM, m_hi = std::min<int64_t>(M, (int64_t)tm1 * CORE_BM);
+      if (chunks->done) RH_CHECK(chunks->done(chunks->ctx, c, m_lo * r3, m_hi * r3, s));
+    }
+    RH_CUDA(cudaEventRecord(e1, chunks->side));
+    RH_CUDA(cudaStreamWaitEvent(st, e1, 0));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
   } else {
-    if (BN == 128) RH_CHECK((launch_core<128, 1>(t1, t2, t3, a, smem, grid, st)));
-    else if (BN == 96) RH_CHECK((launch_core<96, 1>(t1, t2, t3, a, smem, grid, st)));
-    else RH_CHECK((launch_core<64, 1>(t1, t2, t3, a, smem, grid, st)));
-  }
-  if (splits > 1) {
-    core_splitk_reduce<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(part, splits, total, beta);
-    count_launch();
-    RH_LAUNCH_CHECK();
+    RH_CHECK(launch(a, st));
+    if (splits > 1) {
+      core_splitk_reduce<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(part, splits, total, beta);
+      count_launch();
+      RH_LAUNCH_CHECK();
+    }
+    if (chunks && chunks->done) RH_CHECK(chunks->done(chunks->ctx, 0, 0, total, st));
   }
   if (flops_acc) *flops_acc += 2.0 * (double)r1 * r2 * r3 * R;
   return RHOSVD_OK;

@@ -3,6 +3,17 @@
 #include "common.cuh"
 
 namespace rhosvd {
+// Optional row-chunked core launch (overlaps the D2H of finished rows of beta with the
+// rest of the contraction): the row tiles are split into `count` contiguous ranges,
+// launched alternately on the call's stream and `side`; after chunk c, done(c, e0, e1, s)
+// is called with the finished element range [e0, e1) of beta and the stream it was
+// launched on.  Ignored (one launch, one done call) when the problem splits K.
+struct CoreChunks {
+  int count = 1;
+  cudaStream_t side = nullptr;
+  int (*done)(void* ctx, int c, int64_t e0, int64_t e1, cudaStream_t s) = nullptr;
+  void* ctx = nullptr;
+};
 int k_normalize(const double* U, int64_t ldu, int64_t n, int64_t R, int64_t Rp, double* Uh, int64_t ldn,
                 double* s, double* tcol, int* flag, cudaStream_t st);
 int k_xiprime(const double* xi, const double* s1, const double* s2, const double* s3, int64_t R, int64_t Rp,
@@ -18,7 +29,7 @@ int k_sign_fix(double* Z, int64_t ldz, int64_t n, int64_t r, double* W, int64_t 
                cudaStream_t st);
 int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3, int64_t ldw, int64_t r1,
             int64_t r2, int64_t r3, int64_t R, double* beta, double* ws, double* part, size_t part_cap,
-            cudaStream_t st, double* flops_acc);
+            cudaStream_t st, double* flops_acc, const CoreChunks* chunks = nullptr);
 size_t core_ws_doubles(int64_t r2, int64_t R, int64_t ldw);
 size_t core_part_doubles(int64_t r1, int64_t r2, int64_t r3, int64_t R);
 int scale_cols(const double* W, int64_t ldw, const double* xi, int64_t r, int64_t R, double* out, int64_t ldo,

@@ -90,6 +90,7 @@ struct ModeWs {
   DenseWs dws;
 };
 struct Workspace {
+  DBuf Ustage, xistage;  // rhosvd_c2t_host: device copies of the host inputs
   DBuf Uh, s, tcol, xip, xip2, scal, part;
   DBuf G, W1x, W2x, corepart;
   Scratch gsc;
@@ -101,6 +102,7 @@ struct Workspace {
 // next call takes the smallest cached buffer that fits, so a steady stream of same-size
 // calls never grows the memory pool (growing it to hold a 2.2 GB core costs ~0.1 s).
 struct OutCache {
+  bool host = false;  // pinned host buffers (rhosvd_c2t_host outputs) instead of device memory
   std::mutex mu;
   std::multimap<size_t, void*> free_;
   std::map<void*, size_t> cap_;
@@ -116,17 +118,17 @@ struct OutCache {
       return RHOSVD_OK;
     }
     void* p = nullptr;
-    cudaError_t e = cudaMalloc(&p, bytes);
+    cudaError_t e = alloc(&p, bytes);
     if (e != cudaSuccess) {
       cudaGetLastError();
       // release everything cached and retry once
       for (auto& kv : free_) {
-        cudaFree(kv.second);
+        release(kv.second);
         cap_.erase(kv.second);
       }
       free_.clear();
       cached = 0;
-      e = cudaMalloc(&p, bytes);
+      e = alloc(&p, bytes);
       if (e != cudaSuccess) {
         cudaGetLastError();
         return fail(RHOSVD_ENOMEM, std::string("output alloc: ") + cudaGetErrorString(e));
@@ -147,14 +149,27 @@ struct OutCache {
       auto big = std::prev(free_.end());
       cached -= big->first;
       cap_.erase(big->second);
-      cudaFree(big->second);
+      release(big->second);
       free_.erase(big);
     }
   }
+  cudaError_t alloc(void** p, size_t bytes) {
+    return host ? cudaHostAlloc(p, bytes, cudaHostAllocDefault) : cudaMalloc(p, bytes);
+  }
+  void release(void* p) { host ? cudaFreeHost(p) : cudaFree(p); }
 };
 static OutCache& OC() {
   static OutCache c;
   return c;
+}
+// pinned host outputs of rhosvd_c2t_host (pinning 2 GB costs ~1.5 s: keep them)
+static OutCache& HC() {
+  static OutCache* c = [] {
+    auto* h = new OutCache();
+    h->host = true;
+    return h;
+  }();
+  return *c;
 }
 
 // RHOSVD_SERIAL_MODES=1 runs the three per-mode eigensolves one after another
@@ -181,6 +196,28 @@ static cudaStream_t* mode_streams() {
   }
   return it->second.data();
 }
+
+// the H2D / D2H stream of rhosvd_c2t_host (created once per device)
+static cudaStream_t copy_stream() {
+  static std::mutex mu;
+  static std::map<int, cudaStream_t> per_dev;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = per_dev.find(dev);
+  if (it == per_dev.end()) {
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    it = per_dev.emplace(dev, s).first;
+  }
+  return it->second;
+}
+
+// host inputs of rhosvd_c2t_host
+struct HostIn {
+  const double* U[3];
+  const double* xi;
+};
 
 static Workspace& WS() {
   static Workspace w;
@@ -672,8 +709,11 @@ void rhosvd_result_free(rhosvd_result* r) {
     OC().put(r->Z[l]);
     OC().put(r->sigma[l]);
     OC().put(r->W[l]);
+    HC().put(r->hZ[l]);
+    HC().put(r->hsigma[l]);
   }
   OC().put(r->beta);
+  HC().put(r->hbeta);
   delete r;
 }
 
@@ -711,9 +751,69 @@ int rhosvd_result_report(const rhosvd_result* r, rhosvd_report* out) {
   return RHOSVD_OK;
 }
 
-static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n, int64_t Rl,
-                    const rhosvd_opts& o, rhosvd_comm* comm, cudaStream_t st, rhosvd_result* res) {
+// D2H of finished row chunks of beta (rhosvd_c2t_host; CoreChunks callback)
+struct BetaD2H {
+  const double* dev;
+  double* host;
+  cudaStream_t cp;
+};
+static int beta_chunk_d2h(void* ctx, int, int64_t e0, int64_t e1, cudaStream_t s) {
+  auto* b = (BetaD2H*)ctx;
+  if (e1 <= e0) return RHOSVD_OK;
+  cudaEvent_t ev;
+  RH_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  RH_CUDA(cudaEventRecord(ev, s));
+  RH_CUDA(cudaStreamWaitEvent(b->cp, ev, 0));
+  cudaEventDestroy(ev);
+  RH_CUDA(cudaMemcpyAsync(b->host + e0, b->dev + e0, (size_t)(e1 - e0) * sizeof(double), cudaMemcpyDeviceToHost,
+                          b->cp));
+  return RHOSVD_OK;
+}
+
+static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_t n, int64_t Rl,
+                    const rhosvd_opts& o, rhosvd_comm* comm, cudaStream_t st, rhosvd_result* res,
+                    const HostIn* hin = nullptr) {
   Workspace& w = WS();
+  const double* U[3] = {U_in[0], U_in[1], U_in[2]};
+  // host inputs: H2D on the copy stream, one event per mode, so mode l's normalize and
+  // Gram start as soon as its side matrix has arrived (the others still in flight)
+  cudaStream_t cp = nullptr;
+  cudaEvent_t evU[3] = {nullptr, nullptr, nullptr}, evX = nullptr;
+  struct CopyGuard {  // every return path leaves no copy of the caller's buffers in flight
+    cudaStream_t cp = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    ~CopyGuard() {
+      if (cp) cudaStreamSynchronize(cp);
+      for (auto e : ev)
+        if (e) cudaEventDestroy(e);
+    }
+  } guard;
+  if (hin) {
+    cp = copy_stream();
+    if (!cp) return fail(RHOSVD_ECUDA, "copy stream creation failed");
+    guard.cp = cp;
+    const size_t per = Rl > 0 ? (size_t)(Rl - 1) * ldu + n : 0;
+    RH_CHECK(w.Ustage.ensure(3 * std::max<size_t>(per, 1), st));
+    RH_CHECK(w.xistage.ensure(std::max<int64_t>(Rl, 1), st));
+    cudaEvent_t e0;
+    RH_CUDA(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+    RH_CUDA(cudaEventRecord(e0, st));  // the staging buffers are ready on st
+    RH_CUDA(cudaStreamWaitEvent(cp, e0, 0));
+    cudaEventDestroy(e0);
+    for (int l = 0; l < 3; ++l) {
+      double* d = w.Ustage.p + (size_t)l * std::max<size_t>(per, 1);
+      if (per) RH_CUDA(cudaMemcpyAsync(d, hin->U[l], per * sizeof(double), cudaMemcpyHostToDevice, cp));
+      RH_CUDA(cudaEventCreateWithFlags(&evU[l], cudaEventDisableTiming));
+      guard.ev[l] = evU[l];
+      RH_CUDA(cudaEventRecord(evU[l], cp));
+      U[l] = d;
+    }
+    if (Rl > 0) RH_CUDA(cudaMemcpyAsync(w.xistage.p, hin->xi, Rl * sizeof(double), cudaMemcpyHostToDevice, cp));
+    RH_CUDA(cudaEventCreateWithFlags(&evX, cudaEventDisableTiming));
+    guard.ev[3] = evX;
+    RH_CUDA(cudaEventRecord(evX, cp));
+    xi = w.xistage.p;
+  }
   rhosvd_report& rep = res->rep;
   PhaseTimer tm(st);
   Ctx c{st, comm, w, &rep, &tm};
@@ -755,19 +855,42 @@ static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n
     return RHOSVD_OK;
   }
 
-  // ---- S1 normalize (K0)
+  // ---- S1 normalize (K0); with host inputs each mode's Gram (S2) follows its
+  // normalize at once, overlapping the H2D of the next side matrix (a non-finite input
+  // makes that Gram garbage, and the check below rejects the call before it is used)
   RH_CHECK(w.Uh.ensure((size_t)3 * LDN * Rp, st));
   RH_CHECK(w.s.ensure((size_t)3 * Rp, st));
   RH_CHECK(w.tcol.ensure((size_t)3 * Rp, st));
   RH_CHECK(w.xip.ensure((size_t)Rp, st));
   RH_CHECK(w.xip2.ensure((size_t)Rp, st));
   RH_CHECK(w.part.ensure(1024, st));
+  RH_CHECK(w.G.ensure_zero((size_t)3 * LDN * LDN, st));
+  cudaEvent_t g0, g1;
+  cudaEventCreate(&g0);
+  cudaEventCreate(&g1);
   double* Uh[3];
+  auto gram = [&](int l) -> int {
+    double* G = w.G.p + (size_t)l * LDN * LDN;
+    if (Rl > 0) {
+      RH_CHECK(mm(c, n, n, Rl, Uh[l], LDN, false, Uh[l], LDN, false, G, LDN, nullptr, true));
+    } else {
+      RH_CUDA(cudaMemsetAsync(G, 0, (size_t)LDN * LDN * sizeof(double), st));
+    }
+    return RHOSVD_OK;
+  };
+  const bool early_gram = hin != nullptr;
   for (int l = 0; l < 3; ++l) {
     Uh[l] = w.Uh.p + (size_t)l * LDN * Rp;
+    if (hin) RH_CUDA(cudaStreamWaitEvent(st, evU[l], 0));
     RH_CHECK(k_normalize(U[l], ldu, n, Rl, Rp, Uh[l], LDN, w.s.p + l * Rp, w.tcol.p + l * Rp, w.flag, st));
     RH_CHECK(k_fixed_sum(w.tcol.p + l * Rp, Rp, w.scal.p + 4 + l, st));
+    if (early_gram) {
+      if (l == 0) cudaEventRecord(g0, st);
+      RH_CHECK(gram(l));
+      if (l == 2) cudaEventRecord(g1, st);
+    }
   }
+  if (hin) RH_CUDA(cudaStreamWaitEvent(st, evX, 0));
   RH_CHECK(k_xiprime(xi, w.s.p, w.s.p + Rp, w.s.p + 2 * Rp, Rl, Rp, w.xip.p, w.xip2.p, w.flag, st));
   RH_CHECK(k_fixed_sum(w.xip2.p, Rp, w.scal.p + 7, st));
   // flag -> scal[8] as double (non-finite count)
@@ -783,26 +906,21 @@ static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n
   double sc[5];
   RH_CUDA(cudaMemcpyAsync(sc, w.scal.p + 4, sizeof(sc), cudaMemcpyDeviceToHost, st));
   RH_CUDA(cudaStreamSynchronize(st));
-  if (sc[4] != 0.0) return fail(RHOSVD_ENONFINITE, "NaN/Inf in U or xi");
+  if (sc[4] != 0.0) {
+    cudaEventDestroy(g0);
+    cudaEventDestroy(g1);
+    return fail(RHOSVD_ENONFINITE, "NaN/Inf in U or xi");
+  }
   for (int l = 0; l < 3; ++l) rep.trace[l] = sc[l];
   rep.xi_norm = std::sqrt(sc[3]);
 
   // ---- S2 Gram (K1), all three modes, then all-reduce
   tm.mark(PH_GRAM);
-  RH_CHECK(w.G.ensure_zero((size_t)3 * LDN * LDN, st));
-  cudaEvent_t g0, g1;
-  cudaEventCreate(&g0);
-  cudaEventCreate(&g1);
-  cudaEventRecord(g0, st);
-  for (int l = 0; l < 3; ++l) {
-    double* G = w.G.p + (size_t)l * LDN * LDN;
-    if (Rl > 0) {
-      RH_CHECK(mm(c, n, n, Rl, Uh[l], LDN, false, Uh[l], LDN, false, G, LDN, nullptr, true));
-    } else {
-      RH_CUDA(cudaMemsetAsync(G, 0, (size_t)LDN * LDN * sizeof(double), st));
-    }
+  if (!early_gram) {
+    cudaEventRecord(g0, st);
+    for (int l = 0; l < 3; ++l) RH_CHECK(gram(l));
+    cudaEventRecord(g1, st);
   }
-  cudaEventRecord(g1, st);
   RH_CHECK(allreduce(c, w.G.p, 3 * LDN * LDN));
   tm.mark(PH_EIG);
 
@@ -907,11 +1025,46 @@ static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n
     rep.tail[l] = std::sqrt(std::max(0.0, mo[l].tail2));
   }
   tm.mark(PH_EIG);
+  const int64_t r1 = mo[0].r, r2 = mo[1].r, r3 = mo[2].r;
+  const int64_t total = r1 * r2 * r3;
+
+  // host outputs: frames and sigma go back while the core runs; beta chunk by chunk
+  BetaD2H bd{nullptr, nullptr, cp};
+  CoreChunks chunks;
+  if (hin) {
+    cudaEvent_t ev;
+    RH_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    RH_CUDA(cudaEventRecord(ev, st));
+    RH_CUDA(cudaStreamWaitEvent(cp, ev, 0));
+    cudaEventDestroy(ev);
+    for (int l = 0; l < 3; ++l) {
+      const int64_t rl = mo[l].r;
+      if (rl <= 0) continue;
+      RH_CHECK(HC().get((void**)&res->hZ[l], (size_t)LDN * rl * sizeof(double)));
+      RH_CHECK(HC().get((void**)&res->hsigma[l], (size_t)rl * sizeof(double)));
+      RH_CUDA(cudaMemcpyAsync(res->hZ[l], mo[l].Z, (size_t)LDN * rl * sizeof(double), cudaMemcpyDeviceToHost, cp));
+      RH_CUDA(cudaMemcpyAsync(res->hsigma[l], mo[l].sigma, rl * sizeof(double), cudaMemcpyDeviceToHost, cp));
+    }
+    if (total > 0) {
+      RH_CHECK(HC().get((void**)&res->hbeta, (size_t)total * sizeof(double)));
+      bd.host = res->hbeta;
+      if (world == 1) {  // with a communicator beta is complete only after the all-reduce
+        cudaStream_t* ms = mode_streams();
+        if (!ms) return fail(RHOSVD_ECUDA, "mode stream creation failed");
+        static const int nchunks = [] {
+          const char* e = getenv("RHOSVD_CORE_CHUNKS");
+          return e ? std::max(1, atoi(e)) : 8;
+        }();
+        chunks.count = nchunks;
+        chunks.side = ms[1];
+        chunks.done = beta_chunk_d2h;
+        chunks.ctx = &bd;
+      }
+    }
+  }
 
   // ---- S6 core (K7): beta = (W1 (.) W2)(xi' o W3)^T, then all-reduce
   tm.mark(PH_CORE);
-  const int64_t r1 = mo[0].r, r2 = mo[1].r, r3 = mo[2].r;
-  const int64_t total = r1 * r2 * r3;
   cudaEvent_t c0, c1;
   cudaEventCreate(&c0);
   cudaEventCreate(&c1);
@@ -919,6 +1072,7 @@ static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n
     PhaseTimer dt(st);
     if (dbg_on()) dt.mark(0);
     RH_CHECK(OC().get((void**)&res->beta, (size_t)total * sizeof(double)));
+    bd.dev = res->beta;
     if (dbg_on()) dt.mark(1);
     RH_CHECK(w.W1x.ensure((size_t)r1 * Rp, st));
     if (Rl > 0) {
@@ -929,7 +1083,7 @@ static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n
       if (dbg_on()) dt.mark(3);
       cudaEventRecord(c0, st);
       RH_CHECK(core_kr(w.W1x.p, Rp, mo[1].W, mo[2].W, Rp, r1, r2, r3, Rl, res->beta, w.W2x.p, w.corepart.p,
-                       w.corepart.cap, st, &c.flops));
+                       w.corepart.cap, st, &c.flops, chunks.done ? &chunks : nullptr));
       cudaEventRecord(c1, st);
       if (dbg_on()) {
         dt.mark(4);
@@ -942,8 +1096,10 @@ static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n
       RH_CUDA(cudaMemsetAsync(res->beta, 0, (size_t)total * sizeof(double), st));
       cudaEventRecord(c0, st);
       cudaEventRecord(c1, st);
+      if (chunks.done) RH_CHECK(beta_chunk_d2h(&bd, 0, 0, total, st));
     }
     RH_CHECK(allreduce(c, res->beta, total));
+    if (hin && !chunks.done) RH_CHECK(beta_chunk_d2h(&bd, 0, 0, total, st));
     tm.mark(PH_CORE);
     RH_CHECK(k_sumsq(res->beta, total, w.part.p, w.scal.p + 12, st));
   } else {
@@ -956,6 +1112,7 @@ static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n
     RH_CUDA(cudaMemcpyAsync(&bn2, w.scal.p + 12, sizeof(double), cudaMemcpyDeviceToHost, st));
   }
   RH_CUDA(cudaStreamSynchronize(st));
+  if (cp) RH_CUDA(cudaStreamSynchronize(cp));
   RH_CUDA(cudaGetLastError());
   rep.beta_norm = std::sqrt(bn2);
   double st1 = 0.0, st2 = 0.0;
@@ -980,9 +1137,49 @@ static int c2t_impl(const double* U[3], int64_t ldu, const double* xi, int64_t n
   return RHOSVD_OK;
 }
 
+static int c2t_entry(const double* U1, const double* U2, const double* U3, int64_t ldu, const double* xi, int64_t n,
+                     int64_t R_local, const rhosvd_opts* opts, rhosvd_comm* comm, rhosvd_stream stream,
+                     rhosvd_result** out, bool host);
+
 int rhosvd_c2t(const double* U1, const double* U2, const double* U3, int64_t ldu, const double* xi, int64_t n,
                int64_t R_local, const rhosvd_opts* opts, rhosvd_comm* comm, rhosvd_stream stream,
                rhosvd_result** out) {
+  return c2t_entry(U1, U2, U3, ldu, xi, n, R_local, opts, comm, stream, out, false);
+}
+
+int rhosvd_c2t_host(const double* U1, const double* U2, const double* U3, int64_t ldu, const double* xi, int64_t n,
+                    int64_t R_local, const rhosvd_opts* opts, rhosvd_comm* comm, rhosvd_stream stream,
+                    rhosvd_result** out) {
+  return c2t_entry(U1, U2, U3, ldu, xi, n, R_local, opts, comm, stream, out, true);
+}
+
+int rhosvd_result_host_frame(const rhosvd_result* r, int mode, const double** Z, int64_t* ldz) {
+  if (!r || !Z || !ldz || mode < 0 || mode > 2) return fail(RHOSVD_EINVAL, "bad args");
+  if (r->ranks[mode] > 0 && !r->hZ[mode]) return fail(RHOSVD_EINVAL, "no host outputs (use rhosvd_c2t_host)");
+  *Z = r->hZ[mode];
+  *ldz = r->ldz;
+  return RHOSVD_OK;
+}
+int rhosvd_result_host_sigma(const rhosvd_result* r, int mode, const double** s, int64_t* count) {
+  if (!r || !s || !count || mode < 0 || mode > 2) return fail(RHOSVD_EINVAL, "bad args");
+  if (r->ranks[mode] > 0 && !r->hsigma[mode]) return fail(RHOSVD_EINVAL, "no host outputs (use rhosvd_c2t_host)");
+  *s = r->hsigma[mode];
+  *count = r->ranks[mode];
+  return RHOSVD_OK;
+}
+int rhosvd_result_host_core(const rhosvd_result* r, const double** beta) {
+  if (!r || !beta) return fail(RHOSVD_EINVAL, "bad args");
+  if ((int64_t)r->ranks[0] * r->ranks[1] * r->ranks[2] > 0 && !r->hbeta)
+    return fail(RHOSVD_EINVAL, "no host outputs (use rhosvd_c2t_host)");
+  *beta = r->hbeta;
+  return RHOSVD_OK;
+}
+
+}  // extern "C"
+
+static int c2t_entry(const double* U1, const double* U2, const double* U3, int64_t ldu, const double* xi, int64_t n,
+                     int64_t R_local, const rhosvd_opts* opts, rhosvd_comm* comm, rhosvd_stream stream,
+                     rhosvd_result** out, bool host) {
   if (!out) return fail(RHOSVD_EINVAL, "out is null");
   *out = nullptr;
   if (!opts) return fail(RHOSVD_EINVAL, "opts is null");
@@ -1012,7 +1209,8 @@ int rhosvd_c2t(const double* U1, const double* U2, const double* U3, int64_t ldu
   }
   auto* res = new rhosvd_result();
   const double* U[3] = {U1, U2, U3};
-  int s = c2t_impl(U, ldu, xi, n, R_local, o, comm, st, res);
+  HostIn hin{{U1, U2, U3}, xi};
+  int s = c2t_impl(U, ldu, xi, n, R_local, o, comm, st, res, host ? &hin : nullptr);
   if (s != RHOSVD_OK) {
     std::string msg = g_err;
     rhosvd_result_free(res);
@@ -1022,6 +1220,8 @@ int rhosvd_c2t(const double* U1, const double* U2, const double* U3, int64_t ldu
   *out = res;
   return RHOSVD_OK;
 }
+
+extern "C" {
 
 // ---------------------------------------------------------------- kernel-level entry points
 int rhosvd_gram(const double* U, int64_t ldu, int64_t n, int64_t R, double* G, int64_t ldg, rhosvd_stream stream) {

@@ -65,6 +65,10 @@ def lib():
     sig = {
         "rhosvd_opts_default": (None, [C.POINTER(Opts)]),
         "rhosvd_c2t": (C.c_int, [P, P, P, I64, P, I64, I64, C.POINTER(Opts), P, P, C.POINTER(P)]),
+        "rhosvd_c2t_host": (C.c_int, [P, P, P, I64, P, I64, I64, C.POINTER(Opts), P, P, C.POINTER(P)]),
+        "rhosvd_result_host_frame": (C.c_int, [P, C.c_int, C.POINTER(P), C.POINTER(I64)]),
+        "rhosvd_result_host_sigma": (C.c_int, [P, C.c_int, C.POINTER(P), C.POINTER(I64)]),
+        "rhosvd_result_host_core": (C.c_int, [P, C.POINTER(P)]),
         "rhosvd_result_ranks": (C.c_int, [P, C.POINTER(I32)]),
         "rhosvd_result_frame": (C.c_int, [P, C.c_int, C.POINTER(P), C.POINTER(I64)]),
         "rhosvd_result_sigma": (C.c_int, [P, C.c_int, C.POINTER(P), C.POINTER(I64)]),
@@ -105,7 +109,8 @@ EXPORTED = ["rhosvd_opts_default", "rhosvd_c2t", "rhosvd_result_ranks", "rhosvd_
             "rhosvd_nccl_get_unique_id", "rhosvd_comm_init_nccl", "rhosvd_comm_init_callback",
             "rhosvd_comm_destroy", "rhosvd_gram", "rhosvd_dgemm", "rhosvd_syevj", "rhosvd_core",
             "rhosvd_chol_inv", "rhosvd_t2c", "rhosvd_cp_rank", "rhosvd_cp_factor", "rhosvd_cp_core_factor",
-            "rhosvd_cp_weights", "rhosvd_cp_info", "rhosvd_cp_free"]
+            "rhosvd_cp_weights", "rhosvd_cp_info", "rhosvd_cp_free", "rhosvd_c2t_host",
+            "rhosvd_result_host_frame", "rhosvd_result_host_sigma", "rhosvd_result_host_core"]
 
 
 def _check(status):
@@ -284,6 +289,81 @@ def c2t_raw(U, xi, opts: Opts, comm: Comm | None = None, stream=None):
         _check(lib().rhosvd_c2t(_ptr(U1), _ptr(U2), _ptr(U3), n, _ptr(xi), n, R, C.byref(opts),
                                 comm.handle if comm is not None else None, st, C.byref(h)))
     return h
+
+
+class HostResult:
+    """Result of rhosvd_c2t_host: host (pinned, library-owned) outputs viewed as torch CPU
+    tensors WITHOUT a copy.  The views are valid until close() (or garbage collection of
+    this object); copy what must outlive it."""
+
+    def __init__(self, h, n, ranks, report):
+        import numpy as np
+        import torch
+        self._h = h
+        self.ranks = ranks
+        self.report = report
+        L = lib()
+
+        def view(ptr, count):
+            if count == 0 or not ptr:
+                return torch.empty(0, dtype=torch.float64)
+            arr = np.ctypeslib.as_array((C.c_double * count).from_address(ptr))
+            return torch.from_numpy(arr)
+
+        self.Z, self.sigma = [], []
+        for l in range(3):
+            p, ld = C.c_void_p(), C.c_int64()
+            _check(L.rhosvd_result_host_frame(h, l, C.byref(p), C.byref(ld)))
+            rl = ranks[l]
+            self.Z.append(view(p.value, rl * int(ld.value)).view(rl, int(ld.value))[:, :n].t() if rl
+                          else torch.empty(n, 0, dtype=torch.float64))
+            sp, cnt = C.c_void_p(), C.c_int64()
+            _check(L.rhosvd_result_host_sigma(h, l, C.byref(sp), C.byref(cnt)))
+            self.sigma.append(view(sp.value, int(cnt.value)))
+        bp = C.c_void_p()
+        _check(L.rhosvd_result_host_core(h, C.byref(bp)))
+        tot = ranks[0] * ranks[1] * ranks[2]
+        self.beta = view(bp.value, tot).view(*ranks) if tot else torch.zeros(*ranks, dtype=torch.float64)
+
+    def close(self):
+        if self._h is not None:
+            self.Z = self.sigma = self.beta = None
+            lib().rhosvd_result_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def c2t_host(U, xi, eps=None, ranks=None, comm: Comm | None = None, stream=None, device=None, **kw):
+    """rhosvd_c2t_host: host inputs (torch CPU float64 (R_local, n) contiguous, ideally
+    pinned) -> HostResult with host outputs.  H2D / D2H happen inside the call."""
+    import torch
+    U1, U2, U3 = U
+    for i, u in enumerate((U1, U2, U3)):
+        if u.device.type != "cpu" or u.dtype != torch.float64 or not u.is_contiguous():
+            raise ValueError(f"U{i+1} must be a contiguous float64 CPU tensor (R_local, n)")
+    if xi.device.type != "cpu" or xi.dtype != torch.float64 or not xi.is_contiguous():
+        raise ValueError("xi must be a contiguous float64 CPU tensor")
+    R, n = U1.shape
+    if U2.shape != (R, n) or U3.shape != (R, n) or xi.shape != (R,):
+        raise ValueError("shape mismatch: U_l (R_local, n), xi (R_local,)")
+    opts = make_opts(eps=eps, ranks=ranks, **kw)
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else torch.device(device)
+    h = C.c_void_p()
+    with torch.cuda.device(dev):
+        st = _stream_ptr(stream)
+        _check(lib().rhosvd_c2t_host(_ptr(U1), _ptr(U2), _ptr(U3), n, _ptr(xi), n, R, C.byref(opts),
+                                     comm.handle if comm is not None else None, st, C.byref(h)))
+    L = lib()
+    r = (C.c_int32 * 3)()
+    _check(L.rhosvd_result_ranks(h, r))
+    rep = Report()
+    _check(L.rhosvd_result_report(h, C.byref(rep)))
+    return HostResult(h, n, tuple(int(x) for x in r), _report_dict(rep))
 
 
 def _wrap_dev(ptr, nelem, device):
