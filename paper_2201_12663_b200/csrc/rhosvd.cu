@@ -256,6 +256,48 @@ struct PhaseTimer {
 };
 enum { PH_NORM = 0, PH_GRAM = 1, PH_EIG = 2, PH_RR = 3, PH_RANK = 4, PH_PROJ = 5, PH_CORE = 6, PH_COMM = 7 };
 
+// RHOSVD_TIMELINE=1: labelled events per mode, printed relative to the call's start
+// (debug only; shows how the concurrent per-mode solves interleave on the device)
+struct Timeline {
+  bool on = false;
+  std::mutex mu;
+  cudaEvent_t origin = nullptr;
+  struct E { int mode; const char* label; cudaEvent_t ev; };
+  std::vector<E> evs;
+  void begin(cudaStream_t st) {
+    const char* e = getenv("RHOSVD_TIMELINE");
+    on = e && e[0] == '1';
+    if (!on) return;
+    cudaEventCreate(&origin);
+    cudaEventRecord(origin, st);
+  }
+  void mark(int mode, const char* label, cudaStream_t st) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, st);
+    std::lock_guard<std::mutex> lk(mu);
+    evs.push_back({mode, label, e});
+  }
+  void dump() {
+    if (!on) return;
+    cudaDeviceSynchronize();
+    for (auto& x : evs) {
+      float t = 0.f;
+      cudaEventElapsedTime(&t, origin, x.ev);
+      fprintf(stderr, "[timeline] %9.3f ms  mode %2d  %s\n", t, x.mode, x.label);
+      cudaEventDestroy(x.ev);
+    }
+    evs.clear();
+    cudaEventDestroy(origin);
+    on = false;
+  }
+};
+static Timeline& TL() {
+  static Timeline t;
+  return t;
+}
+
 // Collective scheduler for the concurrent per-mode eigensolves on a multi-rank
 // communicator.  One communicator must not be driven by two threads, and the ranks must
 // issue their collectives in the same order; so the mode threads post their all-reduces
@@ -535,6 +577,7 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     // d_k are always taken on a Z produced by at least two passes or by one pass on a
     // well conditioned input.
     RH_CHECK(orth(c, n, b, LDN, w.Y.p, w.Z.p, w.T1.p, ldbs(b), itb <= 2 ? ORTH_SCQR2 : ORTH_CQR1));
+    TL().mark(mode, "iteration", st);
     dbg_check(st, "it Z=orth(GZ)", w.Z.p, n, b, LDN);
     if (b >= m) break;  // full space: exact after one step
     if (itb < 2) continue;
@@ -612,23 +655,28 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
   for (int rs = 0;; ++rs) {
     // W = Z^T Uhat (b x Rp row-major == Rl x b col-major)
     RH_CHECK(mm(c, Rl, b, n, Uh, LDN, true, w.Z.p, LDN, true, w.W.p, Rp));
+    TL().mark(mode, "W = Z^T Uhat", st);
     if (rs >= nref) break;
     // M = Uhat W^T (summed over the R shards), Z <- CholQR2(M)
     RH_CHECK(mm(c, n, b, Rl, Uh, LDN, false, w.W.p, Rp, true, w.M.p, LDN));
+    TL().mark(mode, "M = Uhat W^T", st);
     RH_CHECK(allreduce(c, w.M.p, LDN * b));
     RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldb, ORTH_CQR2));
+    TL().mark(mode, "refine CholQR2", st);
     ++mo.refines;
     c.tm->mark(PH_RR);
   }
   // final one-sided Rayleigh-Ritz: W W^T = P Lambda P^T (high relative accuracy Jacobi)
   RH_CHECK(mm(c, b, b, Rl, w.W.p, Rp, true, w.W.p, Rp, true, w.S.p, ldb, nullptr, true));
   RH_CHECK(allreduce(c, w.S.p, ldb * b));
+  TL().mark(mode, "W W^T", st);
   c.tm->mark(PH_RR);
   {
     int sw = 0;
     RH_CHECK(syevj(b, w.S.p, ldb, w.th.p, w.V.p, ldb, 1e-15, 1e-300, 80, w.dws, st, &sw));
     if (dbg_on()) fprintf(stderr, "[rhosvd dbg] mode %d rr b %lld sweeps %d\n", mode, (long long)b, sw);
     if (sw < 0) return fail(RHOSVD_ENOCONV, "Jacobi on W W^T did not converge");
+    TL().mark(mode, "Jacobi", st);
   }
   c.tm->mark(PH_RANK);
   // rho = ||Uhat - Z W||_F^2 (fused residual epilogue; E never stored)
@@ -642,6 +690,7 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
       RH_CUDA(cudaMemsetAsync(scal + 16 + mode, 0, sizeof(double), st));
     }
     RH_CHECK(allreduce(c, scal + 16 + mode, 1));
+    TL().mark(mode, "residual", st);
     c.tm->mark(PH_RANK);
   }
   double sel[4];
@@ -672,6 +721,7 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     RH_CUDA(cudaMemcpyAsync(mo.sigma, w.inv.p, r * sizeof(double), cudaMemcpyDeviceToDevice, st));
     if (o.flags & RHOSVD_F_SIGN_FIX) RH_CHECK(k_sign_fix(mo.Z, LDN, n, r, mo.W, Rp, Rl, w.sgn.p, st));
   }
+  TL().mark(mode, "projection", st);
   return RHOSVD_OK;
 }
 
@@ -818,6 +868,7 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
   PhaseTimer tm(st);
   Ctx c{st, comm, w, &rep, &tm};
   g_launches = 0;
+  TL().begin(st);
   tm.mark(PH_NORM);
   const int world = comm ? comm->world : 1;
   const int64_t LDN = round_up(n, 16);
@@ -922,6 +973,7 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
     cudaEventRecord(g1, st);
   }
   RH_CHECK(allreduce(c, w.G.p, 3 * LDN * LDN));
+  TL().mark(-1, "Gram", st);
   tm.mark(PH_EIG);
 
   // ---- S3-S5 per mode.  The three modes are independent; on one GPU (no collectives
@@ -1085,6 +1137,7 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
       RH_CHECK(core_kr(w.W1x.p, Rp, mo[1].W, mo[2].W, Rp, r1, r2, r3, Rl, res->beta, w.W2x.p, w.corepart.p,
                        w.corepart.cap, st, &c.flops, chunks.done ? &chunks : nullptr));
       cudaEventRecord(c1, st);
+      TL().mark(-1, "core", st);
       if (dbg_on()) {
         dt.mark(4);
         double ms[16] = {0};
@@ -1134,6 +1187,7 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
   cudaEventDestroy(c1);
   rep.gemm_flops = c.flops;
   rep.launches = g_launches;
+  TL().dump();
   return RHOSVD_OK;
 }
 

@@ -197,7 +197,7 @@ __global__ void __launch_bounds__(1024) jacobi_smem_kernel(JacParams p) {
 // Two grid barriers per round instead of one per rotation step.  Plane rotations
 // inside the pairs keep the relative accuracy of graded (scaled diagonally dominant)
 // matrices; the off-pair blocks see only orthogonal transformations.
-constexpr int BJ_W = 16, BJ_P = 32, BJ_LD = 33, BJ_VT = 64;
+constexpr int BJ_W = 16, BJ_P = 32, BJ_LD = 33, BJ_VT = 64, BJ_THREADS = 288;
 struct BJParams {
   int b, bp, m, h;
   const double* Ain;
@@ -230,16 +230,56 @@ __device__ __forceinline__ void bj_pair(int k, int step, int m, int& I, int& J) 
   J = max(i1, i2);
 }
 
-__global__ void __launch_bounds__(256) jacobi_block_kernel(BJParams p) {
+// ---- inner (pair-block) Jacobi helpers
+// S swizzle: column c of a 32-wide row at c ^ 15 (c >= 16) - for every step of the xor
+// ordering the 16 lower (or upper) indices of the pairs land in 16 distinct double banks
+__device__ __forceinline__ int jb_swz(int c) { return c ^ ((c >> 4) * 15); }
+__device__ __forceinline__ int jb_hbit(int m) { return 1 << (31 - __clz(m)); }
+// the k-th (0..15) index with bit hb clear = the lower element of pair k at a step with
+// highest bit hb; jb_pairof inverts it for either element of the pair
+__device__ __forceinline__ int jb_lower(int k, int hb) { return ((k & ~(hb - 1)) << 1) | (k & (hb - 1)); }
+__device__ __forceinline__ int jb_pairof(int r, int hb) { return ((r >> 1) & ~(hb - 1)) | (r & (hb - 1)); }
+// MUFU seed + two Newton steps: full double precision up to an ulp or two
+__device__ __forceinline__ double jb_rsqrt(double x) {
+  double r;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double h = 0.5 * x;
+  r = r * fma(-h * r, r, 1.5);
+  r = r * fma(-h * r, r, 1.5);
+  return r;
+}
+// Rotation annihilating a_pq of [[app, apq], [apq, aqq]] (p < q): with rho =
+// 1/sqrt(zeta^2 + 4 apq^2), zeta = aqq - app, cos 2th = |zeta| rho, u = 1 + cos 2th >= 1
+// (no cancellation), w = 1/sqrt(2u):  c = u w, s = sgn(zeta) 2 apq rho w,
+// t = s / c = 2 sin2th w^2 (the tangent of the standard formula); the new diagonal
+// app - t apq, aqq + t apq keeps high relative accuracy.  Applied only if
+// apq^2 > max(abs^2, tol^2 |app aqq|) (Demmel-Veselic), else the identity.
+__device__ __forceinline__ void jac_rot(double app, double aqq, double apq, double tol2, double abs2, double& c,
+                                        double& s, double& dA, double& dB, int& act) {
+  const double zeta = aqq - app, two = 2.0 * apq;
+  const double rho = jb_rsqrt(fma(zeta, zeta, two * two));
+  const double u = fma(fabs(zeta), rho, 1.0);
+  const double w = jb_rsqrt(2.0 * u);
+  const double sg = (zeta >= 0.0 ? two : -two) * rho;
+  act = apq * apq > fmax(abs2, tol2 * fabs(app * aqq));
+  c = u * w;
+  s = sg * w;
+  const double t = 2.0 * sg * (w * w);
+  dA = app - t * apq;
+  dB = aqq + t * apq;
+  if (!act) { c = 1.0; s = 0.0; dA = app; dB = aqq; }
+}
+
+__global__ void __launch_bounds__(BJ_THREADS, 3) jacobi_block_kernel(BJParams p) {
   extern __shared__ double sh[];
   double* S = sh;                     // 32 x 33
   double* Q = S + BJ_P * BJ_LD;       // 32 x 33
   double* X = Q + BJ_P * BJ_LD;       // BJ_VT x 33 (phase 2)
   double* Y = X + BJ_VT * BJ_LD;      // BJ_VT x 33 (phase 2)
-  __shared__ double c_[BJ_W], s_[BJ_W], dA_[BJ_W], dB_[BJ_W];
-  __shared__ int pp_[BJ_W], qq_[BJ_W], act_[BJ_W];
-  __shared__ int srot;
-  __shared__ double sdmax[8];
+  __shared__ double c_[2][BJ_W], s_[2][BJ_W], dA_[2][BJ_W], dB_[2][BJ_W];
+  __shared__ int act_[2][BJ_W];
+  __shared__ int srot, srot2;
+  __shared__ double sdmax[16];
   const int tid = threadIdx.x, nth = blockDim.x;
   const int64_t ld = p.ld;
   const int bp = p.bp, b = p.b;
@@ -258,6 +298,7 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(BJParams p) {
     __syncthreads();
   }
   const double abstol = p.abstol * sdmax[0];
+  const double abs2 = abstol * abstol, tol2 = p.tol * p.tol;
   for (int64_t e = gtid; e < (int64_t)bp * bp; e += gthreads) {
     int i = (int)(e % bp), j = (int)(e / bp);
     p.A0[j * ld + i] = (i < b && j < b) ? p.Ain[(int64_t)j * p.lda + i] : 0.0;
@@ -270,7 +311,8 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(BJParams p) {
   const int m = p.m, h = p.h;
   const int vt = (int)cdiv_d(bp, BJ_VT);
   const int nkl = h * (h - 1) / 2;
-  const int ty = tid >> 3, tx = tid & 7;  // phase-2 thread tile: rows ty (+32), cols tx + 8c
+  // phase-2 thread tile: rows ty (+32), cols tx + 8c (threads 0-255; warp 8 idles there)
+  const int ty = tid < 256 ? tid >> 3 : 1 << 20, tx = tid & 7;
   int sweeps = 0;
   bool converged = false;
   unsigned long long tacc[4] = {0, 0, 0, 0}, tq = gtimer();
@@ -280,7 +322,11 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(BJParams p) {
       for (int k = blockIdx.x; k < h; k += gridDim.x) {
         int I, J;
         bj_pair(k, step, m, I, J);
-        {  // 256 threads: 4 loads each, all in flight before the stores
+        double* const S0 = S;  // phase 1: S ping-pong between S and X (phase-2 scratch)
+        double* const S1 = X;
+        // S: the pair block, swizzled (jb_swz) so every half-warp access below is bank-
+        // conflict free; Q: accumulated rotations (pitch BJ_LD)
+        if (tid < 256) {  // 4 loads each, all in flight before the stores
           double v4[4];
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -290,7 +336,7 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(BJParams p) {
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
             const int e = tid + 256 * q, r = e & 31, c = e >> 5;
-            S[r * BJ_LD + c] = v4[q];
+            S0[r * BJ_P + jb_swz(c)] = v4[q];
             Q[r * BJ_LD + c] = (r == c) ? 1.0 : 0.0;
           }
         }
@@ -298,105 +344,129 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(BJParams p) {
         // early exit: no off-diagonal entry of the pair block above its threshold means
         // the inner sweep would rotate nothing (converged sweeps, nearly diagonal input)
         bool any = false;
-        for (int e = tid; e < BJ_P * BJ_P; e += nth) {
-          const int r = e & 31, c = e >> 5;
-          if (r < c) {
-            const double apq = S[r * BJ_LD + c];
-            any |= fabs(apq) > fmax(abstol, p.tol * sqrt(fabs(S[r * BJ_LD + r] * S[c * BJ_LD + c])));
+        if (tid < 256) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int e = tid + 256 * q, r = e & 31, c = e >> 5;
+            if (r < c) {
+              const double apq = S0[r * BJ_P + jb_swz(c)];
+              const double app = S0[r * BJ_P + jb_swz(r)], aqq = S0[c * BJ_P + jb_swz(c)];
+              any |= apq * apq > fmax(abs2, tol2 * fabs(app * aqq));
+            }
           }
         }
-        int rot_total = 0;
-        if (__syncthreads_or(any))
-        for (int isw = 0; isw < p.inner_sweeps; ++isw) {
-          int rot_sw = 0;
-          for (int st = 0; st < BJ_P - 1; ++st) {
-            // rotation parameters of the 16 disjoint pairs of this step (t = tan of the
-            // angle; the standard formulas keep high relative accuracy on the diagonal).
-            // The threshold test and t are evaluated side by side (no branch between the
-            // two square roots).
-            if (tid < 32) {
-              int act = 0;
-              if (tid < BJ_W) {
-                int a1 = rr_index(tid, st, BJ_P), a2 = rr_index(BJ_P - 1 - tid, st, BJ_P);
-                int pq = min(a1, a2), qq = max(a1, a2);
-                double app = S[pq * BJ_LD + pq], aqq = S[qq * BJ_LD + qq], apq = S[pq * BJ_LD + qq];
-                const double zeta = aqq - app, two = 2.0 * apq;
-                // t = 2 apq sgn(zeta) / (|zeta| + sqrt(zeta^2 + 4 apq^2))
-                double t = (zeta >= 0.0 ? two : -two) / (fabs(zeta) + sqrt(fma(zeta, zeta, two * two)));
-                const double thr = fmax(abstol, p.tol * sqrt(fabs(app * aqq)));
-                act = fabs(apq) > thr;
-                if (!isfinite(t)) t = copysign(1.0, two);
-                double c = rsqrt(fma(t, t, 1.0));
-                double s = t * c;
-                if (!act) { c = 1.0; s = 0.0; }
-                c_[tid] = c; s_[tid] = s;
-                // exact diagonal / annihilated entries
-                dA_[tid] = act ? app - t * apq : app;
-                dB_[tid] = act ? aqq + t * apq : aqq;
-                pp_[tid] = pq;
-                qq_[tid] = qq;
-                act_[tid] = act;
-              }
-              unsigned bal = __ballot_sync(0xffffffffu, act);
-              if (tid == 0) srot = __popc(bal);
-            }
-            __syncthreads();
-            const int nrot = srot;
-            rot_sw += nrot;
-            if (nrot) {
-              // one pass: thread (k, l) = (tid / 16, tid % 16) owns the 2 x 2 block
-              // rows {p_k, q_k} x cols {p_l, q_l} of S and applies J_k^T (.) J_l (rows
-              // first, then columns); diagonal blocks (k == l) of rotated pairs get the
-              // exact values.  Q <- Q J: pair k, rows tid % 16 and + 16.
-              const int k = tid >> 4, l = tid & 15;
-              const int pk = pp_[k], qk = qq_[k], pl = pp_[l], ql = qq_[l];
-              const bool ak = act_[k], al = act_[l];
-              if (ak || al) {
-                double x00 = S[pk * BJ_LD + pl], x01 = S[pk * BJ_LD + ql];
-                double x10 = S[qk * BJ_LD + pl], x11 = S[qk * BJ_LD + ql];
-                if (k == l) {
-                  x00 = dA_[k]; x01 = 0.0; x10 = 0.0; x11 = dB_[k];
-                } else {
-                  if (ak) {
-                    const double c = c_[k], s = s_[k];
-                    const double y00 = c * x00 - s * x10, y01 = c * x01 - s * x11;
-                    const double y10 = s * x00 + c * x10, y11 = s * x01 + c * x11;
-                    x00 = y00; x01 = y01; x10 = y10; x11 = y11;
-                  }
-                  if (al) {
-                    const double c = c_[l], s = s_[l];
-                    const double y00 = c * x00 - s * x01, y01 = s * x00 + c * x01;
-                    const double y10 = c * x10 - s * x11, y11 = s * x10 + c * x11;
-                    x00 = y00; x01 = y01; x10 = y10; x11 = y11;
-                  }
-                }
-                S[pk * BJ_LD + pl] = x00; S[pk * BJ_LD + ql] = x01;
-                S[qk * BJ_LD + pl] = x10; S[qk * BJ_LD + ql] = x11;
-              }
-              if (ak) {
-                const double c = c_[k], s = s_[k];
-#pragma unroll
-                for (int h2 = 0; h2 < 2; ++h2) {
-                  const int j = l + 16 * h2;
-                  double vp = Q[j * BJ_LD + pk], vq = Q[j * BJ_LD + qk];
-                  Q[j * BJ_LD + pk] = c * vp - s * vq;
-                  Q[j * BJ_LD + qk] = s * vp + c * vq;
-                }
-              }
-            }
-            __syncthreads();
+        int rot_total = 0, sbuf = 0;
+        if (__syncthreads_or(any)) {
+          // inner cyclic sweeps in the xor ordering: step m (1..31) pairs r with r ^ m.
+          // Rotations of step 1 first; then per step ONE __syncthreads: warps 0-7 apply
+          // the step's 16 rotations (thread (k, l) owns the 2 x 2 block rows {p_k, q_k} x
+          // cols {p_l, q_l}, and Q's columns p_k, q_k), while warp 8 computes the NEXT
+          // step's rotations from the step-start data (it re-forms the one rotated entry
+          // it needs).  Rotation counts: warp 8, lane 0.
+          if (tid < 16) {
+            const int pp = 2 * tid, qq = pp + 1;
+            double c, s, dA, dB;
+            int act;
+            jac_rot(S0[pp * BJ_P + jb_swz(pp)], S0[qq * BJ_P + jb_swz(qq)], S0[pp * BJ_P + jb_swz(qq)], tol2, abs2, c,
+                    s, dA, dB, act);
+            c_[0][tid] = c; s_[0][tid] = s; dA_[0][tid] = dA; dB_[0][tid] = dB; act_[0][tid] = act;
+            const unsigned bal = __ballot_sync(0xffffu, act);
+            if (tid == 0) srot = __popc(bal);
           }
-          rot_total += rot_sw;
-          if (rot_sw == 0) break;
+          __syncthreads();
+          int nrot = srot;  // rotations of the current sweep (warp 8 keeps counting)
+          const int k2 = (tid >> 4) & 15, l2 = tid & 15;
+          int buf = 0;
+          for (int isw = 0; isw < p.inner_sweeps; ++isw) {
+            for (int mm = 1; mm < BJ_P; ++mm) {
+              const int hb = jb_hbit(mm);
+              // S ping-pong: the step reads Sc and writes every entry to Sn (warp 8 reads
+              // step-start entries of Sc while warps 0-7 update)
+              const double* Sc = sbuf ? S1 : S0;
+              double* Sn = sbuf ? S0 : S1;
+              if (tid < 256) {
+                const int pk = jb_lower(k2, hb), qk = pk ^ mm, pl = jb_lower(l2, hb), ql = pl ^ mm;
+                const bool ak = act_[buf][k2], al = act_[buf][l2];
+                double x00 = Sc[pk * BJ_P + jb_swz(pl)], x01 = Sc[pk * BJ_P + jb_swz(ql)];
+                double x10 = Sc[qk * BJ_P + jb_swz(pl)], x11 = Sc[qk * BJ_P + jb_swz(ql)];
+                if (ak || al) {
+                  if (k2 == l2) {  // exact diagonal / annihilated entries
+                    x00 = dA_[buf][k2]; x01 = 0.0; x10 = 0.0; x11 = dB_[buf][k2];
+                  } else {
+                    const double ck = c_[buf][k2], sk = s_[buf][k2], cl = c_[buf][l2], sl = s_[buf][l2];
+                    const double y00 = ck * x00 - sk * x10, y01 = ck * x01 - sk * x11;
+                    const double y10 = sk * x00 + ck * x10, y11 = sk * x01 + ck * x11;
+                    x00 = cl * y00 - sl * y01; x01 = sl * y00 + cl * y01;
+                    x10 = cl * y10 - sl * y11; x11 = sl * y10 + cl * y11;
+                  }
+                }
+                Sn[pk * BJ_P + jb_swz(pl)] = x00; Sn[pk * BJ_P + jb_swz(ql)] = x01;
+                Sn[qk * BJ_P + jb_swz(pl)] = x10; Sn[qk * BJ_P + jb_swz(ql)] = x11;
+                if (ak) {
+                  const double c = c_[buf][k2], s = s_[buf][k2];
+#pragma unroll
+                  for (int h2 = 0; h2 < 2; ++h2) {
+                    const int j = l2 + 16 * h2;
+                    const double vp = Q[j * BJ_LD + pk], vq = Q[j * BJ_LD + qk];
+                    Q[j * BJ_LD + pk] = c * vp - s * vq;
+                    Q[j * BJ_LD + qk] = s * vp + c * vq;
+                  }
+                }
+              } else if (tid < 256 + 32) {
+                // next step's pair j = lane: (pn, qn = pn ^ mn), pn < qn
+                const int j = tid & 15;
+                const int mn = (mm == BJ_P - 1) ? 1 : mm + 1, hn = jb_hbit(mn);
+                const int pn = jb_lower(j, hn), qn = pn ^ mn;
+                // this step's pairs of pn and qn (an upper element r is r0 ^ mm, r0 its lower)
+                const int kp = jb_pairof((pn & hb) ? pn ^ mm : pn, hb), kq = jb_pairof((qn & hb) ? qn ^ mm : qn, hb);
+                const int r0 = jb_lower(kp, hb), r1 = r0 ^ mm, c0 = jb_lower(kq, hb), c1 = c0 ^ mm;
+                const double x00 = Sc[r0 * BJ_P + jb_swz(c0)], x01 = Sc[r0 * BJ_P + jb_swz(c1)];
+                const double x10 = Sc[r1 * BJ_P + jb_swz(c0)], x11 = Sc[r1 * BJ_P + jb_swz(c1)];
+                const double ck = c_[buf][kp], sk = s_[buf][kp], cl = c_[buf][kq], sl = s_[buf][kq];
+                // entry (pn, qn) after this step (pn, qn lie in different pairs kp != kq)
+                const bool rlo = (pn & hb) == 0, clo = (qn & hb) == 0;
+                const double ya = rlo ? ck * x00 - sk * x10 : sk * x00 + ck * x10;
+                const double yb = rlo ? ck * x01 - sk * x11 : sk * x01 + ck * x11;
+                const double apq = clo ? cl * ya - sl * yb : sl * ya + cl * yb;
+                const double app = rlo ? dA_[buf][kp] : dB_[buf][kp];
+                const double aqq = clo ? dA_[buf][kq] : dB_[buf][kq];
+                double c, s, dA, dB;
+                int act;
+                jac_rot(app, aqq, apq, tol2, abs2, c, s, dA, dB, act);
+                if (tid < 256 + 16) {
+                  c_[buf ^ 1][j] = c; s_[buf ^ 1][j] = s; dA_[buf ^ 1][j] = dA; dB_[buf ^ 1][j] = dB;
+                  act_[buf ^ 1][j] = act;
+                }
+                const unsigned bal = __ballot_sync(0xffffffffu, act && tid < 256 + 16);
+                if (mm < BJ_P - 1) nrot += __popc(bal);  // mm = 31 produced the next sweep's step 1
+                if (mm == BJ_P - 1 && tid == 256) srot = __popc(bal);
+              }
+              __syncthreads();
+              buf ^= 1;
+              sbuf ^= 1;
+            }
+            // the sweep's count lives in warp 8; publish it (and the next sweep's step-1 count)
+            if (tid == 256) srot2 = nrot;
+            __syncthreads();
+            const int rot_sw = srot2;
+            nrot = srot;
+            __syncthreads();
+            rot_total += rot_sw;
+            if (rot_sw == 0) break;
+          }
         }
         // write Q_k, the flag and the rotated diagonal block
         double* Qk = p.Qb + (int64_t)k * BJ_P * BJ_P;
-        if (rot_total)  // in place: the pair's diagonal block belongs to this CTA alone
-          for (int e = tid; e < BJ_P * BJ_P; e += nth) {
-            int r = e >> 5, c = e & 31;
+        if (rot_total && tid < 256) {  // in place: the pair's diagonal block belongs to this CTA alone
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int e = tid + 256 * q;
+            const int r = e >> 5, c = e & 31;  // Q_k row-major: consecutive threads, consecutive c
             Qk[r * BJ_P + c] = Q[r * BJ_LD + c];
-            cur[(int64_t)bj_g(c, I, J) * ld + bj_g(r, I, J)] = S[r * BJ_LD + c];
+            const int r2 = e & 31, c2 = e >> 5;  // cur col-major: consecutive threads, consecutive rows
+            cur[(int64_t)bj_g(c2, I, J) * ld + bj_g(r2, I, J)] = (sbuf ? S1 : S0)[r2 * BJ_P + jb_swz(c2)];
           }
+        }
         if (tid == 0) {
           p.rotf[k] = rot_total > 0;
           if (rot_total) atomicAdd(&p.cnt[sw], rot_total);
@@ -428,20 +498,38 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(BJParams p) {
         if (!rk && !rl) continue;  // identity on both sides: the block (or V tile) is unchanged
         const double* Qk = p.Qb + (int64_t)k * BJ_P * BJ_P;
         const double* Ql = p.Qb + (int64_t)l * BJ_P * BJ_P;
-        for (int e = tid; e < rows * BJ_P; e += nth) {
-          int r = e % rows, c = e / rows;
-          int gc = bj_g(c, Il, Jl);
-          X[r * BJ_LD + c] = (t < 0) ? cur[(int64_t)gc * ld + bj_g(r, Ik, Jk)]
-                                     : p.V[(int64_t)gc * ld + t * BJ_VT + r];
-        }
-        for (int e = tid; e < BJ_P * BJ_P; e += nth) {
-          int r = e >> 5, c = e & 31;
-          if (rk) S[r * BJ_LD + c] = Qk[e];
-          if (rl) Q[r * BJ_LD + c] = Ql[e];
+        if (tid < 256) {  // all loads of a thread in flight before its stores
+          // X: rows x 32 (column c of the l pair, rows of the k pair or of V tile t);
+          // thread: row r = tid % 64 (< rows), columns tid / 64 + 4 j
+          double xv[8], qkv[4], qlv[4];
+          const int r = tid & 63, c0 = tid >> 6;
+          const bool rv = r < rows;
+          const int64_t roff = (t < 0) ? (r < BJ_P ? bj_g(r, Ik, Jk) : 0) : (int64_t)t * BJ_VT + r;
+          const double* base = (t < 0) ? cur : p.V;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int c = c0 + 4 * j;
+            xv[j] = rv ? base[(int64_t)bj_g(c, Il, Jl) * ld + roff] : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            qkv[j] = rk ? Qk[tid + 256 * j] : 0.0;
+            qlv[j] = rl ? Ql[tid + 256 * j] : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (rv) X[r * BJ_LD + c0 + 4 * j] = xv[j];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int e = tid + 256 * j, qr = e >> 5, qc = e & 31;
+            if (rk) S[qr * BJ_LD + qc] = qkv[j];
+            if (rl) Q[qr * BJ_LD + qc] = qlv[j];
+          }
         }
         __syncthreads();
         if (rk) {  // Y = Qk^T X (32 x 32)
           double a4[4];
+          if (tid < 256) {
 #pragma unroll
           for (int c = 0; c < 4; ++c) a4[c] = 0.0;
           for (int q = 0; q < BJ_P; ++q) {
@@ -451,6 +539,7 @@ __global__ void __launch_bounds__(256) jacobi_block_kernel(BJParams p) {
           }
 #pragma unroll
           for (int c = 0; c < 4; ++c) Y[ty * BJ_LD + tx + 8 * c] = a4[c];
+          }
           __syncthreads();
           double* tmp = X; X = Y; Y = tmp;
         }
@@ -627,7 +716,7 @@ int syevj(int64_t b, const double* A, int64_t lda, double* lambda, double* Vout,
       bj.inner_sweeps = inner;
     }
     bj.bar = ws.bar; bj.cnt = ws.cnt; bj.info = ws.info;
-    const int threads = 256;
+    const int threads = BJ_THREADS;
     const size_t smem = (size_t)(2 * BJ_P + 2 * BJ_VT) * BJ_LD * sizeof(double);
     static const cudaError_t attr_b =
         cudaFuncSetAttribute(jacobi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
