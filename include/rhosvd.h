@@ -156,6 +156,20 @@ int  rhosvd_result_host_frame(const rhosvd_result* res, int mode, const double**
 int  rhosvd_result_host_sigma(const rhosvd_result* res, int mode, const double** s, int64_t* count);
 int  rhosvd_result_host_core (const rhosvd_result* res, const double** beta);
 
+/* C2T followed by `sweeps` ALS sweeps on the frames (PAPER.md:336-366,
+ * Eq. can_A_Tuck_als, Fig. 2: "only one or two ALS iterations are required").  Per sweep,
+ * for l = 1, 2, 3: Z_l <- the r_l dominant left singular vectors of the mode-l unfolding
+ * of A x_b Z_b^T x_c Z_c^T (the other modes' current frames), computed from its Gram
+ * Uhat_l D [(W_b^T W_b) o (W_c^T W_c)] D Uhat_l^T (D = diag(xi'), W_m = Z_m^T Uhat_m; the
+ * R x R middle factor in column blocks, never stored whole).  The ranks are those of the
+ * RHOSVD start; the result's frames, CP factors and core are the ALS ones, sigma_l the
+ * singular values of the last mode-l unfolding.  sweeps = 0 is rhosvd_c2t.  Cost per
+ * mode ~ 2 n R^2 + 4 R^2 r FLOP (cfg 4: ~1.6e13).  Single GPU: comm must be NULL (EINVAL
+ * otherwise); sweeps < 0: EINVAL.  Other arguments, errors and ownership as rhosvd_c2t. */
+int  rhosvd_c2t_als(const double* U1, const double* U2, const double* U3, int64_t ldu,
+                    const double* xi, int64_t n, int64_t R_local, const rhosvd_opts* opts,
+                    int32_t sweeps, rhosvd_comm* comm, rhosvd_stream stream, rhosvd_result** out);
+
 /* Result accessors (device pointers stay owned by the handle). */
 int  rhosvd_result_ranks   (const rhosvd_result* res, int32_t r[3]);               /* host out */
 int  rhosvd_result_frame   (const rhosvd_result* res, int mode, const double** Z, int64_t* ldz); /* n x r_l col-major */

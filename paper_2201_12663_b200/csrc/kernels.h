@@ -25,6 +25,9 @@ int k_random(double* M, int64_t ldm, int64_t n, int64_t c0, int64_t c1, uint64_t
 int k_ritz_floor(const double* th, int64_t b, double tau, double* inv, cudaStream_t st);
 int k_select_rank(const double* lam, int64_t b, const double* rho, double T, double eps, int r_fixed, int guard,
                   double* tail2, double* out, double* sigma, cudaStream_t st);
+int k_hadamard(const double* A, double* C, int64_t ld, int64_t M, int64_t N, cudaStream_t st);
+int k_transpose(const double* A, int64_t lda, int64_t rows, int64_t cols, double* B, int64_t ldb, cudaStream_t st);
+int k_sqrt_clamp(const double* lam, int64_t r, double* out, cudaStream_t st);
 int k_sign_fix(double* Z, int64_t ldz, int64_t n, int64_t r, double* W, int64_t ldw, int64_t Rl, double* sgn,
                cudaStream_t st);
 int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3, int64_t ldw, int64_t r1,

@@ -305,6 +305,56 @@ int k_select_rank(const double* lam, int64_t b, const double* rho, double T, dou
   LAUNCH_OK();
   return RHOSVD_OK;
 }
+// ALS: C <- A o C elementwise on an M x N column-major block (ld)
+__global__ void hadamard_kernel(const double* A, double* C, int64_t ld, int64_t M, int64_t N) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= M * N) return;
+  const int64_t i = e % M, j = e / M;
+  C[j * ld + i] *= A[j * ld + i];
+}
+int k_hadamard(const double* A, double* C, int64_t ld, int64_t M, int64_t N, cudaStream_t st) {
+  if (M <= 0 || N <= 0) return RHOSVD_OK;
+  hadamard_kernel<<<(unsigned)cdiv(M * N, 256), 256, 0, st>>>(A, C, ld, M, N);
+  LAUNCH_OK();
+  return RHOSVD_OK;
+}
+// B[i * ldb + k] = A[k * lda + i]  (i < rows, k < cols): 32 x 32 tiles through shared
+// memory, coalesced on both sides
+__global__ void transpose_kernel(const double* A, int64_t lda, int64_t rows, int64_t cols, double* B, int64_t ldb) {
+  __shared__ double t[32][33];
+  const int64_t i0 = (int64_t)blockIdx.x * 32, k0 = (int64_t)blockIdx.y * 32;
+  const int tx = threadIdx.x, ty = threadIdx.y;  // 32 x 8
+  for (int q = ty; q < 32; q += 8) {
+    const int64_t i = i0 + tx, k = k0 + q;
+    t[q][tx] = (i < rows && k < cols) ? A[k * lda + i] : 0.0;
+  }
+  __syncthreads();
+  for (int q = ty; q < 32; q += 8) {
+    const int64_t k = k0 + tx, i = i0 + q;
+    if (i < rows && k < cols) B[i * ldb + k] = t[tx][q];
+  }
+}
+int k_transpose(const double* A, int64_t lda, int64_t rows, int64_t cols, double* B, int64_t ldb, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return RHOSVD_OK;
+  if (cdiv(cols, 32) > 65535) return fail(RHOSVD_EINVAL, "transpose: too many columns");
+  transpose_kernel<<<dim3((unsigned)cdiv(rows, 32), (unsigned)cdiv(cols, 32)), dim3(32, 8), 0, st>>>(A, lda, rows,
+                                                                                                    cols, B, ldb);
+  LAUNCH_OK();
+  return RHOSVD_OK;
+}
+
+// out[k] = sqrt(max(lam[k], 0)), k < r  (singular values from Gram eigenvalues)
+__global__ void sqrt_clamp_kernel(const double* lam, int r, double* out) {
+  int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < r) out[k] = sqrt(fmax(lam[k], 0.0));
+}
+int k_sqrt_clamp(const double* lam, int64_t r, double* out, cudaStream_t st) {
+  if (r <= 0) return RHOSVD_OK;
+  sqrt_clamp_kernel<<<(unsigned)cdiv(r, 256), 256, 0, st>>>(lam, (int)r, out);
+  LAUNCH_OK();
+  return RHOSVD_OK;
+}
+
 int k_sign_fix(double* Z, int64_t ldz, int64_t n, int64_t r, double* W, int64_t ldw, int64_t Rl, double* sgn,
                cudaStream_t st) {
   if (r <= 0) return RHOSVD_OK;

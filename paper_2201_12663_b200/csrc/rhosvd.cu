@@ -93,6 +93,7 @@ struct Workspace {
   DBuf Ustage, xistage;  // rhosvd_c2t_host: device copies of the host inputs
   DBuf Uh, s, tcol, xip, xip2, scal, part;
   DBuf G, W1x, W2x, corepart;
+  DBuf alsK1, alsK2, alsT;  // C2T ALS: column blocks of K and of Uhat K
   Scratch gsc;
   ModeWs mw[3];
   int* flag = nullptr;
@@ -725,6 +726,133 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
   return RHOSVD_OK;
 }
 
+// ---------------------------------------------------------------- C2T ALS
+// One frame update of mode l with the frames of the other two modes (b, c) fixed
+// (Eq. can_A_Tuck_als, Fig. 2): Z_l <- the r_l dominant left singular
+// vectors of the mode-l unfolding  M_l = Uhat_l D (W_c (.) W_b)^T  (n x r_b r_c) of
+// A x_b Z_b^T x_c Z_c^T, D = diag(xi'), W_m = Z_m^T Uhat_m.  M_l is never formed
+// (r_b r_c = 4.2e5 columns on cfg 4); its Gram is
+//     G_l = M_l M_l^T = Uhat_l K' Uhat_l^T,   K' = D [(W_b^T W_b) o (W_c^T W_c)] D  (R x R),
+// built from column blocks of K' (never stored whole):  K'[:, blk] by two GEMMs, a
+// Hadamard product and the D scalings; T = Uhat_l K'[:, blk]; G_l += T Uhat_l[:, blk]^T.
+// The dominant eigenvectors of G_l: subspace iteration started from the current Z_l
+// (plus p random columns), CholQR2, then a Rayleigh-Ritz step with the block Jacobi;
+// sigma_l = sqrt of the top r_l Ritz values (singular values of M_l, reading L3).
+// Subspace accuracy is the Gram-domain one (u kappa^2 / gap), enough for the frame
+// update; the core is recomputed from the new frames (reading L2).
+static int als_update(Ctx& c, int l, int64_t n, int64_t LDN, int64_t Rl, int64_t Rp, double* const Uh[3],
+                      const double* xip, ModeOut mo[3], const rhosvd_opts& o, uint64_t seed) {
+  ModeWs& w = *c.m;
+  cudaStream_t st = c.st;
+  const int bm = (l + 1) % 3 < (l + 2) % 3 ? (l + 1) % 3 : (l + 2) % 3;
+  const int cm = 3 - l - bm;
+  const int64_t r = mo[l].r, rb = mo[bm].r, rc = mo[cm].r;
+  if (r <= 0 || Rl <= 0) return RHOSVD_OK;
+  double* G = c.w.G.p + (size_t)l * LDN * LDN;
+  const double* Wb = mo[bm].W;  // r_b x Rp row-major == col-major Rp x r_b (W^T)
+  const double* Wc = mo[cm].W;
+  // Two routes to G_l, the cheaper one by FLOP count:
+  //   direct : M_l^T = (xi' o W_b) (.) W_c contracted with Uhat_l^T over R - the core
+  //            kernel's Khatri-Rao contraction with Uhat_l^T as its third factor - then
+  //            G = M M^T;          2 n R r_b r_c + n^2 r_b r_c      (cfg 5: 1e13)
+  //   blocked: K' column blocks;   2 R^2 (r_b + r_c) + 2 n R^2 + 2 n^2 R   (cfg 4: 1.6e13)
+  const double f_direct = 2.0 * n * (double)Rl * rb * rc + 1.0 * n * (double)n * rb * rc;
+  const double f_block = 2.0 * (double)Rl * Rl * (rb + rc) + 2.0 * n * (double)Rl * Rl + 2.0 * n * (double)n * Rl;
+  // RHOSVD_ALS_ROUTE=direct|block forces a route (tests cover both)
+  static const int route = [] {
+    const char* e = getenv("RHOSVD_ALS_ROUTE");
+    return !e ? 0 : (e[0] == 'd' ? 1 : (e[0] == 'b' ? 2 : 0));
+  }();
+  const bool direct = route == 1 || (route == 0 && f_direct < f_block);
+  if (direct && rb > 0 && rc > 0) {
+    const int64_t kr = rb * rc;
+    RH_CHECK(c.w.alsT.ensure((size_t)LDN * Rp + 64, st));   // Uhat_l^T (LDN x Rp row-major)
+    RH_CHECK(c.w.alsK1.ensure((size_t)LDN * kr + 64, st));  // M_l (LDN x r_b r_c, col-major)
+    RH_CHECK(c.w.W1x.ensure((size_t)rb * Rp + 64, st));
+    RH_CHECK(c.w.W2x.ensure(core_ws_doubles(rc, Rl, Rp), st));
+    RH_CHECK(c.w.corepart.ensure(core_part_doubles(rb, rc, LDN, Rl), st));
+    RH_CHECK(k_transpose(Uh[l], LDN, LDN, Rp, c.w.alsT.p, Rp, st));
+    RH_CHECK(scale_cols(Wb, Rp, xip, rb, Rp, c.w.W1x.p, Rp, st));
+    RH_CHECK(core_kr(c.w.W1x.p, Rp, Wc, c.w.alsT.p, Rp, rb, rc, LDN, Rl, c.w.alsK1.p, c.w.W2x.p, c.w.corepart.p,
+                     c.w.corepart.cap, st, &c.flops));
+    RH_CHECK(mm(c, LDN, LDN, kr, c.w.alsK1.p, LDN, false, c.w.alsK1.p, LDN, false, G, LDN, nullptr, true));
+  } else {
+  // K' column blocks: 2 x Rp x Rb doubles within ~1.5 GB
+  const int64_t Rb = std::max<int64_t>(128, std::min<int64_t>(round_up(Rl, 128), ((int64_t)96 << 20) / Rp / 128 * 128));
+  RH_CHECK(c.w.alsK1.ensure((size_t)Rp * Rb + 64, st));
+  RH_CHECK(c.w.alsK2.ensure((size_t)Rp * Rb + 64, st));
+  RH_CHECK(c.w.alsT.ensure((size_t)LDN * Rb + 64, st));
+  double *K1 = c.w.alsK1.p, *K2 = c.w.alsK2.p, *T = c.w.alsT.p;
+  for (int64_t b0 = 0; b0 < Rl; b0 += Rb) {
+    const int64_t nb = std::min<int64_t>(Rb, Rl - b0);
+    // K1 = D (W_b^T W_b[:, blk]) D_blk ; K2 = W_c^T W_c[:, blk] ; K2 <- K1 o K2
+    if (rb > 0) {
+      RH_CHECK(mm(c, Rl, nb, rb, Wb, Rp, false, Wb + b0, Rp, false, K1, Rp, xip + b0, false, xip));
+    } else {
+      RH_CUDA(cudaMemsetAsync(K1, 0, (size_t)Rp * nb * sizeof(double), st));
+    }
+    if (rc > 0) {
+      RH_CHECK(mm(c, Rl, nb, rc, Wc, Rp, false, Wc + b0, Rp, false, K2, Rp));
+    } else {
+      RH_CUDA(cudaMemsetAsync(K2, 0, (size_t)Rp * nb * sizeof(double), st));
+    }
+    RH_CHECK(k_hadamard(K1, K2, Rp, Rl, nb, st));
+    // T = Uhat_l K'[:, blk]  (n x nb)
+    RH_CHECK(mm(c, n, nb, Rl, Uh[l], LDN, false, K2, Rp, true, T, LDN));
+    // G (+)= T Uhat_l[:, blk]^T
+    GemmArgs g;
+    g.M = n; g.N = n; g.K = nb; g.A = T; g.lda = LDN; g.a_k = false;
+    g.B = Uh[l] + (size_t)b0 * LDN; g.ldb = LDN; g.b_k = false;
+    g.C = G; g.ldc = LDN; g.beta = b0 > 0 ? 1.0 : 0.0;
+    RH_CHECK(gemm(g, w.gsc, st, &c.flops));
+  }
+  }
+  TL().mark(l, "ALS Gram", st);
+  // ---- dominant r eigenvectors of G: start [Z_l | random], CholQR2 subspace iteration
+  const int64_t m = n;
+  const int64_t bsz = std::min<int64_t>(m, r + std::max(1, o.oversample));
+  const int64_t ldb = round_up(std::max<int64_t>(bsz, 2), 2);
+  RH_CHECK(w.Z.ensure((size_t)LDN * bsz + 64, st));
+  RH_CHECK(w.Y.ensure((size_t)LDN * bsz + 64, st));
+  RH_CHECK(w.T1.ensure((size_t)LDN * bsz + 64, st));
+  for (DBuf* d : {&w.S, &w.V, &w.Bp}) RH_CHECK(d->ensure((size_t)ldb * bsz + 64, st));
+  for (DBuf* d : {&w.th, &w.inv, &w.sgn}) RH_CHECK(d->ensure((size_t)bsz + 64, st));
+  RH_CUDA(cudaMemcpy2DAsync(w.Z.p, LDN * sizeof(double), mo[l].Z, LDN * sizeof(double), n * sizeof(double), r,
+                            cudaMemcpyDeviceToDevice, st));
+  if (bsz > r) RH_CHECK(k_random(w.Z.p, LDN, n, r, bsz, seed, st));
+  std::vector<double> d_h(bsz);
+  int need = 60;
+  for (int it = 1; it <= need; ++it) {
+    RH_CHECK(mm(c, n, bsz, n, G, LDN, false, w.Z.p, LDN, true, w.Y.p, LDN));
+    RH_CHECK(k_coldot(w.Z.p, w.Y.p, LDN, n, bsz, w.th.p, st));
+    RH_CHECK(orth(c, n, bsz, LDN, w.Y.p, w.Z.p, w.T1.p, ldb, it == 1 ? ORTH_SCQR3 : ORTH_CQR2));
+    if (it == 2 && bsz > r) {
+      // rate lambda_{b} / lambda_r from the Rayleigh quotients -> iterations for 1e-13
+      RH_CUDA(cudaMemcpyAsync(d_h.data(), w.th.p, bsz * sizeof(double), cudaMemcpyDeviceToHost, st));
+      RH_CUDA(cudaStreamSynchronize(st));
+      const double dr = std::max(d_h[r - 1], 1e-300);
+      const double rho = std::min(0.995, std::max(d_h[bsz - 1], 1e-300 * dr) / dr);
+      need = std::max(3, std::min(60, 2 + (int)std::ceil(std::log(1e-13) / std::log(rho))));
+    }
+    if (bsz >= m) break;  // the whole space: one step is exact
+  }
+  // Rayleigh-Ritz: S = Z^T G Z, S = V diag(lambda) V^T, Z_l = Z V[:, :r], sigma = sqrt(lambda)
+  RH_CHECK(mm(c, n, bsz, n, G, LDN, false, w.Z.p, LDN, true, w.Y.p, LDN));
+  RH_CHECK(mm(c, bsz, bsz, n, w.Z.p, LDN, true, w.Y.p, LDN, true, w.S.p, ldb, nullptr, true));
+  {
+    int sw = 0;
+    RH_CHECK(syevj(bsz, w.S.p, ldb, w.th.p, w.V.p, ldb, 1e-15, 1e-300, 80, w.dws, st, &sw));
+    if (sw < 0) return fail(RHOSVD_ENOCONV, "ALS: Jacobi on Z^T G Z did not converge");
+  }
+  RH_CHECK(mm(c, n, r, bsz, w.Z.p, LDN, false, w.V.p, ldb, true, mo[l].Z, LDN));
+  RH_CHECK(k_sqrt_clamp(w.th.p, r, mo[l].sigma, st));
+  if (o.flags & RHOSVD_F_SIGN_FIX) RH_CHECK(k_sign_fix(mo[l].Z, LDN, n, r, nullptr, 0, 0, w.sgn.p, st));
+  // the new CP factor of the core: W_l = Z_l^T Uhat_l  (r x Rp row-major)
+  RH_CHECK(mm(c, Rl, r, n, Uh[l], LDN, true, mo[l].Z, LDN, true, mo[l].W, Rp));
+  TL().mark(l, "ALS frame update", st);
+  return RHOSVD_OK;
+}
+
 }  // namespace rhosvd
 
 // ====================================================================== C ABI
@@ -822,7 +950,7 @@ static int beta_chunk_d2h(void* ctx, int, int64_t e0, int64_t e1, cudaStream_t s
 
 static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_t n, int64_t Rl,
                     const rhosvd_opts& o, rhosvd_comm* comm, cudaStream_t st, rhosvd_result* res,
-                    const HostIn* hin = nullptr) {
+                    const HostIn* hin = nullptr, int als_sweeps = 0) {
   Workspace& w = WS();
   const double* U[3] = {U_in[0], U_in[1], U_in[2]};
   // host inputs: H2D on the copy stream, one event per mode, so mode l's normalize and
@@ -1077,6 +1205,16 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
     rep.tail[l] = std::sqrt(std::max(0.0, mo[l].tail2));
   }
   tm.mark(PH_EIG);
+  // ---- optional C2T ALS sweeps on the RHOSVD frames (single GPU)
+  for (int sw = 0; sw < als_sweeps; ++sw)
+    for (int l = 0; l < 3; ++l) {
+      c.m = &w.mw[l];
+      const uint64_t seed = o.seed * 0x9E3779B97F4A7C15ull + 0xA15ull * (uint64_t)(3 * sw + l + 1);
+      const int s_ = als_update(c, l, n, LDN, Rl, Rp, Uh, w.xip.p, mo, o, seed);
+      c.m = nullptr;
+      if (s_ != RHOSVD_OK) return s_;
+    }
+  if (als_sweeps > 0) tm.mark(PH_EIG);
   const int64_t r1 = mo[0].r, r2 = mo[1].r, r3 = mo[2].r;
   const int64_t total = r1 * r2 * r3;
 
@@ -1193,7 +1331,16 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
 
 static int c2t_entry(const double* U1, const double* U2, const double* U3, int64_t ldu, const double* xi, int64_t n,
                      int64_t R_local, const rhosvd_opts* opts, rhosvd_comm* comm, rhosvd_stream stream,
-                     rhosvd_result** out, bool host);
+                     rhosvd_result** out, bool host, int als_sweeps = 0);
+
+int rhosvd_c2t_als(const double* U1, const double* U2, const double* U3, int64_t ldu, const double* xi, int64_t n,
+                   int64_t R_local, const rhosvd_opts* opts, int32_t sweeps, rhosvd_comm* comm, rhosvd_stream stream,
+                   rhosvd_result** out) {
+  if (out) *out = nullptr;
+  if (sweeps < 0) return fail(RHOSVD_EINVAL, "sweeps must be >= 0");
+  if (comm && comm->world > 1) return fail(RHOSVD_EINVAL, "ALS sweeps: single GPU only (comm must be NULL)");
+  return c2t_entry(U1, U2, U3, ldu, xi, n, R_local, opts, comm, stream, out, false, sweeps);
+}
 
 int rhosvd_c2t(const double* U1, const double* U2, const double* U3, int64_t ldu, const double* xi, int64_t n,
                int64_t R_local, const rhosvd_opts* opts, rhosvd_comm* comm, rhosvd_stream stream,
@@ -1233,7 +1380,7 @@ int rhosvd_result_host_core(const rhosvd_result* r, const double** beta) {
 
 static int c2t_entry(const double* U1, const double* U2, const double* U3, int64_t ldu, const double* xi, int64_t n,
                      int64_t R_local, const rhosvd_opts* opts, rhosvd_comm* comm, rhosvd_stream stream,
-                     rhosvd_result** out, bool host) {
+                     rhosvd_result** out, bool host, int als_sweeps) {
   if (!out) return fail(RHOSVD_EINVAL, "out is null");
   *out = nullptr;
   if (!opts) return fail(RHOSVD_EINVAL, "opts is null");
@@ -1264,7 +1411,7 @@ static int c2t_entry(const double* U1, const double* U2, const double* U3, int64
   auto* res = new rhosvd_result();
   const double* U[3] = {U1, U2, U3};
   HostIn hin{{U1, U2, U3}, xi};
-  int s = c2t_impl(U, ldu, xi, n, R_local, o, comm, st, res, host ? &hin : nullptr);
+  int s = c2t_impl(U, ldu, xi, n, R_local, o, comm, st, res, host ? &hin : nullptr, als_sweeps);
   if (s != RHOSVD_OK) {
     std::string msg = g_err;
     rhosvd_result_free(res);

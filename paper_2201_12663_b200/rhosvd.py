@@ -66,6 +66,7 @@ def lib():
         "rhosvd_opts_default": (None, [C.POINTER(Opts)]),
         "rhosvd_c2t": (C.c_int, [P, P, P, I64, P, I64, I64, C.POINTER(Opts), P, P, C.POINTER(P)]),
         "rhosvd_c2t_host": (C.c_int, [P, P, P, I64, P, I64, I64, C.POINTER(Opts), P, P, C.POINTER(P)]),
+        "rhosvd_c2t_als": (C.c_int, [P, P, P, I64, P, I64, I64, C.POINTER(Opts), I32, P, P, C.POINTER(P)]),
         "rhosvd_result_host_frame": (C.c_int, [P, C.c_int, C.POINTER(P), C.POINTER(I64)]),
         "rhosvd_result_host_sigma": (C.c_int, [P, C.c_int, C.POINTER(P), C.POINTER(I64)]),
         "rhosvd_result_host_core": (C.c_int, [P, C.POINTER(P)]),
@@ -110,7 +111,8 @@ EXPORTED = ["rhosvd_opts_default", "rhosvd_c2t", "rhosvd_result_ranks", "rhosvd_
             "rhosvd_comm_destroy", "rhosvd_gram", "rhosvd_dgemm", "rhosvd_syevj", "rhosvd_core",
             "rhosvd_chol_inv", "rhosvd_t2c", "rhosvd_cp_rank", "rhosvd_cp_factor", "rhosvd_cp_core_factor",
             "rhosvd_cp_weights", "rhosvd_cp_info", "rhosvd_cp_free", "rhosvd_c2t_host",
-            "rhosvd_result_host_frame", "rhosvd_result_host_sigma", "rhosvd_result_host_core"]
+            "rhosvd_result_host_frame", "rhosvd_result_host_sigma", "rhosvd_result_host_core",
+            "rhosvd_c2t_als"]
 
 
 def _check(status):
@@ -271,8 +273,9 @@ def _report_dict(rep: Report):
         core_ms=rep.core_ms, gram_ms=rep.gram_ms, launches=rep.launches)
 
 
-def c2t_raw(U, xi, opts: Opts, comm: Comm | None = None, stream=None):
-    """Call rhosvd_c2t; returns the raw result handle (caller frees)."""
+def c2t_raw(U, xi, opts: Opts, comm: Comm | None = None, stream=None, als_sweeps=None):
+    """Call rhosvd_c2t (or rhosvd_c2t_als when als_sweeps is given); returns the raw
+    result handle (caller frees)."""
     import torch
     U1, U2, U3 = U
     for i, u in enumerate((U1, U2, U3)):
@@ -286,8 +289,13 @@ def c2t_raw(U, xi, opts: Opts, comm: Comm | None = None, stream=None):
     h = C.c_void_p()
     st = _stream_ptr(stream)
     with torch.cuda.device(U1.device):
-        _check(lib().rhosvd_c2t(_ptr(U1), _ptr(U2), _ptr(U3), n, _ptr(xi), n, R, C.byref(opts),
-                                comm.handle if comm is not None else None, st, C.byref(h)))
+        if als_sweeps is None:
+            _check(lib().rhosvd_c2t(_ptr(U1), _ptr(U2), _ptr(U3), n, _ptr(xi), n, R, C.byref(opts),
+                                    comm.handle if comm is not None else None, st, C.byref(h)))
+        else:
+            _check(lib().rhosvd_c2t_als(_ptr(U1), _ptr(U2), _ptr(U3), n, _ptr(xi), n, R, C.byref(opts),
+                                        int(als_sweeps), comm.handle if comm is not None else None, st,
+                                        C.byref(h)))
     return h
 
 
@@ -376,7 +384,7 @@ def _wrap_dev(ptr, nelem, device):
     return out
 
 
-def c2t(U, xi, eps=None, ranks=None, comm: Comm | None = None, stream=None, keep_w=True, **kw):
+def c2t(U, xi, eps=None, ranks=None, comm: Comm | None = None, stream=None, keep_w=True, als_sweeps=None, **kw):
     """RHOSVD canonical-to-Tucker transform on the GPU (rhosvd_c2t).
 
     U: (U1, U2, U3) torch.float64 CUDA tensors of shape (R_local, n); xi: (R_local,).
@@ -384,7 +392,7 @@ def c2t(U, xi, eps=None, ranks=None, comm: Comm | None = None, stream=None, keep
     """
     import torch
     opts = make_opts(eps=eps, ranks=ranks, **kw)
-    h = c2t_raw(U, xi, opts, comm, stream)
+    h = c2t_raw(U, xi, opts, comm, stream, als_sweeps=als_sweeps)
     L = lib()
     dev = U[0].device
     try:

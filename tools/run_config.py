@@ -20,6 +20,7 @@ def main():
     ap.add_argument("--block0", type=int, default=0)
     ap.add_argument("--oversample", type=int, default=16)
     ap.add_argument("--t2c", type=float, default=None, help="also time rhosvd_t2c with this eps_rel")
+    ap.add_argument("--als", type=int, default=None, help="call rhosvd_c2t_als with this many sweeps")
     args = ap.parse_args()
     import torch
     from paper_2201_12663_b200 import rhosvd
@@ -31,7 +32,7 @@ def main():
     opts = rhosvd.make_opts(eps=p.eps, ranks=p.ranks, block0=args.block0, oversample=args.oversample)
     for i in range(args.reps):
         t0 = time.perf_counter()
-        h = rhosvd.c2t_raw((U1, U2, U3), xi, opts)
+        h = rhosvd.c2t_raw((U1, U2, U3), xi, opts, als_sweeps=args.als)
         rep = rhosvd.Report()
         lib.rhosvd_result_report(h, rhosvd.C.byref(rep))
         t2c = None
@@ -57,7 +58,7 @@ def main():
         torch.cuda.synchronize()
         d = rhosvd._report_dict(rep)
         d["wall_s"] = time.perf_counter() - t0
-        print(json.dumps({"config": args.config, "rep": i, **{k: d[k] for k in
+        print(json.dumps({"config": args.config, "rep": i, "als": args.als, **{k: d[k] for k in
                           ("ranks", "block", "iters", "grow_events", "ms", "core_ms", "gram_ms", "launches",
                            "gemm_flops", "wall_s", "tail", "beta_norm")}, "t2c": t2c}), flush=True)
 
