@@ -45,6 +45,7 @@ struct CoreArgs {
   int A1pad;         // rounded to 8 (1024-B aligned sub-tiles)
   int mt, nt, tiles, splits, kchunk, items;
   int tm0;           // first row tile of this launch (row-chunked launches)
+  int n_off, n_end;  // column segment [n_off, n_end) of this launch (edge segments)
   int stages;
   uint32_t stage_bytes, tx_bytes;
   double* out;       // beta (splits == 1) or partials [split][r1 r2 r3]
@@ -78,7 +79,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1)
     pkend = min(p.R, pk + p.kchunk);
     pa = m0 / p.r2;
     pb = m0 % p.r2;
-    pn = (tile / p.mt) * BN;
+    pn = p.n_off + (tile / p.mt) * BN;
   };
   auto issue_next = [&](int stage) {
     if (pit >= p.items) return;
@@ -124,7 +125,7 @@ __global__ void __launch_bounds__(CORE_THREADS, 1)
   for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
     const int split = it / p.tiles, tile = it % p.tiles;
     const int tm = p.tm0 + tile % p.mt, tn = tile / p.mt;
-    const int m0 = tm * CORE_BM, n0 = tn * BN;
+    const int m0 = tm * CORE_BM, n0 = p.n_off + tn * BN;
     const int a_lo = m0 / p.r2;
     const int kbeg = split * p.kchunk, kend = min(p.R, kbeg + p.kchunk);
     // W1 row (inside the box) of each fragment row this lane touches -> byte offsets
@@ -183,11 +184,11 @@ __global__ void __launch_bounds__(CORE_THREADS, 1)
 #pragma unroll
       for (int j = 0; j < FN; ++j) {
         const int n = n0 + j * 8 + 2 * fc;
-        if (even && n + 1 < p.r3) {
+        if (even && n + 1 < p.n_end) {
           *(double2*)(row + n) = make_double2(acc[i][j][0], acc[i][j][1]);
         } else {
-          if (n < p.r3) row[n] = acc[i][j][0];
-          if (n + 1 < p.r3) row[n + 1] = acc[i][j][1];
+          if (n < p.n_end) row[n] = acc[i][j][0];
+          if (n + 1 < p.n_end) row[n + 1] = acc[i][j][1];
         }
       }
     }
@@ -221,12 +222,27 @@ __global__ void wrap_rows_kernel(const double* W, int64_t ldw, int r2, int ext, 
 
 
 static int pick_bn(int64_t r3) {
-  // padded N work with a mild preference for wide tiles (fewer W1/W2 re-reads)
+  // executed columns (the leftover r3 % BN as an edge segment padded to 16, or a padded
+  // tile when that is no narrower) + ~8 column-equivalents of fixed cost per tile (A
+  // fragment formation, pipeline fill, epilogue) - fitted on cfg 4 (r3 = 652): BN 128 +
+  // edge 16: 789 ms, 96 + edge 80: 799 ms, 64 + edge 16: 834 ms, 96 padded: 809 ms
   const int cand[3] = {128, 96, 64};
   int best = 128;
   double bc = 1e300;
   for (int bn : cand) {
-    double c = (double)cdiv(r3, bn) * bn * (1.0 + 0.03 * (128.0 / bn - 1.0));
+    const int64_t full = r3 / bn, rem = r3 - full * bn;
+    double cols, tiles;
+    if (rem == 0) {
+      cols = (double)r3;
+      tiles = (double)full;
+    } else if (full > 0 && round_up(rem, 16) < bn) {
+      cols = (double)(full * bn + round_up(rem, 16));
+      tiles = (double)full + 1.0;
+    } else {
+      cols = (double)(full + 1) * bn;
+      tiles = (double)full + 1.0;
+    }
+    const double c = cols + 8.2 * tiles;
     if (c < bc) {
       bc = c;
       best = bn;
@@ -281,33 +297,72 @@ int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3,
     if (chunks && chunks->done) RH_CHECK(chunks->done(chunks->ctx, 0, 0, total, st));
     return RHOSVD_OK;
   }
-  const int BN = pick_bn(r3);
+  // 16-wide k-slabs per pipeline stage (one mbarrier round trip each); thread-safe init
+  static const int ksub = [] {
+    const char* e = getenv("RHOSVD_CORE_KSUB");
+    return (e && atoi(e) == 1) ? 1 : 2;
+  }();
+  // column segments: full BN tiles, plus (no split-K, KSUB 2) an edge segment of the r3 %
+  // BN leftover columns tiled at round_up(., 16) instead of BN, so the last column tile
+  // does not run padded DMMAs (r3 = 652, BN = 96: 672 -> 656 columns).  RHOSVD_CORE_BN
+  // forces the main BN, RHOSVD_CORE_EDGE=0 disables the edge segment.
+  static const int force_bn = [] {
+    const char* e = getenv("RHOSVD_CORE_BN");
+    const int v = e ? atoi(e) : 0;
+    return (v == 64 || v == 96 || v == 128) ? v : 0;
+  }();
+  static const bool edge_on = [] {
+    const char* e = getenv("RHOSVD_CORE_EDGE");
+    return !(e && e[0] == '0');
+  }();
+  const int BN = force_bn ? force_bn : pick_bn(r3);
   CoreArgs a{};
   a.r1 = (int)r1; a.r2 = (int)r2; a.r3 = (int)r3; a.R = (int)R;
   a.A1 = (int)std::min<int64_t>((CORE_BM - 1) / r2 + 2, r1 + 1);
   a.A1 = std::max(1, std::min(a.A1, 256));
   a.A1pad = (int)round_up(a.A1, 8);
   a.mt = (int)cdiv(M, CORE_BM);
-  a.nt = (int)cdiv(r3, BN);
-  a.tiles = a.mt * a.nt;
-  // 16-wide k-slabs per pipeline stage (one mbarrier round trip each); thread-safe init
-  static const int ksub = [] {
-    const char* e = getenv("RHOSVD_CORE_KSUB");
-    return (e && atoi(e) == 1) ? 1 : 2;
-  }();
-  a.stage_bytes = (uint32_t)((a.A1pad + CORE_BM + BN) * 128 * ksub);
-  a.tx_bytes = (uint32_t)((a.A1 + CORE_BM + BN) * 128 * ksub);
-  const size_t budget = 227 * 1024 - 1024 - 256;
-  a.stages = (int)std::min<size_t>(8, budget / a.stage_bytes);
-  if (a.stages < 2) return fail(RHOSVD_EINVAL, "core: tile does not fit shared memory");
   const int sms = num_sms();
   int splits = core_splits(r1, r2, r3, R, BN);
   while (splits > 1 && (size_t)splits * total > part_cap) --splits;
   a.kchunk = (int)round_up(cdiv(R, splits), CORE_BK * ksub);
   splits = (int)cdiv(R, a.kchunk);
   a.splits = splits;
-  a.items = a.tiles * splits;
   a.out = splits > 1 ? part : beta;
+  struct Seg {
+    int bn, n_off, n_end;
+  };
+  Seg segs[2];
+  int nseg = 0;
+  {
+    const int64_t full = (r3 / BN) * BN, rem = r3 - full;
+    if (splits == 1 && ksub == 2 && edge_on && rem > 0 && full > 0 && round_up(rem, 16) < BN) {
+      segs[nseg++] = {BN, 0, (int)full};
+      segs[nseg++] = {(int)round_up(rem, 16), (int)full, (int)r3};
+    } else {
+      segs[nseg++] = {BN, 0, (int)r3};
+    }
+  }
+  const size_t budget = 227 * 1024 - 1024 - 256;
+  CoreArgs sa[2];
+  size_t smem[2];
+  CUtensorMap t3[2];
+  for (int q = 0; q < nseg; ++q) {
+    CoreArgs& x = sa[q];
+    x = a;
+    const int bn = segs[q].bn;
+    x.n_off = segs[q].n_off;
+    x.n_end = segs[q].n_end;
+    x.nt = (int)cdiv(x.n_end - x.n_off, bn);
+    x.tiles = x.mt * x.nt;
+    x.items = x.tiles * splits;
+    x.stage_bytes = (uint32_t)((a.A1pad + CORE_BM + bn) * 128 * ksub);
+    x.tx_bytes = (uint32_t)((a.A1 + CORE_BM + bn) * 128 * ksub);
+    x.stages = (int)std::min<size_t>(8, budget / x.stage_bytes);
+    if (x.stages < 2) return fail(RHOSVD_EINVAL, "core: tile does not fit shared memory");
+    smem[q] = 1024 + (size_t)x.stages * x.stage_bytes + 2 * x.stages * sizeof(uint64_t);
+    RH_CHECK(make_tmap_2d(&t3[q], W3, r3, R, ldw, CORE_BK, bn, true));
+  }
 
   // W2ext = W2 with rows [0, BM) repeated after row r2 - 1 (the wrap inside a tile)
   const int64_t ldx = round_up(std::max<int64_t>(R, 2), 16);
@@ -317,21 +372,40 @@ int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3,
     count_launch();
     RH_LAUNCH_CHECK();
   }
-  CUtensorMap t1, t2, t3;
+  CUtensorMap t1, t2;
   RH_CHECK(make_tmap_2d(&t1, W1x, r1, R, ldw1, CORE_BK, a.A1, true));
   RH_CHECK(make_tmap_2d(&t2, ws, r2 + CORE_BM, R, ldx, CORE_BK, CORE_BM, true));
-  RH_CHECK(make_tmap_2d(&t3, W3, r3, R, ldw, CORE_BK, BN, true));
-  const size_t smem = 1024 + (size_t)a.stages * a.stage_bytes + 2 * a.stages * sizeof(uint64_t);
-  auto launch = [&](const CoreArgs& aa, cudaStream_t s) -> int {
+  auto launch_seg = [&](int q, const CoreArgs& aa, cudaStream_t s) -> int {
     const int grid = (int)std::min<int64_t>(aa.items, sms);
+    const int bn = segs[q].bn;
+    const CUtensorMap& t = t3[q];
+    const size_t sm = smem[q];
     if (ksub == 2) {
-      if (BN == 128) RH_CHECK((launch_core<128, 2>(t1, t2, t3, aa, smem, grid, s)));
-      else if (BN == 96) RH_CHECK((launch_core<96, 2>(t1, t2, t3, aa, smem, grid, s)));
-      else RH_CHECK((launch_core<64, 2>(t1, t2, t3, aa, smem, grid, s)));
-    } else {
-      if (BN == 128) RH_CHECK((launch_core<128, 1>(t1, t2, t3, aa, smem, grid, s)));
-      else if (BN == 96) RH_CHECK((launch_core<96, 1>(t1, t2, t3, aa, smem, grid, s)));
-      else RH_CHECK((launch_core<64, 1>(t1, t2, t3, aa, smem, grid, s)));
+      switch (bn) {
+        case 128: return launch_core<128, 2>(t1, t2, t, aa, sm, grid, s);
+        case 112: return launch_core<112, 2>(t1, t2, t, aa, sm, grid, s);
+        case 96: return launch_core<96, 2>(t1, t2, t, aa, sm, grid, s);
+        case 80: return launch_core<80, 2>(t1, t2, t, aa, sm, grid, s);
+        case 64: return launch_core<64, 2>(t1, t2, t, aa, sm, grid, s);
+        case 48: return launch_core<48, 2>(t1, t2, t, aa, sm, grid, s);
+        case 32: return launch_core<32, 2>(t1, t2, t, aa, sm, grid, s);
+        case 16: return launch_core<16, 2>(t1, t2, t, aa, sm, grid, s);
+        default: return fail(RHOSVD_EINVAL, "core: unsupported tile width");
+      }
+    }
+    if (bn == 128) return launch_core<128, 1>(t1, t2, t, aa, sm, grid, s);
+    if (bn == 96) return launch_core<96, 1>(t1, t2, t, aa, sm, grid, s);
+    return launch_core<64, 1>(t1, t2, t, aa, sm, grid, s);
+  };
+  // one row range [tm0, tm0 + mt) of every column segment, in order on stream s
+  auto launch_rows = [&](int tm0, int mtc, cudaStream_t s) -> int {
+    for (int q = 0; q < nseg; ++q) {
+      CoreArgs ac = sa[q];
+      ac.tm0 = tm0;
+      ac.mt = mtc;
+      ac.tiles = ac.mt * ac.nt;
+      ac.items = ac.tiles * ac.splits;
+      RH_CHECK(launch_seg(q, ac, s));
     }
     return RHOSVD_OK;
   };
@@ -344,15 +418,11 @@ int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3,
     RH_CUDA(cudaEventRecord(e0, st));
     RH_CUDA(cudaStreamWaitEvent(chunks->side, e0, 0));
     for (int c = 0; c < nch; ++c) {
-      CoreArgs ac = a;
-      ac.tm0 = (int)((int64_t)a.mt * c / nch);
+      const int tm0 = (int)((int64_t)a.mt * c / nch);
       const int tm1 = (int)((int64_t)a.mt * (c + 1) / nch);
-      ac.mt = tm1 - ac.tm0;
-      ac.tiles = ac.mt * a.nt;
-      ac.items = ac.tiles;
       cudaStream_t s = (c & 1) ? chunks->side : st;
-      RH_CHECK(launch(ac, s));
-      const int64_t m_lo = (int64_t)ac.tm0 * CORE_BM, m_hi = std::min<int64_t>(M, (int64_t)tm1 * CORE_BM);
+      RH_CHECK(launch_rows(tm0, tm1 - tm0, s));
+      const int64_t m_lo = (int64_t)tm0 * CORE_BM, m_hi = std::min<int64_t>(M, (int64_t)tm1 * CORE_BM);
       if (chunks->done) RH_CHECK(chunks->done(chunks->ctx, c, m_lo * r3, m_hi * r3, s));
     }
     RH_CUDA(cudaEventRecord(e1, chunks->side));
@@ -360,7 +430,7 @@ int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3,
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
   } else {
-    RH_CHECK(launch(a, st));
+    RH_CHECK(launch_rows(0, a.mt, st));
     if (splits > 1) {
       core_splitk_reduce<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(part, splits, total, beta);
       count_launch();
