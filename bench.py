@@ -256,7 +256,7 @@ def run_ours(args):
     traffic, traffic_src = None, None
     try:  # DRAM bytes per launch of the dominant kernel from the committed ncu capture
         tj = json.load(open(os.path.join(ROOT, "profiles", "r1_traffic.json")))
-        key = "core_kr_tma_kernel<96,2>" if dom.startswith("core") else "tma_gemm_kernel<128,128,0,0> (Gram)"
+        key = "core (K7) cfg4" if dom.startswith("core") else "tma_gemm_kernel<128,128,0,0> (Gram)"
         if key in tj and (args.config == 4 if dom.startswith("core") else args.config == 5):
             traffic, traffic_src = tj[key]["bytes"], tj[key]["capture"]
     except Exception:

@@ -309,7 +309,7 @@ int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3,
   static const int force_bn = [] {
     const char* e = getenv("RHOSVD_CORE_BN");
     const int v = e ? atoi(e) : 0;
-    return (v == 64 || v == 96 || v == 128) ? v : 0;
+    return (v == 64 || v == 80 || v == 96 || v == 112 || v == 128) ? v : 0;
   }();
   static const bool edge_on = [] {
     const char* e = getenv("RHOSVD_CORE_EDGE");
@@ -395,7 +395,8 @@ int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3,
     }
     if (bn == 128) return launch_core<128, 1>(t1, t2, t, aa, sm, grid, s);
     if (bn == 96) return launch_core<96, 1>(t1, t2, t, aa, sm, grid, s);
-    return launch_core<64, 1>(t1, t2, t, aa, sm, grid, s);
+    if (bn == 64) return launch_core<64, 1>(t1, t2, t, aa, sm, grid, s);
+    return fail(RHOSVD_EINVAL, "core: KSUB 1 supports BN 64 / 96 / 128 only");
   };
   // one row range [tm0, tm0 + mt) of every column segment, in order on stream s
   auto launch_rows = [&](int tm0, int mtc, cudaStream_t s) -> int {
