@@ -48,6 +48,9 @@ def parse():
 
 # ---------------------------------------------------------------- clocks
 class ClockSampler:
+    # nvidia-smi in loop mode during the timed region.  The period is 1 s: at 200 ms the
+    # driver queries cost ~17 ms per 965-ms step (host launches of the latency-bound
+    # eigensolver stall behind them); RHOSVD_BENCH_CLOCK_MS overrides it.
     FIELDS = ["clocks.sm", "clocks.max.sm", "power.draw", "clocks_event_reasons.hw_slowdown",
               "clocks_event_reasons.hw_thermal_slowdown", "clocks_event_reasons.sw_thermal_slowdown",
               "clocks_event_reasons.sw_power_cap"]
@@ -61,7 +64,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + ",".join(self.FIELDS),
-                 "--format=csv,noheader,nounits", "-lms", "200"],
+                 "--format=csv,noheader,nounits", "-lms", os.environ.get("RHOSVD_BENCH_CLOCK_MS", "1000")],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.th = threading.Thread(target=self._read, daemon=True)
             self.th.start()
