@@ -38,9 +38,10 @@ struct GParams {
   int tiles_m, tiles_n, tiles, items;
   int stages;
   uint32_t a_bytes, stage_bytes, tx_bytes;
+  uint32_t b_bytes;  // one k-slab of B (the stage holds KS slabs of A, then KS of B)
 };
 
-template <int BM, int BN, bool AK, bool BKM>
+template <int BM, int BN, bool AK, bool BKM, int KS>
 __global__ void __launch_bounds__(GTHREADS, 1)
     tma_gemm_kernel(const __grid_constant__ CUtensorMap tA, const __grid_constant__ CUtensorMap tB, const GParams p) {
   constexpr int WM = BM / 2, WN = BN / 4, FM = WM / 8, FN = WN / 8;
@@ -79,11 +80,17 @@ __global__ void __launch_bounds__(GTHREADS, 1)
     if (pit >= p.items) return;
     unsigned char* st = ring + (size_t)stage * p.stage_bytes;
     mbar_arrive_expect_tx(&full[stage], p.tx_bytes);
-    if (AK) tma_load_2d(st, &tA, pk, pm, &full[stage]);
-    else tma_load_2d(st, &tA, pm, pk, &full[stage]);
-    if (BKM) tma_load_2d(st + p.a_bytes, &tB, pk, pn, &full[stage]);
-    else tma_load_2d(st + p.a_bytes, &tB, pn, pk, &full[stage]);
-    pk += GBK;
+#pragma unroll
+    for (int j = 0; j < KS; ++j) {
+      unsigned char* sa_ = st + j * p.a_bytes;
+      unsigned char* sb_ = st + KS * p.a_bytes + j * p.b_bytes;
+      const int kk = pk + GBK * j;
+      if (AK) tma_load_2d(sa_, &tA, kk, pm, &full[stage]);
+      else tma_load_2d(sa_, &tA, pm, kk, &full[stage]);
+      if (BKM) tma_load_2d(sb_, &tB, kk, pn, &full[stage]);
+      else tma_load_2d(sb_, &tB, pn, kk, &full[stage]);
+    }
+    pk += GBK * KS;
     if (pk >= pkend) {
       pit += gridDim.x;
       set_item();
@@ -130,7 +137,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
     for (int i = 0; i < FM; ++i)
 #pragma unroll
       for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
-    for (int k0 = kbeg; k0 < kend; k0 += GBK, ++g) {
+    for (int k0 = kbeg; k0 < kend; k0 += GBK * KS, ++g) {
       if (producer && g >= 1) {
         const uint32_t gp = g - 1, sp = gp % p.stages;
         mbar_wait(&empty[sp], (gp / p.stages) & 1);
@@ -138,7 +145,10 @@ __global__ void __launch_bounds__(GTHREADS, 1)
       }
       const uint32_t s = g % p.stages;
       mbar_wait(&full[s], (g / p.stages) & 1);
-      const uint32_t sa = ring_s + s * p.stage_bytes, sb = sa + p.a_bytes;
+#pragma unroll
+      for (int js = 0; js < KS; ++js) {
+      const uint32_t sa = ring_s + s * p.stage_bytes + js * p.a_bytes;
+      const uint32_t sb = ring_s + s * p.stage_bytes + KS * p.a_bytes + js * p.b_bytes;
 #pragma unroll
       for (int q = 0; q < GBK / 4; ++q) {
         double af[FM], bf[FN];
@@ -150,6 +160,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
         for (int i = 0; i < FM; ++i)
 #pragma unroll
           for (int j = 0; j < FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
@@ -262,9 +273,18 @@ void Scratch::release(cudaStream_t st) {
   cap = 0;
 }
 
-template <int BM, int BN, bool AK, bool BKM>
+// k-slabs per pipeline stage (one mbarrier round trip each): 2, RHOSVD_GEMM_KS=1 for 1
+static int gemm_ks() {
+  static const int ks = [] {
+    const char* e = getenv("RHOSVD_GEMM_KS");
+    return (e && atoi(e) == 1) ? 1 : 2;
+  }();
+  return ks;
+}
+
+template <int BM, int BN, bool AK, bool BKM, int KS>
 static int launch_cfg(const GemmArgs& g, GParams gp, cudaStream_t st) {
-  auto kern = tma_gemm_kernel<BM, BN, AK, BKM>;
+  auto kern = tma_gemm_kernel<BM, BN, AK, BKM, KS>;
   CUtensorMap tA, tB;
   if (AK) RH_CHECK(make_tmap_2d(&tA, g.A, g.M, g.K, g.lda, GBK, BM, true));
   else RH_CHECK(make_tmap_2d(&tA, g.A, g.K, g.M, g.lda, BM + 8, GBK, false));
@@ -273,8 +293,9 @@ static int launch_cfg(const GemmArgs& g, GParams gp, cudaStream_t st) {
   const uint32_t a_box = AK ? BM * 128u : (BM + 8) * GBK * 8u;
   const uint32_t b_box = BKM ? BN * 128u : (BN + 8) * GBK * 8u;
   gp.a_bytes = (uint32_t)round_up(a_box, 1024);
-  gp.stage_bytes = gp.a_bytes + (uint32_t)round_up(b_box, 1024);
-  gp.tx_bytes = a_box + b_box;
+  gp.b_bytes = (uint32_t)round_up(b_box, 1024);
+  gp.stage_bytes = KS * (gp.a_bytes + gp.b_bytes);
+  gp.tx_bytes = KS * (a_box + b_box);
   const size_t budget = 227 * 1024 - 1024 - 256;
   gp.stages = (int)std::min<size_t>(8, budget / gp.stage_bytes);
   const size_t smem = 1024 + (size_t)gp.stages * gp.stage_bytes + 2 * gp.stages * sizeof(uint64_t);
@@ -288,12 +309,16 @@ static int launch_cfg(const GemmArgs& g, GParams gp, cudaStream_t st) {
   return RHOSVD_OK;
 }
 
+template <int BM, int BN, int KS>
+static int launch_layout_ks(const GemmArgs& g, const GParams& gp, cudaStream_t st) {
+  if (g.a_k && g.b_k) return launch_cfg<BM, BN, true, true, KS>(g, gp, st);
+  if (g.a_k && !g.b_k) return launch_cfg<BM, BN, true, false, KS>(g, gp, st);
+  if (!g.a_k && g.b_k) return launch_cfg<BM, BN, false, true, KS>(g, gp, st);
+  return launch_cfg<BM, BN, false, false, KS>(g, gp, st);
+}
 template <int BM, int BN>
 static int launch_layout(const GemmArgs& g, const GParams& gp, cudaStream_t st) {
-  if (g.a_k && g.b_k) return launch_cfg<BM, BN, true, true>(g, gp, st);
-  if (g.a_k && !g.b_k) return launch_cfg<BM, BN, true, false>(g, gp, st);
-  if (!g.a_k && g.b_k) return launch_cfg<BM, BN, false, true>(g, gp, st);
-  return launch_cfg<BM, BN, false, false>(g, gp, st);
+  return gemm_ks() == 2 ? launch_layout_ks<BM, BN, 2>(g, gp, st) : launch_layout_ks<BM, BN, 1>(g, gp, st);
 }
 
 int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
@@ -339,7 +364,7 @@ int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
       }
     }
   }
-  int kchunk = (int)round_up(cdiv(std::max<int64_t>(g.K, 1), splits), GBK);
+  int kchunk = (int)round_up(cdiv(std::max<int64_t>(g.K, 1), splits), GBK * gemm_ks());
   splits = (int)std::max<int64_t>(1, cdiv(std::max<int64_t>(g.K, 1), kchunk));
   gp.splits = splits;
   gp.kchunk = kchunk;
