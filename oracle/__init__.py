@@ -5,3 +5,4 @@ from .rhosvd_oracle import *  # noqa: F401,F403
 from .compare import *  # noqa: F401,F403
 from .t2c_oracle import *  # noqa: F401,F403
 from .als_oracle import *  # noqa: F401,F403
+from .conv_oracle import *  # noqa: F401,F403
