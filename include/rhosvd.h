@@ -202,6 +202,22 @@ int  rhosvd_cp_info(const rhosvd_cp* cp, double* eps_abs, double* thr, double* e
                     int32_t* max_sweeps);                                          /* host out */
 void rhosvd_cp_free(rhosvd_cp* cp);
 
+/* ---- 3-D tensor-product convolution of canonical tensors ----
+ * Theta' * P = sum_m sum_q c_m w_q (u_m^(1) * p_q^(1)) (x) (u_m^(2) * p_q^(2))
+ * (x) (u_m^(3) * p_q^(3)), "a sum of tensor products of 1D convolutions".  1-D convolution
+ * (reading C1): (u * p)_i = h sum_j u_j p_{i + floor(n/2) - j}, p_k = 0 outside
+ * [0, n) - the Riemann sum of the continuous convolution on the common grid, central n
+ * samples.  All pointers device, column-major factors:
+ *   Fa[l] : n x Ra (ld lda, even), ca : Ra   - the density (e.g. the C2C output)
+ *   Fp[l] : n x Rp (ld ldp),       cp : Rp   - the kernel
+ *   Fout[l] : n x Ra*Rp (ld n), column m*Rp + q = u_m^(l) * p_q^(l); wout : Ra*Rp = c_m w_q
+ * (caller-allocated).  Runs as one DMMA GEMM per mode against the stacked Toeplitz
+ * matrices of the kernel vectors (2 n^2 Ra Rp FLOP per mode).  EINVAL on null pointers,
+ * n < 1, ld < n, odd lda. */
+int  rhosvd_conv3d(const double* const Fa[3], int64_t lda, const double* ca, int64_t Ra,
+                   const double* const Fp[3], int64_t ldp, const double* cp, int64_t Rp, int64_t n,
+                   double h, double* const Fout[3], double* wout, rhosvd_stream stream);
+
 /* ---- kernel-level entry points (used by the parity unit tests and bench) ----
  * Each runs ONE device kernel family on `stream`, all pointers device.     */
 

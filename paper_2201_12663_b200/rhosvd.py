@@ -67,6 +67,8 @@ def lib():
         "rhosvd_c2t": (C.c_int, [P, P, P, I64, P, I64, I64, C.POINTER(Opts), P, P, C.POINTER(P)]),
         "rhosvd_c2t_host": (C.c_int, [P, P, P, I64, P, I64, I64, C.POINTER(Opts), P, P, C.POINTER(P)]),
         "rhosvd_c2t_als": (C.c_int, [P, P, P, I64, P, I64, I64, C.POINTER(Opts), I32, P, P, C.POINTER(P)]),
+        "rhosvd_conv3d": (C.c_int, [C.POINTER(P), I64, P, I64, C.POINTER(P), I64, P, I64, I64, D,
+                                    C.POINTER(P), P, P]),
         "rhosvd_result_host_frame": (C.c_int, [P, C.c_int, C.POINTER(P), C.POINTER(I64)]),
         "rhosvd_result_host_sigma": (C.c_int, [P, C.c_int, C.POINTER(P), C.POINTER(I64)]),
         "rhosvd_result_host_core": (C.c_int, [P, C.POINTER(P)]),
@@ -112,7 +114,7 @@ EXPORTED = ["rhosvd_opts_default", "rhosvd_c2t", "rhosvd_result_ranks", "rhosvd_
             "rhosvd_chol_inv", "rhosvd_t2c", "rhosvd_cp_rank", "rhosvd_cp_factor", "rhosvd_cp_core_factor",
             "rhosvd_cp_weights", "rhosvd_cp_info", "rhosvd_cp_free", "rhosvd_c2t_host",
             "rhosvd_result_host_frame", "rhosvd_result_host_sigma", "rhosvd_result_host_core",
-            "rhosvd_c2t_als"]
+            "rhosvd_c2t_als", "rhosvd_conv3d"]
 
 
 def _check(status):
@@ -586,3 +588,30 @@ def core(W1, W2, W3, xi, stream=None):
     _check(lib().rhosvd_core(_ptr(W1p), _ptr(W2p), _ptr(W3p), ld, _ptr(xi.contiguous()), r1, r2, r3, R,
                              _ptr(beta), _stream_ptr(stream)))
     return beta
+
+
+def conv3d(Fa, ca, Fp, cp, h, stream=None):
+    """rhosvd_conv3d: tensor-product convolution of two canonical tensors on one n^3 grid.
+    Fa: 3 CUDA float64 tensors (Ra, n) (row k = u_k^(l)), ca (Ra,); Fp: 3 tensors (Rp, n),
+    cp (Rp,).  Returns (F = 3 tensors (Ra*Rp, n), w (Ra*Rp,)); row m*Rp + q = u_m * p_q."""
+    import torch
+    Ra, n = Fa[0].shape
+    Rp = Fp[0].shape[0]
+    for t in list(Fa) + list(Fp) + [ca, cp]:
+        _need_cuda_f64(t, "conv3d operand")
+    dev = Fa[0].device
+    lda = n + (n & 1)
+    if lda != n:  # 16-B aligned rows for TMA: pad each density vector with one zero
+        Fa = [torch.nn.functional.pad(f, (0, 1)).contiguous() for f in Fa]
+    else:
+        Fa = [f.contiguous() for f in Fa]
+    Fp = [f.contiguous() for f in Fp]
+    F = [torch.empty(Ra * Rp, n, dtype=torch.float64, device=dev) for _ in range(3)]
+    w = torch.empty(Ra * Rp, dtype=torch.float64, device=dev)
+    pa = (C.c_void_p * 3)(*[f.data_ptr() for f in Fa])
+    pp = (C.c_void_p * 3)(*[f.data_ptr() for f in Fp])
+    po = (C.c_void_p * 3)(*[f.data_ptr() for f in F])
+    with torch.cuda.device(dev):
+        _check(lib().rhosvd_conv3d(pa, lda, _ptr(ca.contiguous()), Ra, pp, n, _ptr(cp.contiguous()), Rp, n,
+                                   float(h), po, _ptr(w), _stream_ptr(stream)))
+    return F, w
