@@ -10,6 +10,7 @@
 //     tests that run world_size 2 on one GPU or on CPU.
 #include <dlfcn.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <string>
 
@@ -52,7 +53,7 @@ constexpr int kNcclFloat64 = 8, kNcclSum = 0;
 }  // namespace
 
 int comm_allreduce(rhosvd_comm* c, double* p, int64_t count, cudaStream_t st) {
-  if (!c || c->world <= 1 || count <= 0) return RHOSVD_OK;
+  if (!c || !c->active() || count <= 0) return RHOSVD_OK;
   if (c->kind == rhosvd_comm::NCCL) {
     int r = api().allReduce(p, p, (size_t)count, kNcclFloat64, kNcclSum, c->nccl, st);
     if (r != 0)
@@ -94,6 +95,7 @@ extern "C" int rhosvd_comm_init_nccl(const uint8_t id[128], int world, int rank,
   c->kind = rhosvd_comm::NCCL;
   c->world = world;
   c->rank = rank;
+  c->force = getenv("RHOSVD_COMM_FORCE") && getenv("RHOSVD_COMM_FORCE")[0] == '1';
   NcclUid u;
   std::memcpy(u.b, id, 128);
   int r = api().commInitRank(&c->nccl, world, u, rank);
@@ -114,6 +116,7 @@ extern "C" int rhosvd_comm_init_callback(rhosvd_allreduce_fn fn, void* user, int
   c->user = user;
   c->world = world;
   c->rank = rank;
+  c->force = getenv("RHOSVD_COMM_FORCE") && getenv("RHOSVD_COMM_FORCE")[0] == '1';
   *out = c;
   return RHOSVD_OK;
 }

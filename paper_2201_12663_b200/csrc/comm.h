@@ -14,6 +14,10 @@ struct rhosvd_comm {
   rhosvd_allreduce_fn fn = nullptr;
   void* user = nullptr;
   int world = 1, rank = 0;
+  // RHOSVD_COMM_FORCE=1 at creation: a world-1 communicator still runs every collective
+  // (test hook: exercises the NCCL / comm-thread path on a single GPU)
+  bool force = false;
+  bool active() const { return world > 1 || force; }
 };
 
 namespace rhosvd {

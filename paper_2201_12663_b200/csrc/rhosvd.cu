@@ -394,7 +394,7 @@ static int mm(Ctx& c, int64_t M, int64_t N, int64_t K, const double* A, int64_t 
 }
 
 static int allreduce(Ctx& c, double* p, int64_t count) {
-  if (!c.comm || c.comm->world <= 1) return RHOSVD_OK;
+  if (!c.comm || !c.comm->active()) return RHOSVD_OK;
   if (comm_trace()) fprintf(stderr, "[rhosvd comm] rank %d mode %d count %lld\n", c.comm->rank, c.m ? c.mode : -1, (long long)count);
   c.tm->mark(PH_COMM);
   if (c.sched) return c.sched->post(c.mode, p, count, c.st);
@@ -1118,7 +1118,7 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
     RH_CUDA(cudaGetDevice(&dev));
     std::unique_ptr<CommSched> sched;
     std::thread comm_thread;
-    if (comm && comm->world > 1) {
+    if (comm && comm->active()) {
       sched.reset(new CommSched());
       sched->comm = comm;
       sched->dev = dev;
@@ -1238,7 +1238,7 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
     if (total > 0) {
       RH_CHECK(HC().get((void**)&res->hbeta, (size_t)total * sizeof(double)));
       bd.host = res->hbeta;
-      if (world == 1) {  // with a communicator beta is complete only after the all-reduce
+      if (!(comm && comm->active())) {  // with a communicator beta is complete only after the all-reduce
         cudaStream_t* ms = mode_streams();
         if (!ms) return fail(RHOSVD_ECUDA, "mode stream creation failed");
         static const int nchunks = [] {
@@ -1338,7 +1338,7 @@ int rhosvd_c2t_als(const double* U1, const double* U2, const double* U3, int64_t
                    rhosvd_result** out) {
   if (out) *out = nullptr;
   if (sweeps < 0) return fail(RHOSVD_EINVAL, "sweeps must be >= 0");
-  if (comm && comm->world > 1) return fail(RHOSVD_EINVAL, "ALS sweeps: single GPU only (comm must be NULL)");
+  if (comm && comm->active()) return fail(RHOSVD_EINVAL, "ALS sweeps: single GPU only (comm must be NULL)");
   return c2t_entry(U1, U2, U3, ldu, xi, n, R_local, opts, comm, stream, out, false, sweeps);
 }
 
