@@ -216,10 +216,20 @@ def run_ours(args):
         lib.rhosvd_result_report(h, rhosvd.C.byref(rep))
         return rhosvd._report_dict(rep)
 
-    for _ in range(args.warmup):
+    cold_ms = None
+    for wi in range(args.warmup):
+        if wi == 0:  # the cold first call (workspace / output allocation) reported separately
+            torch.cuda.synchronize(dev)
+            c0, c1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            c0.record(stream)
         h = step()
+        if wi == 0:
+            c1.record(stream)
         last = report_of(h)
         lib.rhosvd_result_free(h)
+        if wi == 0:
+            torch.cuda.synchronize(dev)
+            cold_ms = c0.elapsed_time(c1)
     torch.cuda.synchronize(dev)
     if distributed:
         dist.barrier()
@@ -230,13 +240,17 @@ def run_ours(args):
     e0 = torch.cuda.Event(enable_timing=True)
     e1 = torch.cuda.Event(enable_timing=True)
     reps = []
+    step_ev = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     e0.record(stream)
-    for _ in range(args.steps):
+    step_ev[0].record(stream)
+    for i in range(args.steps):
         h = step()
+        step_ev[i + 1].record(stream)
         reps.append(report_of(h))
         lib.rhosvd_result_free(h)
     e1.record(stream)
     torch.cuda.synchronize(dev)
+    per_step = sorted(step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(args.steps))
     clk = clocks.stop()
     ms_max = max_over_ranks(e0.elapsed_time(e1), dev)
     value = p.R * args.steps / (ms_max * 1e-3)
@@ -335,6 +349,8 @@ def run_ours(args):
                        "eps": p.eps, "ranks": p.ranks, "parallelism": f"R-sharded x{world}",
                        "l2": "inputs (3 n R fp64 = %.2f GB) larger than L2; no flush" % (3 * p.n * p.R * 8 / 1e9)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
+            "step_ms": {"median": per_step[len(per_step) // 2], "min": per_step[0], "max": per_step[-1],
+                        "cold_first_call": cold_ms, "note": "this rank's per-step CUDA-event times"},
             "clocks": clk,
             "result": {"ranks": rep["ranks"], "block": rep["block"], "iters": rep["iters"],
                        "tail": rep["tail"], "beta_norm": rep["beta_norm"], "phase_ms": rep["ms"],
