@@ -1057,9 +1057,17 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
     }
     return RHOSVD_OK;
   };
+  for (int l = 0; l < 3; ++l) Uh[l] = w.Uh.p + (size_t)l * LDN * Rp;
+  // Streamed host path (host inputs, one GPU, concurrent modes): each mode's thread
+  // normalises its side matrix, forms its Gram and starts its eigensolve as soon as ITS
+  // H2D copy has landed, so the eigensolves of the first modes overlap the copies of the
+  // later ones (the copy engine, not the SMs, bounds the input phase).  xi' and the
+  // non-finite checks follow from per-mode flags.
+  const bool streamed = hin && modes_concurrent() && !(comm && comm->active()) && Rl > 0;
+  float gram_ms_streamed = 0.f;
   const bool early_gram = hin != nullptr;
+  if (!streamed) {
   for (int l = 0; l < 3; ++l) {
-    Uh[l] = w.Uh.p + (size_t)l * LDN * Rp;
     if (hin) RH_CUDA(cudaStreamWaitEvent(st, evU[l], 0));
     RH_CHECK(k_normalize(U[l], ldu, n, Rl, Rp, Uh[l], LDN, w.s.p + l * Rp, w.tcol.p + l * Rp, w.flag, st));
     RH_CHECK(k_fixed_sum(w.tcol.p + l * Rp, Rp, w.scal.p + 4 + l, st));
@@ -1102,6 +1110,7 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
   }
   RH_CHECK(allreduce(c, w.G.p, 3 * LDN * LDN));
   TL().mark(-1, "Gram", st);
+  }  // !streamed
   tm.mark(PH_EIG);
 
   // ---- S3-S5 per mode.  The three modes are independent; on one GPU (no collectives
@@ -1133,6 +1142,50 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
     double mflops[3] = {0, 0, 0};
     int mlaunch[3] = {0, 0, 0};
     double mphase[3][16] = {{0}};
+    // streamed path: per-mode "normalised" events and a host signal so the main thread
+    // can queue xi' (which needs all three column-norm vectors) behind them
+    cudaEvent_t evN[3] = {nullptr, nullptr, nullptr}, evG[3][2] = {{nullptr, nullptr}};
+    std::mutex nmu;
+    std::condition_variable ncv;
+    int nready = 0;
+    if (streamed)
+      for (int l = 0; l < 3; ++l) {
+        RH_CUDA(cudaEventCreateWithFlags(&evN[l], cudaEventDisableTiming));
+        RH_CUDA(cudaEventCreate(&evG[l][0]));
+        RH_CUDA(cudaEventCreate(&evG[l][1]));
+      }
+    auto prep_mode = [&](Ctx& cl, int l) -> int {
+      struct Signal {  // signal the main thread on every path (no deadlock on errors)
+        std::mutex& mu; std::condition_variable& cv; int& k; bool done = false;
+        void fire() {
+          if (done) return;
+          done = true;
+          { std::lock_guard<std::mutex> lk(mu); ++k; }
+          cv.notify_all();
+        }
+        ~Signal() { fire(); }
+      } sig{nmu, ncv, nready};
+      cudaStream_t ls = cl.st;
+      int* fl = w.flag + 1 + l;
+      RH_CUDA(cudaStreamWaitEvent(ls, evU[l], 0));
+      RH_CHECK(k_normalize(U[l], ldu, n, Rl, Rp, Uh[l], LDN, w.s.p + l * Rp, w.tcol.p + l * Rp, fl, ls));
+      RH_CHECK(k_fixed_sum(w.tcol.p + l * Rp, Rp, w.scal.p + 4 + l, ls));
+      RH_CUDA(cudaEventRecord(evN[l], ls));
+      sig.fire();
+      RH_CUDA(cudaEventRecord(evG[l][0], ls));
+      RH_CHECK(mm(cl, n, n, Rl, Uh[l], LDN, false, Uh[l], LDN, false, w.G.p + (size_t)l * LDN * LDN, LDN, nullptr,
+                  true));
+      RH_CUDA(cudaEventRecord(evG[l][1], ls));
+      double tl = 0.0;
+      int fh = 0;
+      RH_CUDA(cudaMemcpyAsync(&tl, w.scal.p + 4 + l, sizeof(double), cudaMemcpyDeviceToHost, ls));
+      RH_CUDA(cudaMemcpyAsync(&fh, fl, sizeof(int), cudaMemcpyDeviceToHost, ls));
+      RH_CUDA(cudaStreamSynchronize(ls));
+      if (fh) return fail(RHOSVD_ENONFINITE, "NaN/Inf in U");
+      rep.trace[l] = tl;
+      TL().mark(l, "normalize + Gram", ls);
+      return RHOSVD_OK;
+    };
     auto run = [&](int l) {
       cudaSetDevice(dev);
       g_launches = 0;
@@ -1142,6 +1195,16 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
       cl.m = &w.mw[l];
       cl.sched = sched.get();
       cl.mode = l;
+      if (streamed) {
+        mst[l] = prep_mode(cl, l);
+        if (mst[l] != RHOSVD_OK) {
+          merr[l] = g_err;
+          mtm.mark(-1);
+          mtm.collect(mphase[l]);
+          mlaunch[l] = g_launches;
+          return;
+        }
+      }
       mst[l] = solve_mode(cl, l, n, LDN, Rl, Rp, Rg, Uh[l], w.G.p + (size_t)l * LDN * LDN, rep.trace[l], o, mo[l]);
       if (cl.sched) cl.sched->finish(l);
       mtm.mark(-1);
@@ -1150,10 +1213,50 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
       mflops[l] = cl.flops;
       mlaunch[l] = g_launches;
     };
-    std::thread t1(run, 1), t2(run, 2);
-    run(0);
-    t1.join();
-    t2.join();
+    if (streamed) {
+      std::thread t0(run, 0), t1(run, 1), t2(run, 2);
+      {  // xi' behind the three normalisations (the core needs it; the eigensolves do not)
+        std::unique_lock<std::mutex> lk(nmu);
+        ncv.wait(lk, [&] { return nready == 3; });
+      }
+      int xs = RHOSVD_OK;
+      for (int l = 0; l < 3 && xs == RHOSVD_OK; ++l)
+        if (cudaStreamWaitEvent(st, evN[l], 0) != cudaSuccess) xs = fail(RHOSVD_ECUDA, "event wait");
+      if (xs == RHOSVD_OK && cudaStreamWaitEvent(st, evX, 0) != cudaSuccess) xs = fail(RHOSVD_ECUDA, "event wait");
+      if (xs == RHOSVD_OK) xs = k_xiprime(xi, w.s.p, w.s.p + Rp, w.s.p + 2 * Rp, Rl, Rp, w.xip.p, w.xip2.p, w.flag, st);
+      if (xs == RHOSVD_OK) xs = k_fixed_sum(w.xip2.p, Rp, w.scal.p + 7, st);
+      t0.join();
+      t1.join();
+      t2.join();
+      if (xs != RHOSVD_OK) return xs;
+      double x2 = 0.0;
+      int fx = 0;
+      RH_CUDA(cudaMemcpyAsync(&x2, w.scal.p + 7, sizeof(double), cudaMemcpyDeviceToHost, st));
+      RH_CUDA(cudaMemcpyAsync(&fx, w.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
+      RH_CUDA(cudaStreamSynchronize(st));
+      for (int l = 0; l < 3; ++l) {
+        float gm = 0.f;
+        if (mst[l] == RHOSVD_OK && cudaEventElapsedTime(&gm, evG[l][0], evG[l][1]) == cudaSuccess) gram_ms_streamed += gm;
+        cudaEventDestroy(evN[l]);
+        cudaEventDestroy(evG[l][0]);
+        cudaEventDestroy(evG[l][1]);
+      }
+      if (fx) {
+        cudaDeviceSynchronize();
+        for (int q = 0; q < 3; ++q) {
+          OC().put(mo[q].Z);
+          OC().put(mo[q].W);
+          OC().put(mo[q].sigma);
+        }
+        return fail(RHOSVD_ENONFINITE, "NaN/Inf in xi");
+      }
+      rep.xi_norm = std::sqrt(x2);
+    } else {
+      std::thread t1(run, 1), t2(run, 2);
+      run(0);
+      t1.join();
+      t2.join();
+    }
     if (comm_thread.joinable()) comm_thread.join();
     g_launches += mlaunch[0] + mlaunch[1] + mlaunch[2];
     c.flops += mflops[0] + mflops[1] + mflops[2];
@@ -1315,7 +1418,8 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
   rep.bound_ns = rep.xi_norm * std::sqrt(st2);  // reading A12
   tm.collect(rep.ms);
   float gms = 0.f, cms = 0.f;
-  cudaEventElapsedTime(&gms, g0, g1);
+  if (streamed) gms = gram_ms_streamed;
+  else cudaEventElapsedTime(&gms, g0, g1);
   cudaEventElapsedTime(&cms, c0, c1);
   rep.gram_ms = gms;
   rep.core_ms = cms;

@@ -74,3 +74,24 @@ def test_host_api_device_result_has_no_host_outputs(rh):
         assert rh.lib().rhosvd_result_host_core(h, C.byref(b)) == -1  # EINVAL
     finally:
         rh.lib().rhosvd_result_free(h)
+
+
+@pytest.mark.parametrize("where", ["U2", "xi"])
+def test_host_api_nonfinite_rejected(rh, where):
+    """Streamed host path: a NaN in a side matrix (caught by that mode's own flag) or an
+    Inf in xi (caught after the modes) fails the call with ENONFINITE; the library stays
+    usable afterwards."""
+    p = make_random_params(40, 90, seed=7, ranks=(3, 3, 3))
+    U1, U2, U3, xi = make_config(p, backend="torch", device=torch.device("cuda"))
+    hU = [u.cpu().pin_memory() for u in (U1, U2, U3)]
+    hx = xi.cpu().pin_memory()
+    if where == "U2":
+        hU[1][5, 3] = float("nan")
+    else:
+        hx[7] = float("inf")
+    with pytest.raises(rh.RhosvdError) as ei:
+        rh.c2t_host(hU, hx, ranks=p.ranks)
+    assert ei.value.status == -2  # ENONFINITE
+    ok = rh.c2t_host([u.cpu().pin_memory() for u in (U1, U2, U3)], xi.cpu().pin_memory(), ranks=p.ranks)
+    assert ok.ranks == (3, 3, 3)
+    ok.close()
