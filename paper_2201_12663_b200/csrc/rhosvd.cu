@@ -214,6 +214,22 @@ static cudaStream_t copy_stream() {
   return it->second;
 }
 
+// the stream the chunked beta all-reduce runs on (created once per device)
+static cudaStream_t coll_stream() {
+  static std::mutex mu;
+  static std::map<int, cudaStream_t> per_dev;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return nullptr;
+  std::lock_guard<std::mutex> lk(mu);
+  auto it = per_dev.find(dev);
+  if (it == per_dev.end()) {
+    cudaStream_t s = nullptr;
+    if (cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking) != cudaSuccess) return nullptr;
+    it = per_dev.emplace(dev, s).first;
+  }
+  return it->second;
+}
+
 // host inputs of rhosvd_c2t_host
 struct HostIn {
   const double* U[3];
@@ -948,6 +964,27 @@ static int beta_chunk_d2h(void* ctx, int, int64_t e0, int64_t e1, cudaStream_t s
   return RHOSVD_OK;
 }
 
+// R-sharded core: all-reduce each finished row chunk of beta on the collective stream
+// while the next chunks are still being contracted (every rank issues the chunks in the
+// same order from one thread, so the NCCL calls match)
+struct BetaAR {
+  rhosvd_comm* comm;
+  double* beta;
+  cudaStream_t cs;
+};
+static int beta_chunk_allreduce(void* ctx, int, int64_t e0, int64_t e1, cudaStream_t s) {
+  auto* b = (BetaAR*)ctx;
+  if (e1 <= e0) return RHOSVD_OK;
+  cudaEvent_t ev;
+  RH_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  RH_CUDA(cudaEventRecord(ev, s));
+  RH_CUDA(cudaStreamWaitEvent(b->cs, ev, 0));
+  cudaEventDestroy(ev);
+  if (comm_trace()) fprintf(stderr, "[rhosvd comm] rank %d beta chunk [%lld, %lld)\n", b->comm->rank, (long long)e0,
+                            (long long)e1);
+  return comm_allreduce(b->comm, b->beta + e0, e1 - e0, b->cs);
+}
+
 static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_t n, int64_t Rl,
                     const rhosvd_opts& o, rhosvd_comm* comm, cudaStream_t st, rhosvd_result* res,
                     const HostIn* hin = nullptr, int als_sweeps = 0) {
@@ -1356,6 +1393,25 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
     }
   }
 
+  // R-sharded (NCCL): the beta all-reduce overlaps the contraction chunk by chunk
+  BetaAR bar{comm, nullptr, nullptr};
+  bool chunked_ar = false;
+  if (!chunks.done && total > 0 && comm && comm->active() && comm->kind == rhosvd_comm::NCCL) {
+    cudaStream_t* ms = mode_streams();
+    bar.cs = coll_stream();
+    if (ms && bar.cs) {
+      static const int nchunks = [] {
+        const char* e = getenv("RHOSVD_CORE_CHUNKS");
+        return e ? std::max(1, atoi(e)) : 8;
+      }();
+      chunks.count = nchunks;
+      chunks.side = ms[1];
+      chunks.done = beta_chunk_allreduce;
+      chunks.ctx = &bar;
+      chunked_ar = true;
+    }
+  }
+
   // ---- S6 core (K7): beta = (W1 (.) W2)(xi' o W3)^T, then all-reduce
   tm.mark(PH_CORE);
   cudaEvent_t c0, c1;
@@ -1366,6 +1422,7 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
     if (dbg_on()) dt.mark(0);
     RH_CHECK(OC().get((void**)&res->beta, (size_t)total * sizeof(double)));
     bd.dev = res->beta;
+    bar.beta = res->beta;
     if (dbg_on()) dt.mark(1);
     RH_CHECK(w.W1x.ensure((size_t)r1 * Rp, st));
     if (Rl > 0) {
@@ -1390,10 +1447,18 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
       RH_CUDA(cudaMemsetAsync(res->beta, 0, (size_t)total * sizeof(double), st));
       cudaEventRecord(c0, st);
       cudaEventRecord(c1, st);
-      if (chunks.done) RH_CHECK(beta_chunk_d2h(&bd, 0, 0, total, st));
+      if (chunks.done) RH_CHECK(chunks.done(chunks.ctx, 0, 0, total, st));
     }
-    RH_CHECK(allreduce(c, res->beta, total));
-    if (hin && !chunks.done) RH_CHECK(beta_chunk_d2h(&bd, 0, 0, total, st));
+    if (chunked_ar) {  // the chunks' all-reduces were queued on the collective stream
+      cudaEvent_t ev;
+      RH_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+      RH_CUDA(cudaEventRecord(ev, bar.cs));
+      RH_CUDA(cudaStreamWaitEvent(st, ev, 0));
+      cudaEventDestroy(ev);
+    } else {
+      RH_CHECK(allreduce(c, res->beta, total));
+    }
+    if (hin && (chunked_ar || !chunks.done)) RH_CHECK(beta_chunk_d2h(&bd, 0, 0, total, st));
     tm.mark(PH_CORE);
     RH_CHECK(k_sumsq(res->beta, total, w.part.p, w.scal.p + 12, st));
   } else {
