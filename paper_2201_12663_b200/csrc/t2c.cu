@@ -18,6 +18,7 @@
 // (Z1 U, Z2 V) and a column gather of Z3.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <vector>
 
@@ -599,6 +600,14 @@ int rhosvd_t2c(const rhosvd_result* res, double eps_rel, rhosvd_stream stream, r
     cp->max_sweeps = std::max(cp->max_sweeps, hs[m]);
   }
   cp->R = R;
+  if (getenv("RHOSVD_DEBUG") && getenv("RHOSVD_DEBUG")[0] == '1') {  // sweep-count histogram
+    std::vector<int> hist(T2C_MAX_SWEEPS + 1, 0);
+    for (int m = 0; m < r3; ++m) hist[std::max(0, std::min(hs[m], T2C_MAX_SWEEPS))]++;
+    fprintf(stderr, "[rhosvd dbg] t2c %s path, sweeps histogram:", small ? "smem" : "block");
+    for (int k = 0; k <= T2C_MAX_SWEEPS; ++k)
+      if (hist[k]) fprintf(stderr, " %d:%d", k, hist[k]);
+    fprintf(stderr, "\n");
+  }
   // exact error^2 (the slices are orthogonal in mode 3): the discarded energy, summed in slice order
   cp->err2 = 0.0;
   for (int m = 0; m < r3; ++m) cp->err2 += hd[m];
