@@ -37,6 +37,7 @@ namespace rhosvd {
 
 thread_local std::string g_err;
 thread_local int g_launches = 0;
+thread_local int g_coop_cap = 0;
 
 void set_error(const std::string& msg) { g_err = msg; }
 int fail(int status, const std::string& msg) {
@@ -1226,6 +1227,16 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
     auto run = [&](int l) {
       cudaSetDevice(dev);
       g_launches = 0;
+      struct CapGuard {  // cooperative grids of this mode: 1.5 CTAs per SM (see common.cuh)
+        CapGuard() {
+          static const int per2 = [] {  // RHOSVD_COOP_MODE_CAP: CTAs per 2 SMs (0 = no cap)
+            const char* e = getenv("RHOSVD_COOP_MODE_CAP");
+            return e ? std::max(0, atoi(e)) : 2;
+          }();
+          g_coop_cap = per2 ? std::max(1, num_sms() * per2 / 2) : 0;
+        }
+        ~CapGuard() { g_coop_cap = 0; }
+      } cap_guard;
       PhaseTimer mtm(ms[l]);
       mtm.mark(PH_EIG);
       Ctx cl{ms[l], comm, w, &rep, &mtm};

@@ -667,6 +667,7 @@ static int coop_grid(const void* kern, int threads, size_t smem, int64_t want_bl
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, threads, smem);
   if (occ < 1) occ = 1;
   int64_t maxb = std::min<int64_t>((int64_t)occ * num_sms(), cap);
+  if (g_coop_cap > 0) maxb = std::min<int64_t>(maxb, g_coop_cap);
   int64_t g = std::min<int64_t>(maxb, std::max<int64_t>(1, want_blocks));
   return (int)g;
 }
