@@ -723,7 +723,9 @@ int syevj(int64_t b, const double* A, int64_t lda, double* lambda, double* Vout,
         cudaFuncSetAttribute(jacobi_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     RH_CUDA(attr_b);
     int64_t want = (int64_t)bj.h * (bj.h - 1) / 2 + cdiv(bj.bp, BJ_VT) * bj.h;
-    int grid = coop_grid((const void*)jacobi_block_kernel, threads, smem, want);
+    // one CTA per SM: the grid barriers (two per round) cost more with 3 CTAs per SM than
+    // the extra phase-2 items per CTA (b = 732: 444 CTAs 51.5 ms, 296: 38.5, 148: 36.3, 74: 51.3)
+    int grid = coop_grid((const void*)jacobi_block_kernel, threads, smem, std::min<int64_t>(want, num_sms()));
     static const int tsm = [] {
       const char* e = getenv("RHOSVD_TS");
       return (e && e[0] == '1') ? 1 : 0;
