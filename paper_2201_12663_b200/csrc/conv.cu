@@ -17,9 +17,8 @@
 // Toeplitz block is materialised in chunks of kernel terms (HBM traffic n^2 per term,
 // well under the GEMM time for R_a >= ~32), and O, column-major with ld = R_p n, IS the
 // output factor matrix (n x R_a R_p, ld n): column m R_p + q = u_m * p_q (reading C2).
-// O(n^2) per 1-D convolution against the paper's O(n log n) (FFT): on the tensor pipe
-// the dense form is faster up to n ~ 16k at the ranks of the paper's applications
-// (DESIGN.md section 11c).
+// That dense route is O(n^2) per 1-D convolution; for n <= 2730 (N = 2^k >= 1.5 n <=
+// 4096) the FFT route below (O(n log n), the paper's complexity) is used instead.
 #include <algorithm>
 
 #include "gemm.cuh"
@@ -36,6 +35,100 @@ __global__ void toeplitz_stack_kernel(const double* P, int64_t ldp, int n, int q
   const int q = (int)(r / n), i = (int)(r % n);
   const int k = i + n / 2 - j;
   T[(int64_t)j * ldt + r] = (k >= 0 && k < n) ? P[(int64_t)(q0 + q) * ldp + k] : 0.0;
+}
+
+// ---------------------------------------------------------------- FFT route (N <= 4096)
+// The convolution theorem: with N = 2^k >= 1.5 n the circular convolution of the
+// zero-padded vectors equals the linear one on the central window [s, s + n) (no wrap:
+// the full convolution has length 2n - 1 and s + N > 2n - 2), so
+//     (u * p)_i = h Re( IDFT_N( DFT_N(u) . DFT_N(p) ) )_{i + s}.
+// One CTA per transform, the signal in shared memory (N complex doubles <= 64 KB),
+// radix-2: forward transforms by decimation in frequency (spectra kept in bit-reversed
+// order), the inverse by decimation in time (bit-reversed in, natural out),
+// twiddles exp(-2 pi i k / N) from a table built with sincospi (accurate to an ulp).
+// O(n log n) per 1-D convolution, as the paper's tensor-product convolution.
+constexpr int FFT_THREADS = 256, FFT_MAXN = 4096;
+
+__global__ void twiddle_kernel(int N, double2* tw) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= N / 2) return;
+  double sn, cs;
+  sincospi(-2.0 * (double)k / (double)N, &sn, &cs);
+  tw[k] = make_double2(cs, sn);
+}
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+
+// in-place forward DFT of A by decimation in time (bit-reversed input order -> natural
+// output order)
+__device__ void fft_radix2(double2* A, int N, const double2* __restrict__ tw) {
+  for (int len = 2; len <= N; len <<= 1) {
+    const int half = len >> 1, step = N / len;
+    for (int b = threadIdx.x; b < N / 2; b += blockDim.x) {
+      const int grp = b / half, pos = b - grp * half;
+      const int i = grp * len + pos, j = i + half;
+      const double2 t = cmul(__ldg(&tw[pos * step]), A[j]);
+      const double2 a = A[i];
+      A[i] = make_double2(a.x + t.x, a.y + t.y);
+      A[j] = make_double2(a.x - t.x, a.y - t.y);
+    }
+    __syncthreads();
+  }
+}
+
+// in-place forward DFT of A by decimation in frequency (natural input order -> bit-reversed
+// output order), the mirror of fft_radix2: the spectra are kept in bit-reversed order, so
+// every global access below is coalesced and no permutation is ever done
+__device__ void fft_dif(double2* A, int N, const double2* __restrict__ tw) {
+  for (int len = N; len >= 2; len >>= 1) {
+    const int half = len >> 1, step = N / len;
+    for (int b = threadIdx.x; b < N / 2; b += blockDim.x) {
+      const int grp = b / half, pos = b - grp * half;
+      const int i = grp * len + pos, j = i + half;
+      const double2 a = A[i], c = A[j];
+      A[i] = make_double2(a.x + c.x, a.y + c.y);
+      A[j] = cmul(__ldg(&tw[pos * step]), make_double2(a.x - c.x, a.y - c.y));
+    }
+    __syncthreads();
+  }
+}
+
+// spectra (bit-reversed order) of the real vectors X[v] (n values each, ld ldx),
+// zero-padded to N: S[v N + j], one CTA per vector
+__global__ void __launch_bounds__(FFT_THREADS) fft_forward_kernel(const double* X, int64_t ldx, int n, int N,
+                                                                  int logN, const double2* tw, double2* S) {
+  extern __shared__ double2 A[];
+  const int v = blockIdx.x;
+  const double* x = X + (int64_t)v * ldx;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) A[j] = make_double2(j < n ? x[j] : 0.0, 0.0);
+  __syncthreads();
+  fft_dif(A, N, tw);
+  double2* out = S + (int64_t)v * N;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) out[j] = A[j];
+}
+
+// out column (m Rp + q) of the factor = h Re(IDFT(Su[m] . Sp[q]))[s .. s + n), one CTA per pair
+__global__ void __launch_bounds__(FFT_THREADS) fft_pair_kernel(const double2* Su, const double2* Sp, int Rp, int n,
+                                                               int N, int logN, const double2* tw, double h,
+                                                               double* F) {
+  extern __shared__ double2 A[];
+  const int pr = blockIdx.x, m = pr / Rp, q = pr - m * Rp;
+  const double2* su = Su + (int64_t)m * N;
+  const double2* sp = Sp + (int64_t)q * N;
+  // IDFT(Y) = conj(DFT(conj(Y))) / N; Y arrives in bit-reversed order, which is the input
+  // order of the decimation-in-time transform (natural-order output)
+  for (int j = threadIdx.x; j < N; j += blockDim.x) {
+    const double2 y = cmul(__ldg(&su[j]), __ldg(&sp[j]));
+    A[j] = make_double2(y.x, -y.y);
+  }
+  __syncthreads();
+  fft_radix2(A, N, tw);
+  const int s = n / 2;
+  const double sc = h / (double)N;
+  double* out = F + (int64_t)pr * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = sc * A[i + s].x;
 }
 
 __global__ void outer_weights_kernel(const double* ca, int Ra, const double* cp, int Rp, double* w) {
@@ -62,6 +155,44 @@ extern "C" int rhosvd_conv3d(const double* const Fa[3], int64_t lda, const doubl
   outer_weights_kernel<<<(unsigned)cdiv(Ra * Rp, 256), 256, 0, st>>>(ca, (int)Ra, cp, (int)Rp, wout);
   count_launch();
   RH_LAUNCH_CHECK();
+  int logN = 1;
+  while ((1 << logN) < (3 * n + 1) / 2) ++logN;  // N = 2^logN >= 1.5 n
+  const int N = 1 << logN;
+  // RHOSVD_CONV_ROUTE=dense|fft forces a route (tests cover both)
+  static const int route = [] {
+    const char* e = getenv("RHOSVD_CONV_ROUTE");
+    return !e ? 0 : (e[0] == 'd' ? 1 : (e[0] == 'f' ? 2 : 0));
+  }();
+  const bool use_fft = route == 2 ? N <= FFT_MAXN : (route == 0 && N <= FFT_MAXN);
+  if (use_fft) {
+    if ((int64_t)(Ra + Rp) > INT32_MAX / 2) return fail(RHOSVD_EINVAL, "conv3d: too many terms");
+    double2 *tw = nullptr, *Su = nullptr, *Sp = nullptr;
+    RH_CUDA(cudaMallocAsync((void**)&tw, (size_t)(N / 2 + 1) * sizeof(double2), st));
+    RH_CUDA(cudaMallocAsync((void**)&Su, (size_t)Ra * N * sizeof(double2), st));
+    RH_CUDA(cudaMallocAsync((void**)&Sp, (size_t)Rp * N * sizeof(double2), st));
+    twiddle_kernel<<<(unsigned)cdiv(N / 2, 256), 256, 0, st>>>(N, tw);
+    count_launch();
+    const size_t smem = (size_t)N * sizeof(double2);
+    static const cudaError_t a1 =
+        cudaFuncSetAttribute(fft_forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FFT_MAXN * 16);
+    static const cudaError_t a2 =
+        cudaFuncSetAttribute(fft_pair_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, FFT_MAXN * 16);
+    RH_CUDA(a1);
+    RH_CUDA(a2);
+    int status = RHOSVD_OK;
+    for (int l = 0; l < 3 && status == RHOSVD_OK; ++l) {
+      fft_forward_kernel<<<(unsigned)Ra, FFT_THREADS, smem, st>>>(Fa[l], lda, (int)n, N, logN, tw, Su);
+      fft_forward_kernel<<<(unsigned)Rp, FFT_THREADS, smem, st>>>(Fp[l], ldp, (int)n, N, logN, tw, Sp);
+      fft_pair_kernel<<<(unsigned)(Ra * Rp), FFT_THREADS, smem, st>>>(Su, Sp, (int)Rp, (int)n, N, logN, tw, h,
+                                                                       Fout[l]);
+      count_launch(3);
+      if (cudaGetLastError() != cudaSuccess) status = fail(RHOSVD_ECUDA, "conv3d: fft kernels");
+    }
+    cudaFreeAsync(tw, st);
+    cudaFreeAsync(Su, st);
+    cudaFreeAsync(Sp, st);
+    return status;
+  }
   // stacked Toeplitz chunk: qc kernel terms, qc n^2 doubles within ~1 GiB
   const int64_t qc = std::max<int64_t>(1, std::min<int64_t>(Rp, ((int64_t)1 << 27) / (n * n)));
   double* T = nullptr;

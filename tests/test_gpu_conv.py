@@ -25,6 +25,21 @@ def dev(x):
     return torch.as_tensor(np.ascontiguousarray(x), device="cuda")
 
 
+def test_conv3d_both_routes_subprocess():
+    """The FFT route (n <= 2730) and the dense Toeplitz-GEMM route are picked by size;
+    RHOSVD_CONV_ROUTE forces each (read once per process), so this module's parity cases
+    run once per route in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    for route in ("dense", "fft"):
+        env = dict(os.environ, RHOSVD_CONV_ROUTE=route)
+        r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.join(here, "test_gpu_conv.py"),
+                            "-k", "random or gaussians"], env=env, capture_output=True, text=True, timeout=900)
+        assert r.returncode == 0, (route, r.stdout[-3000:], r.stderr[-2000:])
+
+
 @pytest.mark.parametrize("n,Ra,Rp,seed", [(64, 5, 3, 1), (65, 7, 4, 2), (300, 20, 9, 3), (129, 1, 1, 4),
                                           (512, 33, 12, 5)])
 def test_conv3d_random(rh, n, Ra, Rp, seed):
