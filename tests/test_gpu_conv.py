@@ -79,3 +79,20 @@ def test_conv3d_gaussians_analytic(rh):
 def test_conv3d_empty_and_errors(rh):
     F, w = rh.conv3d([dev(np.zeros((0, 8)))] * 3, dev(np.zeros(0)), [dev(np.ones((2, 8)))] * 3, dev(np.ones(2)), 1.0)
     assert F[0].shape == (0, 8) and w.shape == (0,)
+
+
+@pytest.mark.parametrize("n", [1, 2, 3, 2730, 2731])
+def test_conv3d_edge_sizes(rh, n):
+    """Degenerate grids and the FFT / dense boundary (N = 2^k >= 1.5 n: 2730 -> 4096 FFT,
+    2731 -> 8192 dense route)."""
+    rng = np.random.default_rng(n)
+    Ra, Rp, h = 3, 2, 0.5
+    Fa = [rng.normal(size=(n, Ra)) for _ in range(3)]
+    Fp = [rng.normal(size=(n, Rp)) for _ in range(3)]
+    ca, cp = rng.normal(size=Ra), rng.normal(size=Rp)
+    F, w = rh.conv3d([dev(f.T) for f in Fa], dev(ca), [dev(f.T) for f in Fp], dev(cp), h)
+    Fo, wo = conv3d_canonical(Fa, ca, Fp, cp, h)
+    for l in range(3):
+        got = F[l].cpu().numpy().T
+        scale = np.repeat(np.abs(Fa[l]).max(axis=0), Rp) * np.tile(np.abs(Fp[l]).max(axis=0), Ra)
+        assert np.all(np.abs(got - Fo[l]) <= 1e-13 * max(n, 8) * h * scale[None, :])

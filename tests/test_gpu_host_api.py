@@ -95,3 +95,14 @@ def test_host_api_nonfinite_rejected(rh, where):
     ok = rh.c2t_host([u.cpu().pin_memory() for u in (U1, U2, U3)], xi.cpu().pin_memory(), ranks=p.ranks)
     assert ok.ranks == (3, 3, 3)
     ok.close()
+
+
+def test_host_api_empty_and_tiny(rh):
+    """R_local = 0 (empty Tucker tensor) and n = 1 through the host-buffer entry point."""
+    import ctypes as C
+    e = [torch.zeros(0, 8, dtype=torch.float64) for _ in range(3)]
+    h = rh.c2t_host(e, torch.zeros(0, dtype=torch.float64), eps=1e-6)
+    assert h.ranks == (0, 0, 0)
+    h.close()
+    p = make_random_params(1, 5, seed=9, ranks=(1, 1, 1))
+    run_both(rh, p)
