@@ -131,6 +131,120 @@ __global__ void __launch_bounds__(FFT_THREADS) fft_pair_kernel(const double2* Su
   for (int i = threadIdx.x; i < n; i += blockDim.x) out[i] = sc * A[i + s].x;
 }
 
+// ---------------------------------------------------------------- four-step FFT (N > 4096)
+// N = N1 N2 (both <= 4096), j = N2 j1 + j2, k = k1 + N1 k2:
+//   X[k1 + N1 k2] = sum_j2 w_N2^(j2 k2) [ w_N^(j2 k1) sum_j1 w_N1^(j1 k1) x[N2 j1 + j2] ]
+// step 1: N2 transforms of length N1 over strided columns (TB adjacent columns per CTA, so
+// the loads are TB-wide contiguous), times the twiddle w_N^(j2 k1), stored row-major
+// Y[k1 N2 + j2]; step 2: N1 transforms of length N2 over the rows (TB rows per CTA), written
+// to X[k1 + N1 k2] (TB-wide contiguous).  Sub-transforms by decimation in time in shared
+// memory, twiddles from the one N-point table (w_len^p = w_N^(p N / len)).  The inverse of a
+// product of two spectra is the forward transform of its conjugate (real part / N).
+__device__ __forceinline__ double2 tw_get(const double2* __restrict__ tw, int N, int64_t e) {
+  // w_N^e for 0 <= e < N from the half table (w^(e + N/2) = -w^e)
+  const int h = N >> 1;
+  if (e < h) return __ldg(&tw[e]);
+  const double2 v = __ldg(&tw[e - h]);
+  return make_double2(-v.x, -v.y);
+}
+
+// cnt arrays of length L (array a at A + a * P; P = L + 1 keeps the column-wise accesses
+// of the loads / stores bank-conflict free), bit-reversed in, natural out
+__device__ void fft_dit_batch(double2* A, int L, int P, int cnt, const double2* __restrict__ tw, int Ntab) {
+  const int hl = L >> 1;
+  for (int len = 2; len <= L; len <<= 1) {
+    const int half = len >> 1, step = Ntab / len;
+    for (int b = threadIdx.x; b < cnt * hl; b += blockDim.x) {
+      const int a = b / hl, bb = b - a * hl;
+      const int grp = bb / half, pos = bb - grp * half;
+      const int i = a * P + grp * len + pos, j = i + half;
+      const double2 t = cmul(__ldg(&tw[pos * step]), A[j]);
+      const double2 u = A[i];
+      A[i] = make_double2(u.x + t.x, u.y + t.y);
+      A[j] = make_double2(u.x - t.x, u.y - t.y);
+    }
+    __syncthreads();
+  }
+}
+
+struct FS1 {  // step-1 input: a real vector (mode 0) or the conjugated product of two spectra
+  int mode;
+  const double* X;
+  int64_t ldx;
+  int n;
+  const double2* Su;
+  const double2* Sp;
+  int Rp, pair0;
+};
+__global__ void __launch_bounds__(FFT_THREADS) fft4_step1_kernel(FS1 in, int N, int N1, int N2, int logN1, int TB,
+                                                                  const double2* tw, double2* Y) {
+  extern __shared__ double2 A[];
+  const int tiles = N2 / TB;
+  const int t = blockIdx.x / tiles, j20 = (blockIdx.x - t * tiles) * TB;
+  const double* x = nullptr;
+  const double2 *su = nullptr, *sp = nullptr;
+  if (in.mode == 0) {
+    x = in.X + (int64_t)t * in.ldx;
+  } else {
+    const int pr = in.pair0 + t, m = pr / in.Rp, q = pr - m * in.Rp;
+    su = in.Su + (int64_t)m * N;
+    sp = in.Sp + (int64_t)q * N;
+  }
+  for (int e = threadIdx.x; e < TB * N1; e += blockDim.x) {
+    const int a = e % TB, j1 = e / TB;
+    const int64_t j = (int64_t)N2 * j1 + j20 + a;
+    double2 v;
+    if (in.mode == 0) {
+      v = make_double2(j < in.n ? x[j] : 0.0, 0.0);
+    } else {
+      const double2 y = cmul(__ldg(&su[j]), __ldg(&sp[j]));
+      v = make_double2(y.x, -y.y);
+    }
+    A[a * (N1 + 1) + (int)(__brev((unsigned)j1) >> (32 - logN1))] = v;
+  }
+  __syncthreads();
+  fft_dit_batch(A, N1, N1 + 1, TB, tw, N);
+  double2* out = Y + (int64_t)t * N;
+  for (int e = threadIdx.x; e < TB * N1; e += blockDim.x) {
+    const int a = e % TB, k1 = e / TB;
+    const int j2 = j20 + a;
+    out[(int64_t)k1 * N2 + j2] = cmul(A[a * (N1 + 1) + k1], tw_get(tw, N, (int64_t)j2 * k1));
+  }
+}
+
+struct FS2 {  // step-2 output: a spectrum (mode 0) or the central window of an inverse (mode 1)
+  int mode;
+  double2* S;
+  double* F;
+  int n;
+  double scale;  // h / N (mode 1)
+  int pair0;
+};
+__global__ void __launch_bounds__(FFT_THREADS) fft4_step2_kernel(const double2* Y, int N, int N1, int N2, int logN2,
+                                                                  int TB, const double2* tw, FS2 o) {
+  extern __shared__ double2 A[];
+  const int tiles = N1 / TB;
+  const int t = blockIdx.x / tiles, k10 = (blockIdx.x - t * tiles) * TB;
+  const double2* y = Y + (int64_t)t * N;
+  for (int e = threadIdx.x; e < TB * N2; e += blockDim.x) {
+    const int a = e / N2, j2 = e - a * N2;  // row k10 + a, contiguous over j2
+    A[a * (N2 + 1) + (int)(__brev((unsigned)j2) >> (32 - logN2))] = y[(int64_t)(k10 + a) * N2 + j2];
+  }
+  __syncthreads();
+  fft_dit_batch(A, N2, N2 + 1, TB, tw, N);
+  for (int e = threadIdx.x; e < TB * N2; e += blockDim.x) {
+    const int a = e % TB, k2 = e / TB;
+    const int64_t k = (int64_t)(k10 + a) + (int64_t)N1 * k2;
+    const double2 v = A[a * (N2 + 1) + k2];
+    if (o.mode == 0) {
+      o.S[(int64_t)t * N + k] = v;
+    } else {
+      const int s = o.n / 2;
+      if (k >= s && k < s + o.n) o.F[(int64_t)(o.pair0 + t) * o.n + (k - s)] = o.scale * v.x;
+    }
+  }
+}
+
 __global__ void outer_weights_kernel(const double* ca, int Ra, const double* cp, int Rp, double* w) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e < (int64_t)Ra * Rp) w[e] = ca[e / Rp] * cp[e % Rp];
@@ -164,6 +278,55 @@ extern "C" int rhosvd_conv3d(const double* const Fa[3], int64_t lda, const doubl
     return !e ? 0 : (e[0] == 'd' ? 1 : (e[0] == 'f' ? 2 : 0));
   }();
   const bool use_fft = route == 2 ? N <= FFT_MAXN : (route == 0 && N <= FFT_MAXN);
+  const bool use_fft4 = !use_fft && route != 1 && N > FFT_MAXN && logN <= 24;
+  if (use_fft4) {
+    const int logN1 = logN / 2, logN2 = logN - logN1;
+    const int N1 = 1 << logN1, N2 = 1 << logN2;
+    const int TB1 = std::min(N2, FFT_MAXN / N1), TB2 = std::min(N1, FFT_MAXN / N2);
+    const size_t sm1 = (size_t)TB1 * (N1 + 1) * sizeof(double2), sm2 = (size_t)TB2 * (N2 + 1) * sizeof(double2);
+    static const cudaError_t a3 =
+        cudaFuncSetAttribute(fft4_step1_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (FFT_MAXN + 64) * 16);
+    static const cudaError_t a4 =
+        cudaFuncSetAttribute(fft4_step2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (FFT_MAXN + 64) * 16);
+    RH_CUDA(a3);
+    RH_CUDA(a4);
+    // pair batches: the step-1 buffer holds pb transforms of N complex (<= ~512 MiB)
+    const int64_t pb = std::max<int64_t>(1, std::min<int64_t>(Ra * Rp, ((int64_t)1 << 25) / N));
+    const int64_t vb = std::max<int64_t>(Ra, Rp);
+    double2 *tw = nullptr, *Su = nullptr, *Sp = nullptr, *Y = nullptr;
+    RH_CUDA(cudaMallocAsync((void**)&tw, (size_t)(N / 2 + 1) * sizeof(double2), st));
+    RH_CUDA(cudaMallocAsync((void**)&Su, (size_t)Ra * N * sizeof(double2), st));
+    RH_CUDA(cudaMallocAsync((void**)&Sp, (size_t)Rp * N * sizeof(double2), st));
+    RH_CUDA(cudaMallocAsync((void**)&Y, (size_t)std::max(pb, vb) * N * sizeof(double2), st));
+    twiddle_kernel<<<(unsigned)cdiv(N / 2, 256), 256, 0, st>>>(N, tw);
+    count_launch();
+    int status = RHOSVD_OK;
+    auto forward = [&](const double* X, int64_t ldx, int64_t cnt, double2* S) {
+      FS1 in{0, X, ldx, (int)n, nullptr, nullptr, 0, 0};
+      fft4_step1_kernel<<<(unsigned)(cnt * (N2 / TB1)), FFT_THREADS, sm1, st>>>(in, N, N1, N2, logN1, TB1, tw, Y);
+      FS2 o{0, S, nullptr, (int)n, 0.0, 0};
+      fft4_step2_kernel<<<(unsigned)(cnt * (N1 / TB2)), FFT_THREADS, sm2, st>>>(Y, N, N1, N2, logN2, TB2, tw, o);
+      count_launch(2);
+    };
+    for (int l = 0; l < 3 && status == RHOSVD_OK; ++l) {
+      forward(Fa[l], lda, Ra, Su);
+      forward(Fp[l], ldp, Rp, Sp);
+      for (int64_t p0 = 0; p0 < Ra * Rp; p0 += pb) {
+        const int64_t cnt = std::min<int64_t>(pb, Ra * Rp - p0);
+        FS1 in{1, nullptr, 0, (int)n, Su, Sp, (int)Rp, (int)p0};
+        fft4_step1_kernel<<<(unsigned)(cnt * (N2 / TB1)), FFT_THREADS, sm1, st>>>(in, N, N1, N2, logN1, TB1, tw, Y);
+        FS2 o{1, nullptr, Fout[l], (int)n, h / (double)N, (int)p0};
+        fft4_step2_kernel<<<(unsigned)(cnt * (N1 / TB2)), FFT_THREADS, sm2, st>>>(Y, N, N1, N2, logN2, TB2, tw, o);
+        count_launch(2);
+      }
+      if (cudaGetLastError() != cudaSuccess) status = fail(RHOSVD_ECUDA, "conv3d: four-step fft kernels");
+    }
+    cudaFreeAsync(tw, st);
+    cudaFreeAsync(Su, st);
+    cudaFreeAsync(Sp, st);
+    cudaFreeAsync(Y, st);
+    return status;
+  }
   if (use_fft) {
     if ((int64_t)(Ra + Rp) > INT32_MAX / 2) return fail(RHOSVD_EINVAL, "conv3d: too many terms");
     double2 *tw = nullptr, *Su = nullptr, *Sp = nullptr;

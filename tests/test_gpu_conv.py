@@ -36,7 +36,8 @@ def test_conv3d_both_routes_subprocess():
     for route in ("dense", "fft"):
         env = dict(os.environ, RHOSVD_CONV_ROUTE=route)
         r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.join(here, "test_gpu_conv.py"),
-                            "-k", "random or gaussians"], env=env, capture_output=True, text=True, timeout=900)
+                            "-k", "random or gaussians or edge"], env=env, capture_output=True, text=True,
+                           timeout=900)
         assert r.returncode == 0, (route, r.stdout[-3000:], r.stderr[-2000:])
 
 
@@ -81,10 +82,10 @@ def test_conv3d_empty_and_errors(rh):
     assert F[0].shape == (0, 8) and w.shape == (0,)
 
 
-@pytest.mark.parametrize("n", [1, 2, 3, 2730, 2731])
+@pytest.mark.parametrize("n", [1, 2, 3, 2730, 2731, 5000, 6000])
 def test_conv3d_edge_sizes(rh, n):
-    """Degenerate grids and the FFT / dense boundary (N = 2^k >= 1.5 n: 2730 -> 4096 FFT,
-    2731 -> 8192 dense route)."""
+    """Degenerate grids and the route boundaries (N = 2^k >= 1.5 n: 2730 -> 4096 one-CTA FFT,
+    2731 -> 8192 and 5000 -> 8192, 6000 -> 16384: four-step FFT)."""
     rng = np.random.default_rng(n)
     Ra, Rp, h = 3, 2, 0.5
     Fa = [rng.normal(size=(n, Ra)) for _ in range(3)]

@@ -12,6 +12,12 @@ import torch
 from paper_2201_12663_b200 import rhosvd
 
 Ra, Rp = 100, 40
+# warm the GPU (an idle B200 sits at 120 MHz; the first milliseconds run below max clock)
+_w = torch.randn(4096, 4096, dtype=torch.float64, device="cuda")
+for _ in range(20):
+    _w = _w @ _w * 1e-3
+torch.cuda.synchronize()
+del _w
 for n in [int(a) for a in sys.argv[1:]] or [1024, 2048, 4096, 8192, 16384]:
     g = torch.Generator(device="cuda").manual_seed(n)
     Fa = [torch.randn(Ra, n, dtype=torch.float64, device="cuda", generator=g) for _ in range(3)]
