@@ -313,11 +313,110 @@ __global__ void __launch_bounds__(BJ_THREADS, 3) jacobi_block_kernel(BJParams p)
   const int nkl = h * (h - 1) / 2;
   // phase-2 thread tile: rows ty (+32), cols tx + 8c (threads 0-255; warp 8 idles there)
   const int ty = tid < 256 ? tid >> 3 : 1 << 20, tx = tid & 7;
+  // one update item: the off-diagonal pair block (k, l) (t < 0: both sides rotate) or the
+  // 64-row V tile t of pair l (k == l: V <- V Q_l), with the pairing of step stp and the
+  // rotations of buffer par (rotations are double-buffered so the V tiles of step s can be
+  // updated during phase 1 of step s + 1 by the CTAs that have no pair block there)
+  auto item = [&](int k, int l, int t, int stp, int par) {
+        int Ik, Jk, Il, Jl;
+        bj_pair(k, stp, m, Ik, Jk);
+        bj_pair(l, stp, m, Il, Jl);
+        const int* rf = p.rotf + par * h;
+        const bool rk = t < 0 && rf[k], rl = rf[l];
+        const int rows = t < 0 ? BJ_P : min(BJ_VT, bp - t * BJ_VT);
+        if (!rk && !rl) return;  // identity on both sides: the block (or V tile) is unchanged
+        const double* Qk = p.Qb + ((int64_t)par * h + k) * BJ_P * BJ_P;
+        const double* Ql = p.Qb + ((int64_t)par * h + l) * BJ_P * BJ_P;
+        if (tid < 256) {  // all loads of a thread in flight before its stores
+          // X: rows x 32 (column c of the l pair, rows of the k pair or of V tile t);
+          // thread: row r = tid % 64 (< rows), columns tid / 64 + 4 j
+          double xv[8], qkv[4], qlv[4];
+          const int r = tid & 63, c0 = tid >> 6;
+          const bool rv = r < rows;
+          const int64_t roff = (t < 0) ? (r < BJ_P ? bj_g(r, Ik, Jk) : 0) : (int64_t)t * BJ_VT + r;
+          const double* base = (t < 0) ? cur : p.V;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const int c = c0 + 4 * j;
+            xv[j] = rv ? base[(int64_t)bj_g(c, Il, Jl) * ld + roff] : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            qkv[j] = rk ? Qk[tid + 256 * j] : 0.0;
+            qlv[j] = rl ? Ql[tid + 256 * j] : 0.0;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (rv) X[r * BJ_LD + c0 + 4 * j] = xv[j];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const int e = tid + 256 * j, qr = e >> 5, qc = e & 31;
+            if (rk) S[qr * BJ_LD + qc] = qkv[j];
+            if (rl) Q[qr * BJ_LD + qc] = qlv[j];
+          }
+        }
+        __syncthreads();
+        if (rk) {  // Y = Qk^T X (32 x 32)
+          double a4[4];
+          if (tid < 256) {
+#pragma unroll
+          for (int c = 0; c < 4; ++c) a4[c] = 0.0;
+          for (int q = 0; q < BJ_P; ++q) {
+            const double qa = S[q * BJ_LD + ty];
+#pragma unroll
+            for (int c = 0; c < 4; ++c) a4[c] = fma(qa, X[q * BJ_LD + tx + 8 * c], a4[c]);
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c) Y[ty * BJ_LD + tx + 8 * c] = a4[c];
+          }
+          __syncthreads();
+          double* tmp = X; X = Y; Y = tmp;
+        }
+        // out = X Ql (or X), rows <= 64: thread rows ty, ty + 32
+        for (int r = ty; r < rows; r += 32) {
+          double a4[4];
+          if (rl) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) a4[c] = 0.0;
+            for (int q = 0; q < BJ_P; ++q) {
+              const double xa = X[r * BJ_LD + q];
+#pragma unroll
+              for (int c = 0; c < 4; ++c) a4[c] = fma(xa, Q[q * BJ_LD + tx + 8 * c], a4[c]);
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) a4[c] = X[r * BJ_LD + tx + 8 * c];
+          }
+#pragma unroll
+          for (int c = 0; c < 4; ++c) {
+            const int cc = tx + 8 * c;
+            const int gc = bj_g(cc, Il, Jl);
+            if (t < 0) {
+              const int gr = bj_g(r, Ik, Jk);
+              cur[(int64_t)gc * ld + gr] = a4[c];  // in place: block (k, l) and its mirror
+              cur[(int64_t)gr * ld + gc] = a4[c];  // belong to this item alone
+            } else {
+              p.V[(int64_t)gc * ld + t * BJ_VT + r] = a4[c];
+            }
+          }
+        }
+        if (rk) {  // restore buffer roles
+          double* tmp = X; X = Y; Y = tmp;
+        }
+        __syncthreads();
+  };
+  // the V tiles of one step, over the CTAs [c0, gridDim.x)
+  auto v_items = [&](int stp, int par, int c0) {
+    if ((int)blockIdx.x < c0) return;
+    for (int j = blockIdx.x - c0; j < vt * h; j += gridDim.x - c0) item(j / vt, j / vt, j % vt, stp, par);
+  };
   int sweeps = 0;
   bool converged = false;
+  int gs = 0, last_step = 0;  // global step counter (rotation buffer parity), last step run
   unsigned long long tacc[4] = {0, 0, 0, 0}, tq = gtimer();
   for (int sw = 0; sw < p.max_sweeps; ++sw) {
-    for (int step = 0; step < m - 1; ++step) {
+    for (int step = 0; step < m - 1; ++step, ++gs) {
+      last_step = step;
       // ---------------- phase 1: diagonalise each pair block
       for (int k = blockIdx.x; k < h; k += gridDim.x) {
         int I, J;
@@ -456,7 +555,7 @@ __global__ void __launch_bounds__(BJ_THREADS, 3) jacobi_block_kernel(BJParams p)
           }
         }
         // write Q_k, the flag and the rotated diagonal block
-        double* Qk = p.Qb + (int64_t)k * BJ_P * BJ_P;
+        double* Qk = p.Qb + ((int64_t)(gs & 1) * h + k) * BJ_P * BJ_P;
         if (rot_total && tid < 256) {  // in place: the pair's diagonal block belongs to this CTA alone
 #pragma unroll
           for (int q = 0; q < 4; ++q) {
@@ -468,113 +567,25 @@ __global__ void __launch_bounds__(BJ_THREADS, 3) jacobi_block_kernel(BJParams p)
           }
         }
         if (tid == 0) {
-          p.rotf[k] = rot_total > 0;
+          p.rotf[(gs & 1) * h + k] = rot_total > 0;
           if (rot_total) atomicAdd(&p.cnt[sw], rot_total);
         }
         __syncthreads();
       }
+      // the previous step's V tiles, by the CTAs without a pair block (all CTAs after their
+      // pair blocks when the grid is not larger than h)
+      if (gs > 0) v_items(step > 0 ? step - 1 : m - 2, (gs - 1) & 1, (int)gridDim.x > h ? h : 0);
       { unsigned long long t = gtimer(); tacc[0] += t - tq; tq = t; }
       grid_barrier(p.bar);
       { unsigned long long t = gtimer(); tacc[1] += t - tq; tq = t; }
-      // ---------------- phase 2: off-diagonal pair blocks (32 x 32) and V row tiles (64 x 32)
-      for (int it = blockIdx.x; it < nkl + vt * h; it += gridDim.x) {
-        int k, l, t = -1;
-        if (it < nkl) {
-          l = (int)((sqrtf(8.0f * (float)it + 1.0f) + 1.0f) * 0.5f);
-          while (l * (l - 1) / 2 > it) --l;
-          while ((l + 1) * l / 2 <= it) ++l;
-          k = it - l * (l - 1) / 2;  // k < l
-        } else {
-          int j = it - nkl;
-          t = j % vt;
-          l = j / vt;
-          k = l;
-        }
-        int Ik, Jk, Il, Jl;
-        bj_pair(k, step, m, Ik, Jk);
-        bj_pair(l, step, m, Il, Jl);
-        const bool rk = t < 0 && p.rotf[k], rl = p.rotf[l];
-        const int rows = t < 0 ? BJ_P : min(BJ_VT, bp - t * BJ_VT);
-        if (!rk && !rl) continue;  // identity on both sides: the block (or V tile) is unchanged
-        const double* Qk = p.Qb + (int64_t)k * BJ_P * BJ_P;
-        const double* Ql = p.Qb + (int64_t)l * BJ_P * BJ_P;
-        if (tid < 256) {  // all loads of a thread in flight before its stores
-          // X: rows x 32 (column c of the l pair, rows of the k pair or of V tile t);
-          // thread: row r = tid % 64 (< rows), columns tid / 64 + 4 j
-          double xv[8], qkv[4], qlv[4];
-          const int r = tid & 63, c0 = tid >> 6;
-          const bool rv = r < rows;
-          const int64_t roff = (t < 0) ? (r < BJ_P ? bj_g(r, Ik, Jk) : 0) : (int64_t)t * BJ_VT + r;
-          const double* base = (t < 0) ? cur : p.V;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int c = c0 + 4 * j;
-            xv[j] = rv ? base[(int64_t)bj_g(c, Il, Jl) * ld + roff] : 0.0;
-          }
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            qkv[j] = rk ? Qk[tid + 256 * j] : 0.0;
-            qlv[j] = rl ? Ql[tid + 256 * j] : 0.0;
-          }
-#pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (rv) X[r * BJ_LD + c0 + 4 * j] = xv[j];
-#pragma unroll
-          for (int j = 0; j < 4; ++j) {
-            const int e = tid + 256 * j, qr = e >> 5, qc = e & 31;
-            if (rk) S[qr * BJ_LD + qc] = qkv[j];
-            if (rl) Q[qr * BJ_LD + qc] = qlv[j];
-          }
-        }
-        __syncthreads();
-        if (rk) {  // Y = Qk^T X (32 x 32)
-          double a4[4];
-          if (tid < 256) {
-#pragma unroll
-          for (int c = 0; c < 4; ++c) a4[c] = 0.0;
-          for (int q = 0; q < BJ_P; ++q) {
-            const double qa = S[q * BJ_LD + ty];
-#pragma unroll
-            for (int c = 0; c < 4; ++c) a4[c] = fma(qa, X[q * BJ_LD + tx + 8 * c], a4[c]);
-          }
-#pragma unroll
-          for (int c = 0; c < 4; ++c) Y[ty * BJ_LD + tx + 8 * c] = a4[c];
-          }
-          __syncthreads();
-          double* tmp = X; X = Y; Y = tmp;
-        }
-        // out = X Ql (or X), rows <= 64: thread rows ty, ty + 32
-        for (int r = ty; r < rows; r += 32) {
-          double a4[4];
-          if (rl) {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) a4[c] = 0.0;
-            for (int q = 0; q < BJ_P; ++q) {
-              const double xa = X[r * BJ_LD + q];
-#pragma unroll
-              for (int c = 0; c < 4; ++c) a4[c] = fma(xa, Q[q * BJ_LD + tx + 8 * c], a4[c]);
-            }
-          } else {
-#pragma unroll
-            for (int c = 0; c < 4; ++c) a4[c] = X[r * BJ_LD + tx + 8 * c];
-          }
-#pragma unroll
-          for (int c = 0; c < 4; ++c) {
-            const int cc = tx + 8 * c;
-            const int gc = bj_g(cc, Il, Jl);
-            if (t < 0) {
-              const int gr = bj_g(r, Ik, Jk);
-              cur[(int64_t)gc * ld + gr] = a4[c];  // in place: block (k, l) and its mirror
-              cur[(int64_t)gr * ld + gc] = a4[c];  // belong to this item alone
-            } else {
-              p.V[(int64_t)gc * ld + t * BJ_VT + r] = a4[c];
-            }
-          }
-        }
-        if (rk) {  // restore buffer roles
-          double* tmp = X; X = Y; Y = tmp;
-        }
-        __syncthreads();
+      // ---------------- phase 2: off-diagonal pair blocks (32 x 32); the V tiles of this step
+      // are deferred into the next step's phase 1
+      for (int it = blockIdx.x; it < nkl; it += gridDim.x) {
+        int l = (int)((sqrtf(8.0f * (float)it + 1.0f) + 1.0f) * 0.5f);
+        while (l * (l - 1) / 2 > it) --l;
+        while ((l + 1) * l / 2 <= it) ++l;
+        const int k = it - l * (l - 1) / 2;  // k < l
+        item(k, l, -1, step, gs & 1);
       }
       { unsigned long long t = gtimer(); tacc[2] += t - tq; tq = t; }
       grid_barrier(p.bar);
@@ -586,6 +597,8 @@ __global__ void __launch_bounds__(BJ_THREADS, 3) jacobi_block_kernel(BJParams p)
       break;
     }
   }
+  // the last step's V tiles (its rotations are complete: phase 2 ended with a barrier)
+  if (gs > 0) v_items(last_step, (gs - 1) & 1, 0);
   for (int64_t i = gtid; i < b; i += gthreads) p.lam[i] = cur[i * ld + i];
   if (gtid == 0) {
     p.info[0] = sweeps;
