@@ -2,8 +2,8 @@
 (oracle/t2c_oracle.py, Remark 2.1) applied to the SAME core beta
 (the library is deterministic: rhosvd.c2t and rhosvd.c2c return bitwise-identical
 cores), so the comparison isolates the T2C step:
-  * identical per-slice kept counts p_m and total rank R (integer, exact) unless the
-    oracle flags a singular value within 1e-8 of the threshold;
+  * identical per-slice kept counts p_m and total rank R (integer, exact) except for
+    singular values within the sigma tolerance of the threshold (either side may keep them);
   * kept sigma within 1e-12 sigma_1(B_m) + 1e-10 sigma (one-sided Jacobi vs LAPACK);
   * beta_(R) from the GPU factors equal to the oracle's within 1e-11 ||beta||;
   * ||beta - beta_(R)|| <= eps and err2 equal to the oracle's discarded energy;
@@ -49,21 +49,30 @@ def check_case(rh, Us, xi, eps, ranks, t2c_eps):
     cp = rh.c2c(Us, xi, t2c_eps, eps=eps, ranks=ranks)
     o = oracle_t2c(beta, t2c_eps * np.linalg.norm(beta))
     assert abs(cp.thr - o.thr) <= 1e-12 * o.thr
-    if not o.near_tie:
-        assert cp.R == o.sigma.shape[0]
-        sl = cp.slice_of.cpu().numpy()
-        assert np.array_equal(np.bincount(sl, minlength=beta.shape[2]), o.p)
-        w = cp.w.cpu().numpy()
-        for m in range(beta.shape[2]):
-            s1 = np.linalg.norm(beta[:, :, m], 2)
-            wg, wo = w[sl == m], o.sigma[o.slice_of == m]
-            assert np.all(np.abs(wg - wo) <= 1e-12 * s1 + 1e-10 * wo)
+    # A singular value within the sigma tolerance (1e-12 sigma_1(B_m) + 1e-10 sigma) of the
+    # threshold may be kept by one side and dropped by the other: such "ambiguous" values are
+    # the only allowed difference in the per-slice counts, and each adds at most ~thr to the
+    # difference of the truncated cores and ~thr^2 to the discarded energy.
+    sl = cp.slice_of.cpu().numpy()
+    w = cp.w.cpu().numpy()
+    pg = np.bincount(sl, minlength=beta.shape[2])
+    amb_tot = 0
+    for m in range(beta.shape[2]):
+        sv = np.linalg.svd(beta[:, :, m], compute_uv=False)
+        s1 = sv[0] if sv.size else 0.0
+        amb = int(np.sum(np.abs(sv - o.thr) <= 1e-12 * s1 + 1e-10 * o.thr))
+        amb_tot += amb
+        assert abs(int(pg[m]) - int(o.p[m])) <= amb, (m, pg[m], o.p[m])
+        k = min(pg[m], o.p[m])  # the unambiguous leading values agree
+        wg, wo = np.sort(w[sl == m])[::-1][:k], o.sigma[o.slice_of == m][:k]
+        assert np.all(np.abs(wg - wo) <= 1e-12 * s1 + 1e-10 * wo)
+    assert abs(cp.R - o.sigma.shape[0]) <= amb_tot
     bR = beta_from_gpu(cp, beta.shape)
     nb = np.linalg.norm(beta)
-    assert np.linalg.norm(bR - t2c_dense(o, beta.shape)) <= 1e-11 * nb
+    assert np.linalg.norm(bR - t2c_dense(o, beta.shape)) <= 1e-11 * nb + 1.01 * np.sqrt(amb_tot) * o.thr
     err = np.linalg.norm(beta - bR)
     assert err <= cp.eps * (1 + 1e-12) + 1e-12 * nb  # + rounding (columns below 16 u ||B|| are zero)
-    assert abs(cp.err2 - o.err2) <= 1e-10 * o.err2 + 1e-13 * nb ** 2
+    assert abs(cp.err2 - o.err2) <= 1e-10 * o.err2 + 1e-13 * nb ** 2 + 1.03 * amb_tot * o.thr ** 2
     # lifted factors
     Z = [z.cpu().numpy() for z in g.Z]
     F = [f.cpu().numpy() for f in cp.F]
