@@ -245,6 +245,27 @@ __global__ void __launch_bounds__(FFT_THREADS) fft4_step2_kernel(const double2* 
   }
 }
 
+// stream-ordered device scratch released on every return path
+struct AsyncBufs {
+  cudaStream_t st;
+  void* p[4] = {nullptr, nullptr, nullptr, nullptr};
+  explicit AsyncBufs(cudaStream_t s) : st(s) {}
+  template <class T>
+  int get(int i, T** out, size_t bytes) {
+    if (cudaMallocAsync(&p[i], bytes, st) != cudaSuccess) {
+      cudaGetLastError();
+      p[i] = nullptr;
+      return fail(RHOSVD_ENOMEM, "conv3d: scratch allocation");
+    }
+    *out = (T*)p[i];
+    return RHOSVD_OK;
+  }
+  ~AsyncBufs() {
+    for (void* q : p)
+      if (q) cudaFreeAsync(q, st);
+  }
+};
+
 __global__ void outer_weights_kernel(const double* ca, int Ra, const double* cp, int Rp, double* w) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e < (int64_t)Ra * Rp) w[e] = ca[e / Rp] * cp[e % Rp];
@@ -294,10 +315,11 @@ extern "C" int rhosvd_conv3d(const double* const Fa[3], int64_t lda, const doubl
     const int64_t pb = std::max<int64_t>(1, std::min<int64_t>(Ra * Rp, ((int64_t)1 << 25) / N));
     const int64_t vb = std::max<int64_t>(Ra, Rp);
     double2 *tw = nullptr, *Su = nullptr, *Sp = nullptr, *Y = nullptr;
-    RH_CUDA(cudaMallocAsync((void**)&tw, (size_t)(N / 2 + 1) * sizeof(double2), st));
-    RH_CUDA(cudaMallocAsync((void**)&Su, (size_t)Ra * N * sizeof(double2), st));
-    RH_CUDA(cudaMallocAsync((void**)&Sp, (size_t)Rp * N * sizeof(double2), st));
-    RH_CUDA(cudaMallocAsync((void**)&Y, (size_t)std::max(pb, vb) * N * sizeof(double2), st));
+    AsyncBufs bufs(st);
+    RH_CHECK(bufs.get(0, &tw, (size_t)(N / 2 + 1) * sizeof(double2)));
+    RH_CHECK(bufs.get(1, &Su, (size_t)Ra * N * sizeof(double2)));
+    RH_CHECK(bufs.get(2, &Sp, (size_t)Rp * N * sizeof(double2)));
+    RH_CHECK(bufs.get(3, &Y, (size_t)std::max(pb, vb) * N * sizeof(double2)));
     twiddle_kernel<<<(unsigned)cdiv(N / 2, 256), 256, 0, st>>>(N, tw);
     count_launch();
     int status = RHOSVD_OK;
@@ -321,18 +343,15 @@ extern "C" int rhosvd_conv3d(const double* const Fa[3], int64_t lda, const doubl
       }
       if (cudaGetLastError() != cudaSuccess) status = fail(RHOSVD_ECUDA, "conv3d: four-step fft kernels");
     }
-    cudaFreeAsync(tw, st);
-    cudaFreeAsync(Su, st);
-    cudaFreeAsync(Sp, st);
-    cudaFreeAsync(Y, st);
     return status;
   }
   if (use_fft) {
     if ((int64_t)(Ra + Rp) > INT32_MAX / 2) return fail(RHOSVD_EINVAL, "conv3d: too many terms");
     double2 *tw = nullptr, *Su = nullptr, *Sp = nullptr;
-    RH_CUDA(cudaMallocAsync((void**)&tw, (size_t)(N / 2 + 1) * sizeof(double2), st));
-    RH_CUDA(cudaMallocAsync((void**)&Su, (size_t)Ra * N * sizeof(double2), st));
-    RH_CUDA(cudaMallocAsync((void**)&Sp, (size_t)Rp * N * sizeof(double2), st));
+    AsyncBufs bufs(st);
+    RH_CHECK(bufs.get(0, &tw, (size_t)(N / 2 + 1) * sizeof(double2)));
+    RH_CHECK(bufs.get(1, &Su, (size_t)Ra * N * sizeof(double2)));
+    RH_CHECK(bufs.get(2, &Sp, (size_t)Rp * N * sizeof(double2)));
     twiddle_kernel<<<(unsigned)cdiv(N / 2, 256), 256, 0, st>>>(N, tw);
     count_launch();
     const size_t smem = (size_t)N * sizeof(double2);
@@ -351,15 +370,13 @@ extern "C" int rhosvd_conv3d(const double* const Fa[3], int64_t lda, const doubl
       count_launch(3);
       if (cudaGetLastError() != cudaSuccess) status = fail(RHOSVD_ECUDA, "conv3d: fft kernels");
     }
-    cudaFreeAsync(tw, st);
-    cudaFreeAsync(Su, st);
-    cudaFreeAsync(Sp, st);
     return status;
   }
   // stacked Toeplitz chunk: qc kernel terms, qc n^2 doubles within ~1 GiB
   const int64_t qc = std::max<int64_t>(1, std::min<int64_t>(Rp, ((int64_t)1 << 27) / (n * n)));
   double* T = nullptr;
-  RH_CUDA(cudaMallocAsync((void**)&T, (size_t)round_up(qc * n, 2) * n * sizeof(double), st));
+  AsyncBufs tbuf(st);
+  RH_CHECK(tbuf.get(0, &T, (size_t)round_up(qc * n, 2) * n * sizeof(double)));
   Scratch scr;
   int status = RHOSVD_OK;
   for (int l = 0; l < 3 && status == RHOSVD_OK; ++l) {
@@ -384,6 +401,5 @@ extern "C" int rhosvd_conv3d(const double* const Fa[3], int64_t lda, const doubl
     }
   }
   scr.release(st);
-  cudaFreeAsync(T, st);
   return status;
 }
