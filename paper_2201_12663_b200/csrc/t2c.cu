@@ -204,6 +204,220 @@ __global__ void __launch_bounds__(T2C_THREADS) t2c_slice_kernel(T2CParams p) {
   }
 }
 
+// ---------------------------------------------------------------- QR-preconditioned slices
+// Drmac-Veselic preconditioning: the one-sided Jacobi above needs ~30 sweeps on Tucker-core
+// slices (sigma over ~20 decades: the parallel ordering converges slowly among the many
+// graded columns).  A Householder QR with column pivoting first, B P = Q R, then the
+// one-sided Jacobi on the ROWS of R (= columns of R^T, whose singular values are those of B)
+// converges in ~8 (CPU experiment on cfg 3 slices, same tolerance).  With the rotated rows
+// w_k: sigma_k = ||w_k||, v_k = P w_k / sigma_k (right singular vectors, in the original
+// column order) and u_k = B v_k / sigma_k from the original slice (renormalised).  Q is
+// never formed.  Same outputs and conventions as t2c_slice_kernel.
+__global__ void __launch_bounds__(T2C_THREADS) t2c_slice_qr_kernel(T2CParams p) {
+  extern __shared__ double sb[];  // B (col-major, pitch ldb) | norms | Householder vector | order | perm
+  const int r1 = p.r1, r2 = p.r2, ld = p.ldb;
+  const int m2 = r2 + (r2 & 1);
+  const int rr = min(r1, r2);
+  const int mr = rr + (rr & 1);   // even row count for the tournament (row rr: virtual zero)
+  double* B = sb;
+  double* sig = B + (size_t)ld * m2;       // m2
+  double* hv = sig + m2;                   // ld
+  int* ord = reinterpret_cast<int*>(hv + ld);  // m2
+  int* perm = ord + m2;                    // m2
+  __shared__ int srot, spiv;
+  __shared__ double salpha, svn2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = T2C_THREADS / 32;
+  for (int m = blockIdx.x; m < p.r3; m += gridDim.x) {
+    const double* Bm = p.Bt + (size_t)m * r1 * r2;
+    for (int e = tid; e < ld * m2; e += T2C_THREADS) {
+      const int a = e % ld, b = e / ld;
+      B[e] = (a < r1 && b < r2) ? Bm[(size_t)a * r2 + b] : 0.0;
+    }
+    for (int j = tid; j < m2; j += T2C_THREADS) perm[j] = j;
+    __shared__ double sfro;
+    __syncthreads();
+    if (warp == 0) {
+      double s = 0.0;
+      for (int e = lane; e < ld * m2; e += 32) s = fma(B[e], B[e], s);
+      s = warp_sum(s);
+      if (lane == 0) sfro = s;
+    }
+    // ---- Householder QR with column pivoting (largest remaining column norm, lowest index on ties)
+    for (int k = 0; k < rr; ++k) {
+      for (int j = k + warp; j < r2; j += nw) {
+        double s = 0.0;
+        for (int i = k + lane; i < r1; i += 32) s = fma(B[(size_t)j * ld + i], B[(size_t)j * ld + i], s);
+        s = warp_sum(s);
+        if (lane == 0) sig[j] = s;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        double best = -1.0;
+        int bi = 0x7fffffff;
+        for (int j = k + lane; j < r2; j += 32)
+          if (sig[j] > best) { best = sig[j]; bi = j; }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (lane == 0) spiv = bi;
+      }
+      __syncthreads();
+      const int pv = spiv;
+      if (pv != k) {
+        for (int i = tid; i < r1; i += T2C_THREADS) {
+          const double t = B[(size_t)k * ld + i];
+          B[(size_t)k * ld + i] = B[(size_t)pv * ld + i];
+          B[(size_t)pv * ld + i] = t;
+        }
+        if (tid == 0) {
+          const int t = perm[k];
+          perm[k] = perm[pv];
+          perm[pv] = t;
+        }
+      }
+      __syncthreads();
+      if (warp == 0) {  // reflector for column k, rows k..r1-1: H x = alpha e_1
+        double s = 0.0;
+        for (int i = k + lane; i < r1; i += 32) s = fma(B[(size_t)k * ld + i], B[(size_t)k * ld + i], s);
+        s = warp_sum(s);
+        const double x0 = B[(size_t)k * ld + k];
+        const double nrm = sqrt(s);
+        const double alpha = (x0 >= 0.0) ? -nrm : nrm;
+        for (int i = k + lane; i < r1; i += 32) hv[i] = (i == k) ? x0 - alpha : B[(size_t)k * ld + i];
+        if (lane == 0) {
+          salpha = alpha;
+          svn2 = s - x0 * x0 + (x0 - alpha) * (x0 - alpha);
+        }
+      }
+      __syncthreads();
+      const double vn2 = svn2;
+      if (vn2 > 0.0) {
+        for (int j = k + 1 + warp; j < r2; j += nw) {
+          double w = 0.0;
+          for (int i = k + lane; i < r1; i += 32) w = fma(hv[i], B[(size_t)j * ld + i], w);
+          w = warp_sum(w);
+          const double f = 2.0 * w / vn2;
+          for (int i = k + lane; i < r1; i += 32) B[(size_t)j * ld + i] = fma(-f, hv[i], B[(size_t)j * ld + i]);
+        }
+        for (int i = k + tid; i < r1; i += T2C_THREADS) B[(size_t)k * ld + i] = (i == k) ? salpha : 0.0;
+      }
+      __syncthreads();
+    }
+    // ---- one-sided Jacobi on the rows of R (row r: B[c ld + r], c < r2)
+    const double tiny2 = 256.0 * 1.2325951644078309e-32 * sfro;
+    int sw = 0;
+    bool conv = false;
+    for (; sw < T2C_MAX_SWEEPS && !conv; ++sw) {
+      for (int r = warp; r < rr; r += nw) {
+        double s = 0.0;
+        for (int c = lane; c < r2; c += 32) s = fma(B[(size_t)c * ld + r], B[(size_t)c * ld + r], s);
+        s = warp_sum(s);
+        if (lane == 0) sig[r] = s;
+      }
+      if (tid == 0) srot = 0;
+      __syncthreads();
+      for (int k = tid; k < rr; k += T2C_THREADS) {  // de Rijk: decreasing-norm visiting order
+        const double v = sig[k];
+        int q = 0;
+        for (int j = 0; j < rr; ++j) q += (sig[j] > v) || (sig[j] == v && j < k);
+        ord[q] = k;
+      }
+      if (tid == 0 && mr > rr) ord[rr] = rr;  // the virtual zero row
+      __syncthreads();
+      for (int st = 0; st < mr - 1; ++st) {
+        for (int k = warp; k < mr / 2; k += nw) {
+          const int pr = ord[t2c_rr(k, st, mr)], qr = ord[t2c_rr(mr - 1 - k, st, mr)];
+          if (pr >= rr || qr >= rr) continue;
+          double al = 0.0, be = 0.0, ga = 0.0;
+          for (int c = lane; c < r2; c += 32) {
+            const double x = B[(size_t)c * ld + pr], y = B[(size_t)c * ld + qr];
+            al = fma(x, x, al);
+            be = fma(y, y, be);
+            ga = fma(x, y, ga);
+          }
+          al = warp_sum(al);
+          be = warp_sum(be);
+          ga = warp_sum(ga);
+          if (al > tiny2 && be > tiny2 && fabs(ga) > p.tol * sqrt(al * be)) {
+            const double zeta = (be - al) / (2.0 * ga);
+            const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+            const double c = rsqrt(1.0 + t * t), s = c * t;
+            for (int cc = lane; cc < r2; cc += 32) {
+              const double x = B[(size_t)cc * ld + pr], y = B[(size_t)cc * ld + qr];
+              B[(size_t)cc * ld + pr] = c * x - s * y;
+              B[(size_t)cc * ld + qr] = s * x + c * y;
+            }
+            if (lane == 0) atomicAdd(&srot, 1);
+          }
+        }
+        __syncthreads();
+      }
+      conv = (srot == 0);
+      __syncthreads();
+    }
+    // sigma_r = ||row r||, descending order (ties: lower row first)
+    for (int r = warp; r < rr; r += nw) {
+      double s = 0.0;
+      for (int c = lane; c < r2; c += 32) s = fma(B[(size_t)c * ld + r], B[(size_t)c * ld + r], s);
+      s = warp_sum(s);
+      if (lane == 0) sig[r] = sqrt(s);
+    }
+    __syncthreads();
+    for (int k = tid; k < rr; k += T2C_THREADS) {
+      const double v = sig[k];
+      int q = 0;
+      for (int j = 0; j < rr; ++j) q += (sig[j] > v) || (sig[j] == v && j < k);
+      ord[q] = k;
+    }
+    __syncthreads();
+    double* Us = p.Us + (size_t)m * r2 * r1;
+    double* Vs = p.Vs + (size_t)m * r2 * r2;
+    double* sg = p.sg + (size_t)m * r2;
+    int keep = 0;
+    for (int j = 0; j < rr; ++j) keep += sig[ord[j]] > p.thr;
+    // kept triplets, one warp each: v = P w / sigma; u = B v / sigma from the original slice
+    // (rows of Bt, gathered through P), renormalised; sign rule on u (largest |.| positive)
+    for (int j = warp; j < keep; j += nw) {
+      const int r = ord[j];
+      const double s = sig[r], inv = 1.0 / s;
+      double* uo = Us + (size_t)j * r1;
+      double un = 0.0;
+      double best = -1.0;
+      double bval = 0.0;
+      for (int a = 0; a < r1; ++a) {
+        const double* brow = Bm + (size_t)a * r2;
+        double acc = 0.0;
+        for (int c = lane; c < r2; c += 32) acc = fma(brow[perm[c]], B[(size_t)c * ld + r], acc);
+        acc = warp_sum(acc) * inv * inv;  // (B P w)_a / sigma^2 = (B v)_a / sigma
+        if (lane == 0) uo[a] = acc;
+        un = fma(acc, acc, un);
+        const double aa = fabs(acc);
+        if (aa > best) { best = aa; bval = acc; }  // first maximum: lowest index on ties
+      }
+      const double sgn = ((bval < 0.0) ? -1.0 : 1.0) * (un > 0.0 ? 1.0 / sqrt(un) : 0.0);
+      __syncwarp();
+      __threadfence_block();
+      for (int a = lane; a < r1; a += 32) uo[a] *= sgn;
+      const double vs = (bval < 0.0 ? -inv : inv);
+      double* vo = Vs + (size_t)j * r2;
+      for (int c = lane; c < r2; c += 32) vo[perm[c]] = vs * B[(size_t)c * ld + r];
+      if (lane == 0) sg[j] = s;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      p.cnt[m] = keep;
+      p.sweeps[m] = conv ? sw : -1;
+      double d = 0.0;
+      for (int j = rr - 1; j >= keep; --j) d = fma(sig[ord[j]], sig[ord[j]], d);
+      p.drop[m] = d;
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- large slices
 // Slices too large for shared memory: block one-sided Jacobi with the slice in global
 // memory (column-major per slice, L2-resident working set).  One-sided rotations only
@@ -550,11 +764,26 @@ int rhosvd_t2c(const rhosvd_result* res, double eps_rel, rhosvd_stream stream, r
   }
   cudaError_t e = cudaSuccess;
   if (small) {
-    T2CParams tp{Bt, r1, r2, r3, ldb, cp->thr, tol, Us, Vs, sg, cnt, sweeps, drop};
+    // QR-preconditioned kernel when its extra shared memory fits (RHOSVD_T2C_QR=0: plain);
+    // its row Jacobi works on rows of length r2, so the tolerance uses max(r1, r2)
+    static const bool qr_on = [] {
+      const char* e2 = getenv("RHOSVD_T2C_QR");
+      return !(e2 && e2[0] == '0');
+    }();
+    const size_t smem_qr = smem + (size_t)ldb * sizeof(double) + (size_t)m2 * sizeof(int);
+    const bool use_qr = qr_on && smem_qr <= 220 * 1024;
+    const double tol_qr = tol_mult * std::sqrt((double)std::max(std::max(r1, r2), 1)) * 1.1102230246251565e-16;
+    T2CParams tp{Bt, r1, r2, r3, ldb, cp->thr, use_qr ? tol_qr : tol, Us, Vs, sg, cnt, sweeps, drop};
     static const cudaError_t attr =
         cudaFuncSetAttribute(t2c_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    static const cudaError_t attr_q =
+        cudaFuncSetAttribute(t2c_slice_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     (void)attr;
-    t2c_slice_kernel<<<std::min(r3, 4 * num_sms()), T2C_THREADS, smem, st>>>(tp);
+    (void)attr_q;
+    if (use_qr)
+      t2c_slice_qr_kernel<<<std::min(r3, 4 * num_sms()), T2C_THREADS, smem_qr, st>>>(tp);
+    else
+      t2c_slice_kernel<<<std::min(r3, 4 * num_sms()), T2C_THREADS, smem, st>>>(tp);
     e = cudaGetLastError();
   } else {
     // column-major slice copies: the original (for v = B^T u / sigma) and the working copy

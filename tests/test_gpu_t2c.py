@@ -123,3 +123,17 @@ def test_t2c_cfg2(rh):
     p = make_params(2)
     Us, xi = dev_inputs(p)
     check_case(rh, Us, xi, p.eps, p.ranks, 1e-6)
+
+
+def test_t2c_plain_kernel_subprocess():
+    """The shared-memory path defaults to the QR-preconditioned kernel; RHOSVD_T2C_QR=0
+    selects the plain one-sided Jacobi kernel (read once per process), so the random and
+    baseline cases run once more with it in a subprocess."""
+    import os
+    import subprocess
+    import sys
+    here = os.path.dirname(os.path.abspath(__file__))
+    env = dict(os.environ, RHOSVD_T2C_QR="0")
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.join(here, "test_gpu_t2c.py"),
+                        "-k", "random or baseline_configs"], env=env, capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-2000:])
