@@ -213,7 +213,8 @@ __global__ void __launch_bounds__(T2C_THREADS) t2c_slice_kernel(T2CParams p) {
 // w_k: sigma_k = ||w_k||, v_k = P w_k / sigma_k (right singular vectors, in the original
 // column order) and u_k = B v_k / sigma_k from the original slice (renormalised).  Q is
 // never formed.  Same outputs and conventions as t2c_slice_kernel.
-__global__ void __launch_bounds__(T2C_THREADS) t2c_slice_qr_kernel(T2CParams p) {
+template <int NT>
+__global__ void __launch_bounds__(NT) t2c_slice_qr_kernel(T2CParams p) {
   extern __shared__ double sb[];  // B (col-major, pitch ldb) | norms | Householder vector | order | perm
   const int r1 = p.r1, r2 = p.r2, ld = p.ldb;
   const int m2 = r2 + (r2 & 1);
@@ -226,14 +227,14 @@ __global__ void __launch_bounds__(T2C_THREADS) t2c_slice_qr_kernel(T2CParams p) 
   int* perm = ord + m2;                    // m2
   __shared__ int srot, spiv;
   __shared__ double salpha, svn2;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = T2C_THREADS / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
   for (int m = blockIdx.x; m < p.r3; m += gridDim.x) {
     const double* Bm = p.Bt + (size_t)m * r1 * r2;
-    for (int e = tid; e < ld * m2; e += T2C_THREADS) {
+    for (int e = tid; e < ld * m2; e += NT) {
       const int a = e % ld, b = e / ld;
       B[e] = (a < r1 && b < r2) ? Bm[(size_t)a * r2 + b] : 0.0;
     }
-    for (int j = tid; j < m2; j += T2C_THREADS) perm[j] = j;
+    for (int j = tid; j < m2; j += NT) perm[j] = j;
     __shared__ double sfro;
     __syncthreads();
     if (warp == 0) {
@@ -267,7 +268,7 @@ __global__ void __launch_bounds__(T2C_THREADS) t2c_slice_qr_kernel(T2CParams p) 
       __syncthreads();
       const int pv = spiv;
       if (pv != k) {
-        for (int i = tid; i < r1; i += T2C_THREADS) {
+        for (int i = tid; i < r1; i += NT) {
           const double t = B[(size_t)k * ld + i];
           B[(size_t)k * ld + i] = B[(size_t)pv * ld + i];
           B[(size_t)pv * ld + i] = t;
@@ -302,7 +303,7 @@ __global__ void __launch_bounds__(T2C_THREADS) t2c_slice_qr_kernel(T2CParams p) 
           const double f = 2.0 * w / vn2;
           for (int i = k + lane; i < r1; i += 32) B[(size_t)j * ld + i] = fma(-f, hv[i], B[(size_t)j * ld + i]);
         }
-        for (int i = k + tid; i < r1; i += T2C_THREADS) B[(size_t)k * ld + i] = (i == k) ? salpha : 0.0;
+        for (int i = k + tid; i < r1; i += NT) B[(size_t)k * ld + i] = (i == k) ? salpha : 0.0;
       }
       __syncthreads();
     }
@@ -319,7 +320,7 @@ __global__ void __launch_bounds__(T2C_THREADS) t2c_slice_qr_kernel(T2CParams p) 
       }
       if (tid == 0) srot = 0;
       __syncthreads();
-      for (int k = tid; k < rr; k += T2C_THREADS) {  // de Rijk: decreasing-norm visiting order
+      for (int k = tid; k < rr; k += NT) {  // de Rijk: decreasing-norm visiting order
         const double v = sig[k];
         int q = 0;
         for (int j = 0; j < rr; ++j) q += (sig[j] > v) || (sig[j] == v && j < k);
@@ -366,7 +367,7 @@ __global__ void __launch_bounds__(T2C_THREADS) t2c_slice_qr_kernel(T2CParams p) 
       if (lane == 0) sig[r] = sqrt(s);
     }
     __syncthreads();
-    for (int k = tid; k < rr; k += T2C_THREADS) {
+    for (int k = tid; k < rr; k += NT) {
       const double v = sig[k];
       int q = 0;
       for (int j = 0; j < rr; ++j) q += (sig[j] > v) || (sig[j] == v && j < k);
@@ -776,12 +777,30 @@ int rhosvd_t2c(const rhosvd_result* res, double eps_rel, rhosvd_stream stream, r
     T2CParams tp{Bt, r1, r2, r3, ldb, cp->thr, use_qr ? tol_qr : tol, Us, Vs, sg, cnt, sweeps, drop};
     static const cudaError_t attr =
         cudaFuncSetAttribute(t2c_slice_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    static const cudaError_t attr_q =
-        cudaFuncSetAttribute(t2c_slice_qr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    // QR kernel block size (RHOSVD_T2C_QR_THREADS): more warps = fewer column pairs per warp
+    // per Jacobi step (the per-pair dot-product latency is the cost)
+    static const int qr_nt = [] {
+      const char* e2 = getenv("RHOSVD_T2C_QR_THREADS");
+      const int v = e2 ? atoi(e2) : 1024;  // cfg 3: 256 17.6 ms, 512 12.6, 1024 11.2
+      return (v == 256 || v == 512) ? v : 1024;
+    }();
+    static const cudaError_t attr_q1 =
+        cudaFuncSetAttribute(t2c_slice_qr_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    static const cudaError_t attr_q2 =
+        cudaFuncSetAttribute(t2c_slice_qr_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    static const cudaError_t attr_q4 =
+        cudaFuncSetAttribute(t2c_slice_qr_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     (void)attr;
-    (void)attr_q;
-    if (use_qr)
-      t2c_slice_qr_kernel<<<std::min(r3, 4 * num_sms()), T2C_THREADS, smem_qr, st>>>(tp);
+    (void)attr_q1;
+    (void)attr_q2;
+    (void)attr_q4;
+    const int qgrid = std::min(r3, 4 * num_sms());
+    if (use_qr && qr_nt == 256)
+      t2c_slice_qr_kernel<256><<<qgrid, 256, smem_qr, st>>>(tp);
+    else if (use_qr && qr_nt == 1024)
+      t2c_slice_qr_kernel<1024><<<qgrid, 1024, smem_qr, st>>>(tp);
+    else if (use_qr)
+      t2c_slice_qr_kernel<512><<<qgrid, 512, smem_qr, st>>>(tp);
     else
       t2c_slice_kernel<<<std::min(r3, 4 * num_sms()), T2C_THREADS, smem, st>>>(tp);
     e = cudaGetLastError();
