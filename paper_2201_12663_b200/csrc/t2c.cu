@@ -438,7 +438,8 @@ struct T2CBlockParams {
   double* drop;
 };
 
-__global__ void __launch_bounds__(T2C_THREADS) t2c_slice_block_kernel(T2CBlockParams p) {
+template <int NT>
+__global__ void __launch_bounds__(NT) t2c_slice_block_kernel(T2CBlockParams p) {
   extern __shared__ double sbk[];
   const int r1 = p.r1, r2 = p.r2, ld = p.ldp, CB = p.CB, nb = p.nb;
   double* P = sbk;                              // 2 CB columns, pitch ld
@@ -446,11 +447,11 @@ __global__ void __launch_bounds__(T2C_THREADS) t2c_slice_block_kernel(T2CBlockPa
   int* ord = reinterpret_cast<int*>(sig + r2);  // r2
   __shared__ int srot;
   __shared__ double sfro;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = T2C_THREADS / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
   for (int m = blockIdx.x; m < p.r3; m += gridDim.x) {
     const double* Bo = p.Bo + (size_t)m * r2 * r1;
     double* Bw = p.Bw + (size_t)m * r2 * r1;
-    for (int e = tid; e < r1 * r2; e += T2C_THREADS) Bw[e] = Bo[e];
+    for (int e = tid; e < r1 * r2; e += NT) Bw[e] = Bo[e];
     if (warp == 0) {  // ||B||_F^2 (fixed order)
       double s = 0.0;
       for (int e = lane; e < r1 * r2; e += 32) s = fma(Bo[e], Bo[e], s);
@@ -471,7 +472,7 @@ __global__ void __launch_bounds__(T2C_THREADS) t2c_slice_block_kernel(T2CBlockPa
       }
       if (tid == 0) srot = 0;
       __syncthreads();
-      for (int k = tid; k < r2; k += T2C_THREADS) {
+      for (int k = tid; k < r2; k += NT) {
         const double v = sig[k];
         int r = 0;
         for (int j = 0; j < r2; ++j) r += (sig[j] > v) || (sig[j] == v && j < k);
@@ -483,7 +484,7 @@ __global__ void __launch_bounds__(T2C_THREADS) t2c_slice_block_kernel(T2CBlockPa
           const int b1 = t2c_rr(k, rd, nb), b2 = t2c_rr(nb - 1 - k, rd, nb);
           const int I = min(b1, b2), J = max(b1, b2);
           // local column l < CB -> global I CB + l, else J CB + (l - CB); beyond r2 -> zero
-          for (int e = tid; e < 2 * CB * ld; e += T2C_THREADS) {
+          for (int e = tid; e < 2 * CB * ld; e += NT) {
             const int l = e / ld, a = e % ld;
             const int pos = l < CB ? I * CB + l : J * CB + (l - CB);
             P[e] = (a < r1 && pos < r2) ? Bw[(size_t)ord[pos] * r1 + a] : 0.0;
@@ -519,7 +520,7 @@ __global__ void __launch_bounds__(T2C_THREADS) t2c_slice_block_kernel(T2CBlockPa
             }
             __syncthreads();
           }
-          for (int e = tid; e < 2 * CB * ld; e += T2C_THREADS) {
+          for (int e = tid; e < 2 * CB * ld; e += NT) {
             const int l = e / ld, a = e % ld;
             const int pos = l < CB ? I * CB + l : J * CB + (l - CB);
             if (a < r1 && pos < r2) Bw[(size_t)ord[pos] * r1 + a] = P[e];
@@ -538,7 +539,7 @@ __global__ void __launch_bounds__(T2C_THREADS) t2c_slice_block_kernel(T2CBlockPa
       if (lane == 0) sig[k] = sqrt(s);
     }
     __syncthreads();
-    for (int k = tid; k < r2; k += T2C_THREADS) {
+    for (int k = tid; k < r2; k += NT) {
       const double v = sig[k];
       int r = 0;
       for (int j = 0; j < r2; ++j) r += (sig[j] > v) || (sig[j] == v && j < k);
@@ -582,7 +583,7 @@ __global__ void __launch_bounds__(T2C_THREADS) t2c_slice_block_kernel(T2CBlockPa
     const int JT = min(8, 2 * CB * ld / max(r1, 1));
     for (int j0 = 0; j0 < keep; j0 += JT) {
       const int jn = min(JT, keep - j0);
-      for (int e = tid; e < jn * r1; e += T2C_THREADS) P[e] = Us[(size_t)j0 * r1 + e];
+      for (int e = tid; e < jn * r1; e += NT) P[e] = Us[(size_t)j0 * r1 + e];
       __syncthreads();
       for (int b = warp; b < r2; b += nw) {
         const double* ob = Bo + (size_t)b * r1;
@@ -813,10 +814,28 @@ int rhosvd_t2c(const rhosvd_result* res, double eps_rel, rhosvd_stream stream, r
       t2c_transpose_cm_kernel<<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(res->beta, r1, r2, r3, Bt);
       const int nbk = (int)cdiv(r2, CB);
       T2CBlockParams bp{Bt, Bw, r1, r2, r3, ldb, CB, nbk + (nbk & 1), cp->thr, tol, Us, Vs, sg, cnt, sweeps, drop};
-      static const cudaError_t attr2 =
-          cudaFuncSetAttribute(t2c_slice_block_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-      (void)attr2;
-      t2c_slice_block_kernel<<<std::min(r3, num_sms()), T2C_THREADS, smem_blk, st>>>(bp);
+      // block size (RHOSVD_T2C_BLK_THREADS, default 1024): one warp per column pair of a step
+      static const int blk_nt = [] {
+        const char* e2 = getenv("RHOSVD_T2C_BLK_THREADS");
+        const int v = e2 ? atoi(e2) : 1024;
+        return (v == 256 || v == 512) ? v : 1024;
+      }();
+      static const cudaError_t attr2a =
+          cudaFuncSetAttribute(t2c_slice_block_kernel<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      static const cudaError_t attr2b =
+          cudaFuncSetAttribute(t2c_slice_block_kernel<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      static const cudaError_t attr2c =
+          cudaFuncSetAttribute(t2c_slice_block_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      (void)attr2a;
+      (void)attr2b;
+      (void)attr2c;
+      const int bgrid = std::min(r3, num_sms());
+      if (blk_nt == 256)
+        t2c_slice_block_kernel<256><<<bgrid, 256, smem_blk, st>>>(bp);
+      else if (blk_nt == 512)
+        t2c_slice_block_kernel<512><<<bgrid, 512, smem_blk, st>>>(bp);
+      else
+        t2c_slice_block_kernel<1024><<<bgrid, 1024, smem_blk, st>>>(bp);
       e = cudaGetLastError();
       if (e == cudaSuccess) e = cudaStreamSynchronize(st);
       cudaFree(Bw);
