@@ -315,6 +315,10 @@ int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3,
     const char* e = getenv("RHOSVD_CORE_EDGE");
     return !(e && e[0] == '0');
   }();
+  static const bool wide_edge = [] {  // RHOSVD_CORE_WIDE_EDGE=0: keep the 16-wide edge
+    const char* e = getenv("RHOSVD_CORE_WIDE_EDGE");
+    return !(e && e[0] == '0');
+  }();
   const int BN = force_bn ? force_bn : pick_bn(r3);
   CoreArgs a{};
   a.r1 = (int)r1; a.r2 = (int)r2; a.r3 = (int)r3; a.R = (int)R;
@@ -336,7 +340,13 @@ int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3,
   int nseg = 0;
   {
     const int64_t full = (r3 / BN) * BN, rem = r3 - full;
-    if (splits == 1 && ksub == 2 && edge_on && rem > 0 && full > 0 && round_up(rem, 16) < BN) {
+    if (splits == 1 && ksub == 2 && edge_on && rem > 0 && full > BN && BN == 128 && rem <= 16 && wide_edge) {
+      // a thin leftover (<= 16 columns) joins the last full tile as one wide 144-column
+      // edge tile (18 n-fragments, 239 registers): the 16-wide edge runs at ~60 % of the
+      // main rate (2 n-fragments per A fragment), the wide one at the main rate
+      segs[nseg++] = {BN, 0, (int)(full - BN)};
+      segs[nseg++] = {144, (int)(full - BN), (int)r3};
+    } else if (splits == 1 && ksub == 2 && edge_on && rem > 0 && full > 0 && round_up(rem, 16) < BN) {
       segs[nseg++] = {BN, 0, (int)full};
       segs[nseg++] = {(int)round_up(rem, 16), (int)full, (int)r3};
     } else {
@@ -382,6 +392,7 @@ int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3,
     const size_t sm = smem[q];
     if (ksub == 2) {
       switch (bn) {
+        case 144: return launch_core<144, 2>(t1, t2, t, aa, sm, grid, s);
         case 128: return launch_core<128, 2>(t1, t2, t, aa, sm, grid, s);
         case 112: return launch_core<112, 2>(t1, t2, t, aa, sm, grid, s);
         case 96: return launch_core<96, 2>(t1, t2, t, aa, sm, grid, s);

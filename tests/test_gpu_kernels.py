@@ -91,10 +91,12 @@ def test_syevj_graded_high_relative_accuracy(rh, b):
     assert np.max(np.abs(lam - ref) / ref) < 1e-11
 
 
+# (6, 7, 270) and (3, 40, 652): BN 128 with a <= 16-column leftover -> the 144-wide edge tile
 @pytest.mark.parametrize("r,R", [((1, 1, 1), 1), ((3, 5, 7), 50), ((10, 10, 10), 200), ((70, 129, 33), 1500),
                                  ((20, 20, 20), 40001), ((5, 130, 97), 3000), ((4, 3, 130), 777),
                                  ((2, 1, 65), 100), ((40, 200, 300), 2000), ((130, 131, 97), 513),
-                                 ((30, 30, 60), 10), ((9, 256, 200), 4099)])
+                                 ((30, 30, 60), 10), ((9, 256, 200), 4099),
+                                 ((6, 7, 270), 300), ((3, 40, 652), 1000)])
 def test_core(rh, r, R):
     from oracle import core_kr
     rng = np.random.default_rng(sum(r) + R)
