@@ -280,7 +280,8 @@ def run_ours(args):
         pass
     roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak_tf, "unit": "TFLOP/s",
             "frac": (achieved / peak_tf) if (achieved and peak_tf) else None, "traffic": traffic,
-            "traffic_unit": "bytes per launch (ncu dram__bytes_read.sum + dram__bytes_write.sum)",
+            "traffic_unit": "bytes per call of the dominant kernel (ncu dram__bytes_read.sum + dram__bytes_write.sum, "
+                            "summed over its launches in one call, like achieved)",
             "traffic_source": traffic_src,
             "peak_source": "measured DMMA m8n8k4.f64 microbenchmark (tools/fp64_peak.cu) on this GPU; "
                            "MEASURED_PEAKS.json has no FP64 entry",
