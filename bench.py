@@ -250,7 +250,8 @@ def run_ours(args):
         lib.rhosvd_result_free(h)
     e1.record(stream)
     torch.cuda.synchronize(dev)
-    per_step = sorted(step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(args.steps))
+    step_seq = [step_ev[i].elapsed_time(step_ev[i + 1]) for i in range(args.steps)]
+    per_step = sorted(step_seq)
     clk = clocks.stop()
     ms_max = max_over_ranks(e0.elapsed_time(e1), dev)
     value = p.R * args.steps / (ms_max * 1e-3)
@@ -351,7 +352,8 @@ def run_ours(args):
                        "l2": "inputs (3 n R fp64 = %.2f GB) larger than L2; no flush" % (3 * p.n * p.R * 8 / 1e9)},
             "roofline": roof, "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": launches,
             "step_ms": {"median": per_step[len(per_step) // 2], "min": per_step[0], "max": per_step[-1],
-                        "cold_first_call": cold_ms, "note": "this rank's per-step CUDA-event times"},
+                        "cold_first_call": cold_ms, "in_order": [round(x, 2) for x in step_seq],
+                        "note": "this rank's per-step CUDA-event times"},
             "clocks": clk,
             "result": {"ranks": rep["ranks"], "block": rep["block"], "iters": rep["iters"],
                        "tail": rep["tail"], "beta_norm": rep["beta_norm"], "phase_ms": rep["ms"],
