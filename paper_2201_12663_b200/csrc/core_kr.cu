@@ -122,6 +122,10 @@ __global__ void __launch_bounds__(CORE_THREADS, 1)
   for (int q = 0; q < CORE_BK / 4; ++q) koff[q] = sw128_off(fr, 4 * q + fc) - fr * 128;
   const uint32_t ring_s = smem_u32(ring);
   uint32_t g = 0;  // k-tiles consumed by this CTA
+  // ring position of k-tile g (stage g % stages, parity (g / stages) & 1), advanced
+  // incrementally: no integer division on the per-stage path
+  uint32_t cs = 0, cph = 0;
+  const uint32_t nst = (uint32_t)p.stages;
   for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
     const int split = it / p.tiles, tile = it % p.tiles;
     const int tm = p.tm0 + tile % p.mt, tn = tile / p.mt;
@@ -146,12 +150,12 @@ __global__ void __launch_bounds__(CORE_THREADS, 1)
     for (int k0 = kbeg; k0 < kend; k0 += CORE_BK * KSUB, ++g) {
       // refill the stage released one step ago (its 8 warps are done with it)
       if (producer && g >= 1) {
-        const uint32_t gp = g - 1, sp = gp % p.stages;
-        mbar_wait(&empty[sp], (gp / p.stages) & 1);
+        const uint32_t sp = cs == 0 ? nst - 1 : cs - 1, php = cs == 0 ? cph ^ 1u : cph;
+        mbar_wait(&empty[sp], php);
         issue_next((int)sp);
       }
-      const uint32_t s = g % p.stages;
-      mbar_wait(&full[s], (g / p.stages) & 1);
+      const uint32_t s = cs;
+      mbar_wait(&full[s], cph);
 #pragma unroll
       for (int js = 0; js < KSUB; ++js) {
       const uint32_t w1 = ring_s + s * p.stage_bytes + js * slab;
@@ -172,6 +176,10 @@ __global__ void __launch_bounds__(CORE_THREADS, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (++cs == nst) {
+        cs = 0;
+        cph ^= 1u;
+      }
     }
     // epilogue: rows m (flattened a r2 + b), columns n of beta_(12)(3)
     double* out = p.out + (p.splits > 1 ? (int64_t)split * M * p.r3 : 0);

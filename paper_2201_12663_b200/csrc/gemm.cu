@@ -126,6 +126,10 @@ __global__ void __launch_bounds__(GTHREADS, 1)
   constexpr uint32_t ASTEP = AK ? 1024u : 64u, BSTEP = BKM ? 1024u : 64u;  // next 8 rows
   const uint32_t ring_s = smem_u32(ring);
   uint32_t g = 0;
+  // ring position of k-tile g (stage g % stages, parity (g / stages) & 1), advanced
+  // incrementally: no integer division on the per-stage path
+  uint32_t cs = 0, cph = 0;
+  const uint32_t nst = (uint32_t)p.stages;
   for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
     const int split = it / p.tiles;
     int tm, tn;
@@ -139,12 +143,12 @@ __global__ void __launch_bounds__(GTHREADS, 1)
       for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     for (int k0 = kbeg; k0 < kend; k0 += GBK * KS, ++g) {
       if (producer && g >= 1) {
-        const uint32_t gp = g - 1, sp = gp % p.stages;
-        mbar_wait(&empty[sp], (gp / p.stages) & 1);
+        const uint32_t sp = cs == 0 ? nst - 1 : cs - 1, php = cs == 0 ? cph ^ 1u : cph;
+        mbar_wait(&empty[sp], php);
         issue_next((int)sp);
       }
-      const uint32_t s = g % p.stages;
-      mbar_wait(&full[s], (g / p.stages) & 1);
+      const uint32_t s = cs;
+      mbar_wait(&full[s], cph);
 #pragma unroll
       for (int js = 0; js < KS; ++js) {
       const uint32_t sa = ring_s + s * p.stage_bytes + js * p.a_bytes;
@@ -164,6 +168,10 @@ __global__ void __launch_bounds__(GTHREADS, 1)
       }
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[s]);
+      if (++cs == nst) {
+        cs = 0;
+        cph ^= 1u;
+      }
     }
 
     // ---- epilogue
