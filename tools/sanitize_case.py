@@ -25,5 +25,15 @@ M = torch.as_tensor(rng.normal(size=(300, 97)), device=dev)
 rhosvd.chol_inv(M.t() @ M)
 W = [torch.as_tensor(rng.normal(size=(r, 500)), device=dev) for r in (5, 130, 97)]
 rhosvd.core(W[0], W[1], W[2], torch.as_tensor(rng.normal(size=500), device=dev))
+# 144-wide edge tile (r3 = 652 -> 4 x 128 + 144), ring wrapping (R / 32 > stages)
+W = [torch.as_tensor(rng.normal(size=(r, 700)), device=dev) for r in (3, 40, 652)]
+rhosvd.core(W[0], W[1], W[2], torch.as_tensor(rng.normal(size=700), device=dev))
+# host-buffer entry point, ALS sweep, convolution
+h = rhosvd.c2t_host([u.cpu().pin_memory() for u in (U1, U2, U3)], xi.cpu().pin_memory(), eps=p.eps)
+h.close()
+rhosvd.c2t([U1, U2, U3], xi, eps=p.eps, als_sweeps=1)
+F = [torch.as_tensor(rng.normal(size=(4, 100)), device=dev) for _ in range(3)]
+P = [torch.as_tensor(rng.normal(size=(2, 100)), device=dev) for _ in range(3)]
+rhosvd.conv3d(F, torch.ones(4, dtype=torch.float64, device=dev), P, torch.ones(2, dtype=torch.float64, device=dev), 0.5)
 torch.cuda.synchronize()
 print("ok", g.ranks, cp.R)
