@@ -36,6 +36,7 @@ struct GParams {
   double* part;   // split-K partials [split][N][M] (col-major, ld M) or residual per-item sums
   int splits, kchunk;
   int tiles_m, tiles_n, tiles, items;
+  int n_off;      // first output column of this launch (column segments)
   int stages;
   uint32_t a_bytes, stage_bytes, tx_bytes;
   uint32_t b_bytes;  // one k-slab of B (the stage holds KS slabs of A, then KS of B)
@@ -72,7 +73,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
     int tm, tn;
     tile_of(pit % p.tiles, tm, tn);
     pm = tm * BM;
-    pn = tn * BN;
+    pn = p.n_off + tn * BN;
     pk = split * p.kchunk;
     pkend = min(p.K, pk + p.kchunk);
   };
@@ -134,7 +135,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
     const int split = it / p.tiles;
     int tm, tn;
     tile_of(it % p.tiles, tm, tn);
-    const int m0 = tm * BM, n0 = tn * BN;
+    const int m0 = tm * BM, n0 = p.n_off + tn * BN;
     const int kbeg = split * p.kchunk, kend = min(p.K, kbeg + p.kchunk);
     double acc[FM][FN][2];
 #pragma unroll
@@ -328,6 +329,15 @@ template <int BM, int BN>
 static int launch_layout(const GemmArgs& g, const GParams& gp, cudaStream_t st) {
   return gemm_ks() == 2 ? launch_layout_ks<BM, BN, 2>(g, gp, st) : launch_layout_ks<BM, BN, 1>(g, gp, st);
 }
+// the narrow last column segment of a 128 x 128 GEMM (KS 2 only)
+static int launch_edge(int bn, const GemmArgs& g, const GParams& gp, cudaStream_t st) {
+  switch (bn) {
+    case 32: return launch_layout_ks<128, 32, 2>(g, gp, st);
+    case 64: return launch_layout_ks<128, 64, 2>(g, gp, st);
+    case 96: return launch_layout_ks<128, 96, 2>(g, gp, st);
+    default: return fail(RHOSVD_EINVAL, "gemm: unsupported edge width");
+  }
+}
 
 int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
   if (g.M <= 0 || g.N <= 0) return RHOSVD_OK;
@@ -397,10 +407,44 @@ int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
     }
     return RHOSVD_OK;
   }
-  if (big)
+  // column edge: N % 128 leftover columns as one narrower segment (BN 32 / 64 / 96) so
+  // the last column tile does not run padded DMMAs (b = 730: 768 -> 736 columns; b = 147:
+  // 256 -> 160).  Not for the symmetric (upper-tile) or residual-epilogue forms.
+  static const bool edge_on = [] {
+    const char* e = getenv("RHOSVD_GEMM_EDGE");
+    return !(e && e[0] == '0');
+  }();
+  const int64_t rem = g.N % 128;
+  const int ebn = (int)round_up(rem, 32);
+  bool use_edge = big && edge_on && !g.upper_sym && g.epi != EPI_RESID && gemm_ks() == 2 && g.N > 128 && rem > 0 &&
+                  ebn < 128;
+  if (use_edge) {
+    // waves of 128-tile time: the two launches each end on their own partial wave, so the
+    // edge only pays when it removes more padding than it adds tail (an edge tile costs
+    // ~(ebn + 16) / 128 of a full one)
+    const int64_t i1 = (int64_t)tm * (g.N / 128) * splits, i2 = (int64_t)tm * splits, ia = (int64_t)gp.tiles * splits;
+    const double c_edge = (double)cdiv(i1, sms) + (double)cdiv(i2, sms) * (ebn + 16) / 128.0;
+    const double c_pad = (double)cdiv(ia, sms);
+    use_edge = c_edge < 0.95 * c_pad;
+  }
+  if (use_edge) {
+    GParams g1 = gp;
+    g1.tiles_n = (int)(g.N / 128);
+    g1.tiles = tm * g1.tiles_n;
+    g1.items = g1.tiles * splits;
+    g1.n_off = 0;
+    RH_CHECK((launch_layout<128, 128>(g, g1, st)));
+    GParams g2 = gp;
+    g2.tiles_n = 1;
+    g2.tiles = tm;
+    g2.items = g2.tiles * splits;
+    g2.n_off = (int)(g.N - rem);
+    RH_CHECK(launch_edge(ebn, g, g2, st));
+  } else if (big) {
     RH_CHECK((launch_layout<128, 128>(g, gp, st)));
-  else
+  } else {
     RH_CHECK((launch_layout<64, 64>(g, gp, st)));
+  }
 
   if (g.epi == EPI_RESID) {
     sum_fixed_order_kernel<<<1, 256, 0, st>>>(gp.part, gp.items * (GTHREADS / 32), g.resid_out);

@@ -20,8 +20,11 @@ def dev(x):
     return torch.as_tensor(np.ascontiguousarray(x), device="cuda")
 
 
+# (1000, 730, 2048), (147, 3000, 2048), (3000, 147, 2500), (200, 300, 5000): 128-tiles plus a
+# narrower column-edge launch (96 / 32 / 64 wide), with and without split-K
 @pytest.mark.parametrize("M,N,K", [(1, 1, 1), (7, 5, 3), (64, 64, 16), (130, 67, 301), (200, 300, 5000),
-                                   (513, 129, 1000), (31, 33, 20000)])
+                                   (513, 129, 1000), (31, 33, 20000), (1000, 730, 2048), (147, 3000, 2048),
+                                   (3000, 147, 2500)])
 @pytest.mark.parametrize("ta,tb", [(False, False), (True, False), (False, True), (True, True)])
 def test_dgemm(rh, M, N, K, ta, tb):
     rng = np.random.default_rng(M * 7 + N * 13 + K)
