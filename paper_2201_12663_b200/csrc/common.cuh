@@ -34,6 +34,16 @@ inline int64_t cdiv(int64_t x, int64_t m) { return (x + m - 1) / m; }
 
 int num_sms();
 
+// Small device -> host readbacks (ranks, Ritz values, flags) go through pinned memory: a
+// cudaMemcpyAsync into pageable memory is staged by the driver and can queue behind the
+// large pinned copies already in flight (rhosvd_c2t_host's H2D of the side matrices),
+// which stalled every host decision of the eigensolvers until the whole input had landed.
+// d2h_wait copies `bytes` from device `src` to host `dst` through this thread's pinned
+// buffer and waits for stream `st`.
+int d2h_wait(void* dst, const void* src, size_t bytes, cudaStream_t st);
+// host -> device counterpart (through a pinned staging block; waits for `st`)
+int h2d_wait(void* dst, const void* src, size_t bytes, cudaStream_t st);
+
 // count of kernels launched by the library (per-thread; reset by rhosvd_c2t)
 extern thread_local int g_launches;
 // cap on cooperative grids launched from this thread (0 = none): the three concurrent

@@ -55,6 +55,62 @@ int num_sms() {
   return s;
 }
 
+// pinned staging blocks of d2h_wait (shared by all threads; a block is owned by one
+// readback at a time)
+static std::mutex g_pin_mu;
+static std::multimap<size_t, void*> g_pin_free;
+
+// one staging block out of the pool (or a new one of >= bytes)
+static void* pin_get(size_t bytes, size_t* cap) {
+  {
+    std::lock_guard<std::mutex> lk(g_pin_mu);
+    auto it = g_pin_free.lower_bound(bytes);
+    if (it != g_pin_free.end()) {
+      *cap = it->first;
+      void* b = it->second;
+      g_pin_free.erase(it);
+      return b;
+    }
+  }
+  void* b = nullptr;
+  *cap = std::max<size_t>(4096, bytes);
+  if (cudaMallocHost(&b, *cap) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return b;
+}
+static void pin_put(void* b, size_t cap) {
+  std::lock_guard<std::mutex> lk(g_pin_mu);
+  g_pin_free.emplace(cap, b);
+}
+
+int h2d_wait(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return RHOSVD_OK;
+  size_t cap = 0;
+  void* buf = pin_get(bytes, &cap);
+  if (!buf) return fail(RHOSVD_ENOMEM, "pinned staging buffer");
+  std::memcpy(buf, src, bytes);
+  cudaError_t e = cudaMemcpyAsync(dst, buf, bytes, cudaMemcpyHostToDevice, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  pin_put(buf, cap);
+  if (e != cudaSuccess) return fail(RHOSVD_ECUDA, std::string("staging: ") + cudaGetErrorString(e));
+  return RHOSVD_OK;
+}
+
+int d2h_wait(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  if (bytes == 0) return RHOSVD_OK;
+  size_t cap = 0;
+  void* buf = pin_get(bytes, &cap);
+  if (!buf) return fail(RHOSVD_ENOMEM, "pinned readback buffer");
+  cudaError_t e = cudaMemcpyAsync(buf, src, bytes, cudaMemcpyDeviceToHost, st);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+  if (e == cudaSuccess) std::memcpy(dst, buf, bytes);
+  pin_put(buf, cap);
+  if (e != cudaSuccess) return fail(RHOSVD_ECUDA, std::string("readback: ") + cudaGetErrorString(e));
+  return RHOSVD_OK;
+}
+
 struct DBuf {
   double* p = nullptr;
   size_t cap = 0;
@@ -600,8 +656,7 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     if (b >= m) break;  // full space: exact after one step
     if (itb < 2) continue;
     d_h.resize(b);
-    RH_CUDA(cudaMemcpyAsync(d_h.data(), w.th.p, b * sizeof(double), cudaMemcpyDeviceToHost, st));
-    RH_CUDA(cudaStreamSynchronize(st));
+    RH_CHECK(d2h_wait(d_h.data(), w.th.p, b * sizeof(double), st));
     if (epsmode) r_est = predict_r(d_h, b);
     if (epsmode && r_est + p > b && guard < 12) {
       // grow towards the predicted size, at most 2x per event (the log-linear tail
@@ -714,10 +769,9 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
   double sel[4];
   RH_CHECK(k_select_rank(w.th.p, b, scal + 16 + mode, T, epsmode ? o.eps : 0.0, (int)rfix, 8, w.tail2.p,
                          scal + 24 + 4 * mode, w.inv.p, st));
-  RH_CUDA(cudaMemcpyAsync(sel, scal + 24 + 4 * mode, 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  RH_CHECK(d2h_wait(sel, scal + 24 + 4 * mode, 3 * sizeof(double), st));
   double rho_h = 0.0;
-  RH_CUDA(cudaMemcpyAsync(&rho_h, scal + 16 + mode, sizeof(double), cudaMemcpyDeviceToHost, st));
-  RH_CUDA(cudaStreamSynchronize(st));
+  RH_CHECK(d2h_wait(&rho_h, scal + 16 + mode, sizeof(double), st));
   int64_t r = (int64_t)sel[0];
   if (r < 0) {  // the block did not reach the threshold (should not happen after growth)
     r = b;
@@ -845,8 +899,7 @@ static int als_update(Ctx& c, int l, int64_t n, int64_t LDN, int64_t Rl, int64_t
     RH_CHECK(orth(c, n, bsz, LDN, w.Y.p, w.Z.p, w.T1.p, ldb, it == 1 ? ORTH_SCQR3 : ORTH_CQR2));
     if (it == 2 && bsz > r) {
       // rate lambda_{b} / lambda_r from the Rayleigh quotients -> iterations for 1e-13
-      RH_CUDA(cudaMemcpyAsync(d_h.data(), w.th.p, bsz * sizeof(double), cudaMemcpyDeviceToHost, st));
-      RH_CUDA(cudaStreamSynchronize(st));
+      RH_CHECK(d2h_wait(d_h.data(), w.th.p, bsz * sizeof(double), st));
       const double dr = std::max(d_h[r - 1], 1e-300);
       const double rho = std::min(0.995, std::max(d_h[bsz - 1], 1e-300 * dr) / dr);
       need = std::max(3, std::min(60, 2 + (int)std::ceil(std::log(1e-13) / std::log(rho))));
@@ -1055,10 +1108,9 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
                          o.oversample * 17 + o.block0 * 19 + o.refine_steps * 23) % 1000000007) +
                o.eps * 1e6;
     double v[4] = {(double)Rl, h, h * h, 1.0};
-    RH_CUDA(cudaMemcpyAsync(w.scal.p, v, sizeof(v), cudaMemcpyHostToDevice, st));
+    RH_CHECK(h2d_wait(w.scal.p, v, sizeof(v), st));
     RH_CHECK(allreduce(c, w.scal.p, 4));
-    RH_CUDA(cudaMemcpyAsync(v, w.scal.p, sizeof(v), cudaMemcpyDeviceToHost, st));
-    RH_CUDA(cudaStreamSynchronize(st));
+    RH_CHECK(d2h_wait(v, w.scal.p, sizeof(v), st));
     if (std::fabs(v[1] - world * h) > 1e-6 * std::fabs(world * h) + 1e-9 ||
         std::fabs(v[2] - world * h * h) > 1e-6 * std::fabs(world * h * h) + 1e-9)
       return fail(RHOSVD_EMISMATCH, "ranks disagree on n / options");
@@ -1121,16 +1173,14 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
   // flag -> scal[8] as double (non-finite count)
   {
     int fl = 0;
-    RH_CUDA(cudaMemcpyAsync(&fl, w.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-    RH_CUDA(cudaStreamSynchronize(st));
+    RH_CHECK(d2h_wait(&fl, w.flag, sizeof(int), st));
     double f = fl ? 1.0 : 0.0;
-    RH_CUDA(cudaMemcpyAsync(w.scal.p + 8, &f, sizeof(double), cudaMemcpyHostToDevice, st));
+    RH_CHECK(h2d_wait(w.scal.p + 8, &f, sizeof(double), st));
   }
   tm.mark(PH_NORM);
   RH_CHECK(allreduce(c, w.scal.p + 4, 5));  // T1..T3, ||xi'||^2, flag
   double sc[5];
-  RH_CUDA(cudaMemcpyAsync(sc, w.scal.p + 4, sizeof(sc), cudaMemcpyDeviceToHost, st));
-  RH_CUDA(cudaStreamSynchronize(st));
+  RH_CHECK(d2h_wait(sc, w.scal.p + 4, sizeof(sc), st));
   if (sc[4] != 0.0) {
     cudaEventDestroy(g0);
     cudaEventDestroy(g1);
@@ -1206,6 +1256,7 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
       cudaStream_t ls = cl.st;
       int* fl = w.flag + 1 + l;
       RH_CUDA(cudaStreamWaitEvent(ls, evU[l], 0));
+      TL().mark(l, "H2D landed", ls);
       RH_CHECK(k_normalize(U[l], ldu, n, Rl, Rp, Uh[l], LDN, w.s.p + l * Rp, w.tcol.p + l * Rp, fl, ls));
       RH_CHECK(k_fixed_sum(w.tcol.p + l * Rp, Rp, w.scal.p + 4 + l, ls));
       RH_CUDA(cudaEventRecord(evN[l], ls));
@@ -1214,11 +1265,11 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
       RH_CHECK(mm(cl, n, n, Rl, Uh[l], LDN, false, Uh[l], LDN, false, w.G.p + (size_t)l * LDN * LDN, LDN, nullptr,
                   true));
       RH_CUDA(cudaEventRecord(evG[l][1], ls));
+      TL().mark(l, "Gram", ls);
       double tl = 0.0;
       int fh = 0;
-      RH_CUDA(cudaMemcpyAsync(&tl, w.scal.p + 4 + l, sizeof(double), cudaMemcpyDeviceToHost, ls));
-      RH_CUDA(cudaMemcpyAsync(&fh, fl, sizeof(int), cudaMemcpyDeviceToHost, ls));
-      RH_CUDA(cudaStreamSynchronize(ls));
+      RH_CHECK(d2h_wait(&tl, w.scal.p + 4 + l, sizeof(double), ls));
+      RH_CHECK(d2h_wait(&fh, fl, sizeof(int), ls));
       if (fh) return fail(RHOSVD_ENONFINITE, "NaN/Inf in U");
       rep.trace[l] = tl;
       TL().mark(l, "normalize + Gram", ls);
@@ -1279,9 +1330,8 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
       if (xs != RHOSVD_OK) return xs;
       double x2 = 0.0;
       int fx = 0;
-      RH_CUDA(cudaMemcpyAsync(&x2, w.scal.p + 7, sizeof(double), cudaMemcpyDeviceToHost, st));
-      RH_CUDA(cudaMemcpyAsync(&fx, w.flag, sizeof(int), cudaMemcpyDeviceToHost, st));
-      RH_CUDA(cudaStreamSynchronize(st));
+      RH_CHECK(d2h_wait(&x2, w.scal.p + 7, sizeof(double), st));
+      RH_CHECK(d2h_wait(&fx, w.flag, sizeof(int), st));
       for (int l = 0; l < 3; ++l) {
         float gm = 0.f;
         if (mst[l] == RHOSVD_OK && cudaEventElapsedTime(&gm, evG[l][0], evG[l][1]) == cudaSuccess) gram_ms_streamed += gm;
@@ -1478,9 +1528,7 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
   }
   tm.mark(-1);
   double bn2 = 0.0;
-  if (total > 0) {
-    RH_CUDA(cudaMemcpyAsync(&bn2, w.scal.p + 12, sizeof(double), cudaMemcpyDeviceToHost, st));
-  }
+  if (total > 0) RH_CHECK(d2h_wait(&bn2, w.scal.p + 12, sizeof(double), st));
   RH_CUDA(cudaStreamSynchronize(st));
   if (cp) RH_CUDA(cudaStreamSynchronize(cp));
   RH_CUDA(cudaGetLastError());

@@ -773,8 +773,7 @@ int syevj(int64_t b, const double* A, int64_t lda, double* lambda, double* Vout,
   RH_LAUNCH_CHECK();
   if (sweeps_host) {
     int info[4];
-    RH_CUDA(cudaMemcpyAsync(info, ws.info, sizeof(info), cudaMemcpyDeviceToHost, st));
-    RH_CUDA(cudaStreamSynchronize(st));
+    RH_CHECK(d2h_wait(info, ws.info, sizeof(info), st));
     *sweeps_host = info[0];
     if (info[2]) *sweeps_host = -info[0];  // negative: not converged
   }
