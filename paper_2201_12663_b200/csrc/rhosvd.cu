@@ -1442,9 +1442,9 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
       if (!(comm && comm->active())) {  // with a communicator beta is complete only after the all-reduce
         cudaStream_t* ms = mode_streams();
         if (!ms) return fail(RHOSVD_ECUDA, "mode stream creation failed");
-        static const int nchunks = [] {
+        static const int nchunks = [] {  // 16: the exposed D2H of the last chunk is ~140 MB
           const char* e = getenv("RHOSVD_CORE_CHUNKS");
-          return e ? std::max(1, atoi(e)) : 8;
+          return e ? std::max(1, atoi(e)) : 16;
         }();
         chunks.count = nchunks;
         chunks.side = ms[1];
