@@ -256,7 +256,8 @@ def run_ours(args):
     ms_max = max_over_ranks(e0.elapsed_time(e1), dev)
     value = p.R * args.steps / (ms_max * 1e-3)
 
-    # dominant kernel roofline (FP64 DMMA pipe): the core K7 for cfg 2/4, the Gram K1 for cfg 3/5
+    # dominant kernel roofline (FP64 DMMA pipe): the one with the larger share of the step
+    # (the core K7 on cfg 2/4, the Gram K1 on cfg 3/5)
     rep = reps[-1]
     r1, r2, r3 = rep["ranks"]
     Rl = k1 - k0
@@ -264,7 +265,7 @@ def run_ours(args):
     gram_flops = 3.0 * p.n * (p.n + 1) * Rl  # upper-triangle Gram, 3 modes
     core_ms = sum(r["core_ms"] for r in reps) / len(reps)
     gram_ms = sum(r["gram_ms"] for r in reps) / len(reps)
-    if core_flops * gram_ms >= gram_flops * core_ms or args.config in (2, 4):
+    if core_ms >= gram_ms:
         dom, fl, kms = "core_kr (K7)", core_flops, core_ms
     else:
         dom, fl, kms = "gram (K1)", gram_flops, gram_ms
