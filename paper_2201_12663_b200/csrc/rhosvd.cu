@@ -739,39 +739,53 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     ++mo.refines;
     c.tm->mark(PH_RR);
   }
-  // final one-sided Rayleigh-Ritz: W W^T = P Lambda P^T (high relative accuracy Jacobi)
-  RH_CHECK(mm(c, b, b, Rl, w.W.p, Rp, true, w.W.p, Rp, true, w.S.p, ldb, nullptr, true));
-  RH_CHECK(allreduce(c, w.S.p, ldb * b));
-  TL().mark(mode, "W W^T", st);
-  c.tm->mark(PH_RR);
-  {
-    int sw = 0;
-    RH_CHECK(syevj(b, w.S.p, ldb, w.th.p, w.V.p, ldb, 1e-15, 1e-300, 80, w.dws, st, &sw));
-    if (dbg_on()) fprintf(stderr, "[rhosvd dbg] mode %d rr b %lld sweeps %d\n", mode, (long long)b, sw);
-    if (sw < 0) return fail(RHOSVD_ENOCONV, "Jacobi on W W^T did not converge");
-    TL().mark(mode, "Jacobi", st);
-  }
-  c.tm->mark(PH_RANK);
-  // rho = ||Uhat - Z W||_F^2 (fused residual epilogue; E never stored)
-  {
-    GemmArgs g;
-    g.M = n; g.N = Rl; g.K = b; g.A = w.Z.p; g.lda = LDN; g.a_k = false; g.B = w.W.p; g.ldb = Rp; g.b_k = false;
-    g.epi = EPI_RESID; g.D = Uh; g.ldd = LDN; g.resid_out = scal + 16 + mode;
-    if (Rl > 0) {
-      RH_CHECK(gemm(g, w.gsc, st, &c.flops));
-    } else {
-      RH_CUDA(cudaMemsetAsync(scal + 16 + mode, 0, sizeof(double), st));
-    }
-    RH_CHECK(allreduce(c, scal + 16 + mode, 1));
-    TL().mark(mode, "residual", st);
-    c.tm->mark(PH_RANK);
-  }
+  // The rank rule must be met inside the block after the growth (rho = tail2[b] is the
+  // block's residual, ~1e-7 on cfg 4 against eps^2 T = 4.8e-6).  A miss is an anomaly:
+  // on cfg 4 about one call in 50 returned a residual 1e2-1e3 times too large for one mode
+  // (the recomputation is bitwise the normal value, so the inputs Z, W are right and the
+  // residual GEMM was transiently wrong; cause open, profiles/README.md r1z).  It is
+  // reported on stderr and the final step is recomputed (single GPU only: with a
+  // communicator every rank would have to agree to redo the collectives).
   double sel[4];
-  RH_CHECK(k_select_rank(w.th.p, b, scal + 16 + mode, T, epsmode ? o.eps : 0.0, (int)rfix, 8, w.tail2.p,
-                         scal + 24 + 4 * mode, w.inv.p, st));
-  RH_CHECK(d2h_wait(sel, scal + 24 + 4 * mode, 3 * sizeof(double), st));
   double rho_h = 0.0;
-  RH_CHECK(d2h_wait(&rho_h, scal + 16 + mode, sizeof(double), st));
+  for (int attempt = 0;; ++attempt) {
+    // final one-sided Rayleigh-Ritz: W W^T = P Lambda P^T (high relative accuracy Jacobi)
+    RH_CHECK(mm(c, b, b, Rl, w.W.p, Rp, true, w.W.p, Rp, true, w.S.p, ldb, nullptr, true));
+    RH_CHECK(allreduce(c, w.S.p, ldb * b));
+    TL().mark(mode, "W W^T", st);
+    c.tm->mark(PH_RR);
+    {
+      int sw = 0;
+      RH_CHECK(syevj(b, w.S.p, ldb, w.th.p, w.V.p, ldb, 1e-15, 1e-300, 80, w.dws, st, &sw));
+      if (dbg_on()) fprintf(stderr, "[rhosvd dbg] mode %d rr b %lld sweeps %d\n", mode, (long long)b, sw);
+      if (sw < 0) return fail(RHOSVD_ENOCONV, "Jacobi on W W^T did not converge");
+      TL().mark(mode, "Jacobi", st);
+    }
+    c.tm->mark(PH_RANK);
+    // rho = ||Uhat - Z W||_F^2 (fused residual epilogue; E never stored)
+    {
+      GemmArgs g;
+      g.M = n; g.N = Rl; g.K = b; g.A = w.Z.p; g.lda = LDN; g.a_k = false; g.B = w.W.p; g.ldb = Rp; g.b_k = false;
+      g.epi = EPI_RESID; g.D = Uh; g.ldd = LDN; g.resid_out = scal + 16 + mode;
+      if (Rl > 0) {
+        RH_CHECK(gemm(g, w.gsc, st, &c.flops));
+      } else {
+        RH_CUDA(cudaMemsetAsync(scal + 16 + mode, 0, sizeof(double), st));
+      }
+      RH_CHECK(allreduce(c, scal + 16 + mode, 1));
+      TL().mark(mode, "residual", st);
+      c.tm->mark(PH_RANK);
+    }
+    RH_CHECK(k_select_rank(w.th.p, b, scal + 16 + mode, T, epsmode ? o.eps : 0.0, (int)rfix, 8, w.tail2.p,
+                           scal + 24 + 4 * mode, w.inv.p, st));
+    RH_CHECK(d2h_wait(sel, scal + 24 + 4 * mode, 3 * sizeof(double), st));
+    RH_CHECK(d2h_wait(&rho_h, scal + 16 + mode, sizeof(double), st));
+    if (sel[0] >= 0 || attempt >= 2 || (c.comm && c.comm->active())) break;
+    fprintf(stderr,
+            "[rhosvd] mode %d: rank rule not met inside the block (b %lld, rho %.6e, T %.6e, tail2 %.6e);"
+            " recomputing the final Rayleigh-Ritz step (attempt %d)\n",
+            mode, (long long)b, rho_h, T, sel[1], attempt + 1);
+  }
   int64_t r = (int64_t)sel[0];
   if (r < 0) {  // the block did not reach the threshold (should not happen after growth)
     r = b;
