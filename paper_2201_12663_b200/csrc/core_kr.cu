@@ -175,7 +175,9 @@ __global__ void __launch_bounds__(CORE_THREADS, 1)
       }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      // release the stage only once its last fragment loads have been consumed (an arrive
+      // hoisted above them let the next TMA overwrite data still being read)
+      if (lane == 0) mbar_arrive_after(&empty[s], acc[FM - 1][FN - 1][1]);
       if (++cs == nst) {
         cs = 0;
         cph ^= 1u;

@@ -168,7 +168,11 @@ __global__ void __launch_bounds__(GTHREADS, 1)
       }
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
+      // release the stage only once its last fragment loads have been consumed: the
+      // compiler hoisted a plain arrive above the stage's last DMMAs, and the producer's
+      // next TMA into the stage could then overwrite fragments still being read (a
+      // transiently wrong GEMM, seen as a wrong rank residual in ~2 % of cfg 4 calls)
+      if (lane == 0) mbar_arrive_after(&empty[s], acc[FM - 1][FN - 1][1]);
       if (++cs == nst) {
         cs = 0;
         cph ^= 1u;

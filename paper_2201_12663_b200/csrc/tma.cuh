@@ -32,6 +32,20 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t by
 __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];\n" ::"r"(smem_u32(bar)) : "memory");
 }
+// arrive once `dep` (a register produced from the stage's last fragment loads) exists:
+// the stage is released only after every load from it has returned its value, so the
+// producer's next TMA into the stage cannot overtake a read still in flight
+__device__ __forceinline__ void mbar_arrive_after(uint64_t* bar, double dep) {
+  asm volatile(
+      "{\n"
+      ".reg .pred q;\n"
+      "setp.eq.f64 q, %1, %1;\n"  // true unless NaN; either way one arrive, after dep exists
+      "@q mbarrier.arrive.shared::cta.b64 _, [%0];\n"
+      "@!q mbarrier.arrive.shared::cta.b64 _, [%0];\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "d"(dep)
+      : "memory");
+}
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   asm volatile(
       "{\n"
