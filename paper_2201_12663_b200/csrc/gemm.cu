@@ -414,9 +414,9 @@ int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
   // column edge: N % 128 leftover columns as one narrower segment (BN 32 / 64 / 96) so
   // the last column tile does not run padded DMMAs (b = 730: 768 -> 736 columns; b = 147:
   // 256 -> 160).  Not for the symmetric (upper-tile) or residual-epilogue forms.
-  // OFF by default (RHOSVD_GEMM_EDGE=1 enables it): bitwise repeatable as a kernel, but
-  // with it the concurrent-mode C2T on cfg 3 returned a different (less accurate) mode
-  // result in ~7 % of calls, cause not yet found (profiles/README.md r1z).
+  // OFF by default (RHOSVD_GEMM_EDGE=1 enables it): with it the concurrent-mode C2T on
+  // cfg 3 differed from run to run in ~7 % of calls - most likely the ring race fixed in
+  // r1z (profiles/README.md) - and it has not been re-validated since.
   static const bool edge_on = [] {
     const char* e = getenv("RHOSVD_GEMM_EDGE");
     return e && e[0] == '1';

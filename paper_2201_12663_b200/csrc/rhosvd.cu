@@ -740,12 +740,11 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     c.tm->mark(PH_RR);
   }
   // The rank rule must be met inside the block after the growth (rho = tail2[b] is the
-  // block's residual, ~1e-7 on cfg 4 against eps^2 T = 4.8e-6).  A miss is an anomaly:
-  // on cfg 4 about one call in 50 returned a residual 1e2-1e3 times too large for one mode
-  // (the recomputation is bitwise the normal value, so the inputs Z, W are right and the
-  // residual GEMM was transiently wrong; cause open, profiles/README.md r1z).  It is
-  // reported on stderr and the final step is recomputed (single GPU only: with a
-  // communicator every rank would have to agree to redo the collectives).
+  // block's residual, ~1e-7 on cfg 4 against eps^2 T = 4.8e-6).  A miss is an anomaly -
+  // it exposed a pipeline race in the GEMM engine (fixed: mbar_arrive_after, see
+  // profiles/README.md r1z) - so it is reported on stderr and the final step is
+  // recomputed (single GPU only: with a communicator every rank would have to agree to
+  // redo the collectives).
   double sel[4];
   double rho_h = 0.0;
   for (int attempt = 0;; ++attempt) {
