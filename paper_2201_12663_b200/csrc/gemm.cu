@@ -414,12 +414,12 @@ int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
   // column edge: N % 128 leftover columns as one narrower segment (BN 32 / 64 / 96) so
   // the last column tile does not run padded DMMAs (b = 730: 768 -> 736 columns; b = 147:
   // 256 -> 160).  Not for the symmetric (upper-tile) or residual-epilogue forms.
-  // OFF by default (RHOSVD_GEMM_EDGE=1 enables it): with it the concurrent-mode C2T on
-  // cfg 3 differed from run to run in ~7 % of calls - most likely the ring race fixed in
-  // r1z (profiles/README.md) - and it has not been re-validated since.
+  // RHOSVD_GEMM_EDGE=0 disables it.  (Before the ring fix of r1z, profiles/README.md, the
+  // extra launches made that race visible as run-to-run differences on cfg 3; after it,
+  // 250 cfg 3 calls with the edge were bitwise identical.)
   static const bool edge_on = [] {
     const char* e = getenv("RHOSVD_GEMM_EDGE");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   const int64_t rem = g.N % 128;
   const int ebn = (int)round_up(rem, 32);

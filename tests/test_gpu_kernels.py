@@ -20,8 +20,8 @@ def dev(x):
     return torch.as_tensor(np.ascontiguousarray(x), device="cuda")
 
 
-# (1000, 730, 2048), (147, 3000, 2048), (3000, 147, 2500), (200, 300, 5000): the shapes where
-# RHOSVD_GEMM_EDGE=1 adds a narrower column-edge launch (tests/test_gpu_tiling_invariance.py)
+# (1000, 730, 2048), (147, 3000, 2048), (3000, 147, 2500), (200, 300, 5000): 128-tiles plus a
+# narrower column-edge launch where the wave model takes it, with and without split-K
 @pytest.mark.parametrize("M,N,K", [(1, 1, 1), (7, 5, 3), (64, 64, 16), (130, 67, 301), (200, 300, 5000),
                                    (513, 129, 1000), (31, 33, 20000), (1000, 730, 2048), (147, 3000, 2048),
                                    (3000, 147, 2500)])
