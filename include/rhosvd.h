@@ -39,6 +39,10 @@
  *
  * Thread safety: calls on different streams/handles may run concurrently;
  * one rhosvd_comm must not be used by two calls at once.
+ *
+ * Devices: one CUDA device per process.  The first call pins the current device
+ * (workspaces, output caches and kernel attributes are process-wide); a call made
+ * while another device is current returns RHOSVD_EINVAL.
  */
 #ifndef RHOSVD_H_
 #define RHOSVD_H_
@@ -54,7 +58,12 @@ typedef enum {
   RHOSVD_OK = 0,
   RHOSVD_EINVAL = -1,      /* bad argument (null pointer, n < 1, R_local < 0, ldu < n, eps not in (0,1), r < 1) */
   RHOSVD_ENONFINITE = -2,  /* NaN/Inf in U or xi (detected by the normalisation kernel) */
-  RHOSVD_ENOCONV = -3,     /* a small dense solver (Jacobi / Cholesky) did not converge */
+  RHOSVD_ENOCONV = -3,     /* no convergence: the subspace iteration stopped at max_iters
+                              short of its modelled count (sin theta_r ~ rho^(iters + refine)
+                              > 1e-7, rho = block-edge Rayleigh quotient / r-th), the eps rank
+                              rule was not met inside the final block (A1),
+                              or a small dense Jacobi solve did not converge.  Never a silently
+                              truncated rank. */
   RHOSVD_ENOMEM = -4,      /* device allocation failed */
   RHOSVD_ECUDA = -5,       /* CUDA runtime error */
   RHOSVD_ENCCL = -6,       /* collective failed */
@@ -62,7 +71,13 @@ typedef enum {
 } rhosvd_status;
 
 enum { RHOSVD_FIXED_RANK = 0, RHOSVD_EPS = 1 };
-enum { RHOSVD_F_SIGN_FIX = 1u, RHOSVD_F_KEEP_W = 2u };
+/* Flags.  SIGN_FIX: canonical frame signs (A9).  KEEP_W: the CP factors W_l of the core
+ * are kept in the result (always the case in this build; the flag is accepted for ABI
+ * compatibility).  ROOT_ONLY_CORE (multi-rank only): the core's sum over the R shards is
+ * reduced to rank 0 (ncclReduce) instead of all-reduced; on the other ranks
+ * rhosvd_result_core / rhosvd_result_host_core / rhosvd_t2c return EINVAL and
+ * report.beta_norm is NaN.  Frames, sigma and ranks stay replicated. */
+enum { RHOSVD_F_SIGN_FIX = 1u, RHOSVD_F_KEEP_W = 2u, RHOSVD_F_ROOT_ONLY_CORE = 4u };
 
 /* Options.  Initialise with rhosvd_opts_default(). */
 typedef struct {

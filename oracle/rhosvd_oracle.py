@@ -196,11 +196,14 @@ class OracleResult:
     report: dict = field(default_factory=dict)
 
 
-def rhosvd(Us, xi, eps=None, ranks=None, with_W=True):
+def rhosvd(Us, xi, eps=None, ranks=None, with_W=True, with_core=True):
     """RHOSVD canonical-to-Tucker transform (O1-O8), d = len(Us) (3 here).
 
     Us: list of (R, n_l) arrays (raw, unnormalized); xi: (R,).
     Exactly one of eps (relative tail rule A1) or ranks (fixed) is given.
+    with_core=False stops after O6 (frames, sigma, ranks, W; beta = None): the
+    Tucker tensor is then fixed by the frames through Def. 2.1, and the full-size
+    parity fixtures need only those.
     """
     d = len(Us)
     if (eps is None) == (ranks is None):
@@ -225,7 +228,9 @@ def rhosvd(Us, xi, eps=None, ranks=None, with_W=True):
         tails.append(math.sqrt(max(tail2[r], 0.0)) if sg.shape[0] else 0.0)
         margins.append(mar)
         Ws.append(project(Z, Uh[l]))
-    if d == 3:
+    if not with_core:
+        beta = None
+    elif d == 3:
         beta = core_kr(Ws[0], Ws[1], Ws[2], xip)
     else:
         raise NotImplementedError("hot path is d = 3")
@@ -233,7 +238,7 @@ def rhosvd(Us, xi, eps=None, ranks=None, with_W=True):
     rep = dict(
         ranks=list(rs), trace=[float(t) for t in T], tail=[float(t) for t in tails],
         xi_norm=float(np.linalg.norm(xip)), bound_paper=bp, bound_ns=bns,
-        beta_norm=float(np.linalg.norm(beta)),
+        beta_norm=None if beta is None else float(np.linalg.norm(beta)),
         margins=[[None if v is None else float(v) for v in m] for m in margins],
         near_tie=[bool(m[0] is not None and (abs(m[0]) < 1e-6 or abs(m[1]) < 1e-6)) for m in margins],
     )

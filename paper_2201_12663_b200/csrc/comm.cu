@@ -24,6 +24,8 @@ struct NcclApi {
   int (*getUniqueId)(void*) = nullptr;
   int (*commInitRank)(void**, int, NcclUid, int) = nullptr;
   int (*allReduce)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
+  int (*reduce)(const void*, void*, size_t, int, int, int, void*, cudaStream_t) = nullptr;
+  int (*broadcast)(const void*, void*, size_t, int, int, void*, cudaStream_t) = nullptr;
   int (*commDestroy)(void*) = nullptr;
   const char* (*getErrorString)(int) = nullptr;
   bool ok = false;
@@ -42,9 +44,11 @@ NcclApi& api() {
       a.getUniqueId = (int (*)(void*))dlsym(a.h, "ncclGetUniqueId");
       a.commInitRank = (int (*)(void**, int, NcclUid, int))dlsym(a.h, "ncclCommInitRank");
       a.allReduce = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(a.h, "ncclAllReduce");
+      a.reduce = (int (*)(const void*, void*, size_t, int, int, int, void*, cudaStream_t))dlsym(a.h, "ncclReduce");
+      a.broadcast = (int (*)(const void*, void*, size_t, int, int, void*, cudaStream_t))dlsym(a.h, "ncclBroadcast");
       a.commDestroy = (int (*)(void*))dlsym(a.h, "ncclCommDestroy");
       a.getErrorString = (const char* (*)(int))dlsym(a.h, "ncclGetErrorString");
-      a.ok = a.getUniqueId && a.commInitRank && a.allReduce && a.commDestroy;
+      a.ok = a.getUniqueId && a.commInitRank && a.allReduce && a.reduce && a.broadcast && a.commDestroy;
     }
   }
   return a;
@@ -71,6 +75,31 @@ int comm_allreduce(rhosvd_comm* c, double* p, int64_t count, cudaStream_t st) {
   e = cudaDeviceSynchronize();
   if (e != cudaSuccess) return fail(RHOSVD_ECUDA, cudaGetErrorString(e));
   return RHOSVD_OK;
+}
+
+static int nccl_status(int r, const char* what) {
+  if (r == 0) return RHOSVD_OK;
+  return fail(RHOSVD_ENCCL, std::string(what) + ": " +
+                                (api().getErrorString ? api().getErrorString(r) : std::to_string(r)));
+}
+
+int comm_reduce_root(rhosvd_comm* c, double* p, int64_t count, cudaStream_t st) {
+  if (!c || !c->active() || count <= 0) return RHOSVD_OK;
+  if (c->kind == rhosvd_comm::NCCL)
+    return nccl_status(api().reduce(p, p, (size_t)count, kNcclFloat64, kNcclSum, 0, c->nccl, st), "ncclReduce");
+  return comm_allreduce(c, p, count, st);  // callback backend: every rank gets the sum
+}
+
+int comm_broadcast(rhosvd_comm* c, double* p, int64_t count, int root, cudaStream_t st) {
+  if (!c || !c->active() || count <= 0) return RHOSVD_OK;
+  if (c->kind == rhosvd_comm::NCCL)
+    return nccl_status(api().broadcast(p, p, (size_t)count, kNcclFloat64, root, c->nccl, st), "ncclBroadcast");
+  // callback backend (sum only): the non-root ranks contribute zeros; x + 0 = x exactly
+  if (c->rank != root) {
+    cudaError_t e = cudaMemsetAsync(p, 0, (size_t)count * sizeof(double), st);
+    if (e != cudaSuccess) return fail(RHOSVD_ECUDA, cudaGetErrorString(e));
+  }
+  return comm_allreduce(c, p, count, st);
 }
 
 }  // namespace rhosvd

@@ -23,4 +23,9 @@ struct rhosvd_comm {
 namespace rhosvd {
 // in-place fp64 sum all-reduce over all ranks (no-op for world == 1 / null comm)
 int comm_allreduce(rhosvd_comm* c, double* p, int64_t count, cudaStream_t st);
+// in-place fp64 sum reduce to rank 0 (RHOSVD_F_ROOT_ONLY_CORE); the callback backend
+// all-reduces instead
+int comm_reduce_root(rhosvd_comm* c, double* p, int64_t count, cudaStream_t st);
+// in-place broadcast of `count` doubles from rank `root`
+int comm_broadcast(rhosvd_comm* c, double* p, int64_t count, int root, cudaStream_t st);
 }  // namespace rhosvd

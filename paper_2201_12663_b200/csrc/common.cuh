@@ -34,6 +34,12 @@ inline int64_t cdiv(int64_t x, int64_t m) { return (x + m - 1) / m; }
 
 int num_sms();
 
+// One CUDA device per process: the workspace, the output caches, the cached SM count and
+// the per-kernel shared-memory attributes are process-wide.  The first library call pins
+// the current device; a later call on another device fails with EINVAL (instead of
+// reusing the first device's buffers).
+int device_guard();
+
 // Small device -> host readbacks (ranks, Ritz values, flags) go through pinned memory: a
 // cudaMemcpyAsync into pageable memory is staged by the driver and can queue behind the
 // large pinned copies already in flight (rhosvd_c2t_host's H2D of the side matrices),

@@ -285,6 +285,7 @@ extern "C" int rhosvd_conv3d(const double* const Fa[3], int64_t lda, const doubl
   for (int l = 0; l < 3; ++l)
     if (!Fa[l] || !Fp[l] || !Fout[l]) return fail(RHOSVD_EINVAL, "conv3d: null factor");
   if (lda & 1) return fail(RHOSVD_EINVAL, "conv3d: lda must be even (16-B TMA rows)");
+  RH_CHECK(device_guard());
   cudaStream_t st = (cudaStream_t)stream;
   g_launches = 0;
   outer_weights_kernel<<<(unsigned)cdiv(Ra * Rp, 256), 256, 0, st>>>(ca, (int)Ra, cp, (int)Rp, wout);

@@ -402,13 +402,12 @@ int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
   if (g.K <= 0) {  // empty contraction: C = beta C
     GParams z = gp;
     z.splits = 1;
-    if (!scr.ensure((size_t)g.M * g.N, st)) {
-      RH_CUDA(cudaMemsetAsync(scr.ptr, 0, (size_t)g.M * g.N * sizeof(double), st));
-      z.part = scr.ptr;
-      splitk_reduce_kernel<<<(unsigned)cdiv(g.M * g.N, 256), 256, 0, st>>>(z);
-      count_launch();
-      RH_LAUNCH_CHECK();
-    }
+    RH_CHECK(scr.ensure((size_t)g.M * g.N, st));  // ENOMEM goes back to the caller
+    RH_CUDA(cudaMemsetAsync(scr.ptr, 0, (size_t)g.M * g.N * sizeof(double), st));
+    z.part = scr.ptr;
+    splitk_reduce_kernel<<<(unsigned)cdiv(g.M * g.N, 256), 256, 0, st>>>(z);
+    count_launch();
+    RH_LAUNCH_CHECK();
     return RHOSVD_OK;
   }
   // column edge: N % 128 leftover columns as one narrower segment (BN 32 / 64 / 96) so

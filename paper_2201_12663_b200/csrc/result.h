@@ -9,6 +9,7 @@ struct rhosvd_result {
   double* sigma[3] = {nullptr, nullptr, nullptr};  // r_l
   double* W[3] = {nullptr, nullptr, nullptr};      // r_l x Rp row-major (CP factors of the core)
   double* beta = nullptr;                          // r1 x r2 x r3, C order
+  bool beta_valid = true;                          // false on ranks != 0 with RHOSVD_F_ROOT_ONLY_CORE
   // rhosvd_c2t_host: pinned host copies of Z (ld ldz), sigma and beta
   double* hZ[3] = {nullptr, nullptr, nullptr};
   double* hsigma[3] = {nullptr, nullptr, nullptr};

@@ -45,6 +45,20 @@ int fail(int status, const std::string& msg) {
   return status;
 }
 
+int device_guard() {
+  static std::mutex mu;
+  static int pinned = -1;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(RHOSVD_ECUDA, std::string("cudaGetDevice: ") + cudaGetErrorString(e));
+  std::lock_guard<std::mutex> lk(mu);
+  if (pinned < 0) pinned = dev;
+  if (dev != pinned)
+    return fail(RHOSVD_EINVAL, "librhosvd serves one CUDA device per process (first used " +
+                                   std::to_string(pinned) + ", current " + std::to_string(dev) + ")");
+  return RHOSVD_OK;
+}
+
 int num_sms() {
   static const int s = [] {
     int dev = 0, v = 0;
@@ -640,6 +654,8 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     return (int64_t)std::ceil(rr);
   };
   int it_total = 0, itb = 0, guard = 0;
+  int need_last = 0;     // modelled iteration count of the last convergence test
+  bool capped = false;   // the last block stopped at max_iters before need_last
   int64_t r_est = rfix;
   while (true) {
     ++it_total;
@@ -676,7 +692,12 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     const double dr = std::max(d_h[rr - 1], 1e-300);
     const double rho = std::min(0.999, std::max(d_h[b - 1], 1e-300 * dr) / dr);
     const int need = std::max(2, (int)std::ceil(std::log(1e-7) / std::log(rho)));
-    if (itb >= std::min(need, std::max(2, o.max_iters))) break;
+    const int cap = std::max(2, o.max_iters);
+    if (itb >= std::min(need, cap)) {
+      need_last = need;
+      capped = need > cap;
+      break;
+    }
   }
   mo.iters = it_total;
   // block truncation: smallest b' >= r + p with d_b' <= 0.02 d_r (leading columns carry
@@ -725,6 +746,13 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
         fprintf(stderr, "[rhosvd dbg] mode %d refine model e0 %.2e rho %.3e -> %d steps\n", mode, e0, rho, nref);
     }
   }
+  // ENOCONV: the iteration cap stopped the subspace iteration before its
+  // modelled count, and the refinement steps (each contracts the subspace error by the
+  // same rate) cannot make up the difference: sin(theta_r) ~ rho^(itb + nref) > 1e-7.
+  if (capped && itb + nref < need_last)
+    return fail(RHOSVD_ENOCONV, "mode " + std::to_string(mode) + ": subspace iteration hit max_iters (" +
+                                    std::to_string(o.max_iters) + ") with " + std::to_string(need_last) +
+                                    " iterations needed for the block edge rate");
   for (int rs = 0;; ++rs) {
     // W = Z^T Uhat (b x Rp row-major == Rl x b col-major)
     RH_CHECK(mm(c, Rl, b, n, Uh, LDN, true, w.Z.p, LDN, true, w.W.p, Rp));
@@ -739,16 +767,14 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     ++mo.refines;
     c.tm->mark(PH_RR);
   }
-  // The rank rule must be met inside the block after the growth (rho = tail2[b] is the
-  // block's residual, ~1e-7 on cfg 4 against eps^2 T = 4.8e-6).  A miss is an anomaly -
-  // it exposed a pipeline race in the GEMM engine (fixed: mbar_arrive_after, see
-  // profiles/README.md r1z) - so it is reported on stderr and the final step is
-  // recomputed (single GPU only: with a communicator every rank would have to agree to
-  // redo the collectives).
+  // Final one-sided Rayleigh-Ritz, residual and rank.  The rank rule must be met inside
+  // the block (rho = ||Uhat - Z_b W_b||^2 is the out-of-block energy, ~1e-7 on cfg 4
+  // against eps^2 T = 4.8e-6): a miss means the block or the subspace did not converge,
+  // and the call fails with ENOCONV instead of returning a rank that violates the rule.
   double sel[4];
   double rho_h = 0.0;
-  for (int attempt = 0;; ++attempt) {
-    // final one-sided Rayleigh-Ritz: W W^T = P Lambda P^T (high relative accuracy Jacobi)
+  {
+    // W W^T = P Lambda P^T (high relative accuracy Jacobi)
     RH_CHECK(mm(c, b, b, Rl, w.W.p, Rp, true, w.W.p, Rp, true, w.S.p, ldb, nullptr, true));
     RH_CHECK(allreduce(c, w.S.p, ldb * b));
     TL().mark(mode, "W W^T", st);
@@ -779,15 +805,18 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
                            scal + 24 + 4 * mode, w.inv.p, st));
     RH_CHECK(d2h_wait(sel, scal + 24 + 4 * mode, 3 * sizeof(double), st));
     RH_CHECK(d2h_wait(&rho_h, scal + 16 + mode, sizeof(double), st));
-    if (sel[0] >= 0 || attempt >= 2 || (c.comm && c.comm->active())) break;
-    fprintf(stderr,
-            "[rhosvd] mode %d: rank rule not met inside the block (b %lld, rho %.6e, T %.6e, tail2 %.6e);"
-            " recomputing the final Rayleigh-Ritz step (attempt %d)\n",
-            mode, (long long)b, rho_h, T, sel[1], attempt + 1);
   }
   int64_t r = (int64_t)sel[0];
-  if (r < 0) {  // the block did not reach the threshold (should not happen after growth)
-    r = b;
+  // full space (b = min(n, R)): the tail beyond b is zero, so r = b is the rule's answer
+  // (the residual is rounding only; the oracle's rule also returns m when no r < m meets it)
+  if (r < 0 && b >= m) r = b;
+  if (r < 0) {
+    char msg[256];
+    snprintf(msg, sizeof msg,
+             "mode %d: rank rule not met inside the final block (b %lld, tail^2 %.6e > eps^2 T %.6e; "
+             "rho %.6e) - block growth or subspace iteration did not converge",
+             mode, (long long)b, sel[1], epsmode ? o.eps * o.eps * T : 0.0, rho_h);
+    return fail(RHOSVD_ENOCONV, msg);
   }
   mo.r = (int)r;
   mo.b = (int)b;
@@ -997,6 +1026,7 @@ int rhosvd_result_sigma(const rhosvd_result* r, int mode, const double** s, int6
 }
 int rhosvd_result_core(const rhosvd_result* r, const double** beta) {
   if (!r || !beta) return fail(RHOSVD_EINVAL, "bad args");
+  if (!r->beta_valid) return fail(RHOSVD_EINVAL, "RHOSVD_F_ROOT_ONLY_CORE: beta is on rank 0 only");
   *beta = r->beta;
   return RHOSVD_OK;
 }
@@ -1038,6 +1068,7 @@ struct BetaAR {
   rhosvd_comm* comm;
   double* beta;
   cudaStream_t cs;
+  bool root_only;  // RHOSVD_F_ROOT_ONLY_CORE: reduce to rank 0 instead of all-reduce
 };
 static int beta_chunk_allreduce(void* ctx, int, int64_t e0, int64_t e1, cudaStream_t s) {
   auto* b = (BetaAR*)ctx;
@@ -1049,7 +1080,8 @@ static int beta_chunk_allreduce(void* ctx, int, int64_t e0, int64_t e1, cudaStre
   cudaEventDestroy(ev);
   if (comm_trace()) fprintf(stderr, "[rhosvd comm] rank %d beta chunk [%lld, %lld)\n", b->comm->rank, (long long)e0,
                             (long long)e1);
-  return comm_allreduce(b->comm, b->beta + e0, e1 - e0, b->cs);
+  return b->root_only ? comm_reduce_root(b->comm, b->beta + e0, e1 - e0, b->cs)
+                     : comm_allreduce(b->comm, b->beta + e0, e1 - e0, b->cs);
 }
 
 static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_t n, int64_t Rl,
@@ -1226,20 +1258,30 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
   if (concurrent) {
     int dev = 0;
     RH_CUDA(cudaGetDevice(&dev));
-    std::unique_ptr<CommSched> sched;
-    std::thread comm_thread;
-    if (comm && comm->active()) {
-      sched.reset(new CommSched());
-      sched->comm = comm;
-      sched->dev = dev;
-      comm_thread = std::thread([&] { sched->run(); });
-    }
     cudaStream_t* ms = mode_streams();
     if (!ms) return fail(RHOSVD_ECUDA, "mode stream creation failed");
     cudaEvent_t ev0;
     RH_CUDA(cudaEventCreateWithFlags(&ev0, cudaEventDisableTiming));
     RH_CUDA(cudaEventRecord(ev0, st));
     for (int l = 0; l < 3; ++l) RH_CUDA(cudaStreamWaitEvent(ms[l], ev0, 0));
+    std::unique_ptr<CommSched> sched;
+    std::thread comm_thread;
+    // every return path below stops the comm thread: all modes marked finished, joined
+    struct CommJoin {
+      std::unique_ptr<CommSched>& s;
+      std::thread& t;
+      ~CommJoin() {
+        if (!t.joinable()) return;
+        for (int l = 0; l < 3; ++l) s->finish(l);
+        t.join();
+      }
+    } comm_join{sched, comm_thread};
+    if (comm && comm->active()) {
+      sched.reset(new CommSched());
+      sched->comm = comm;
+      sched->dev = dev;
+      comm_thread = std::thread([&] { sched->run(); });
+    }
     double mflops[3] = {0, 0, 0};
     int mlaunch[3] = {0, 0, 0};
     double mphase[3][16] = {{0}};
@@ -1468,7 +1510,12 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
   }
 
   // R-sharded (NCCL): the beta all-reduce overlaps the contraction chunk by chunk
-  BetaAR bar{comm, nullptr, nullptr};
+  // RHOSVD_F_ROOT_ONLY_CORE: beta is reduced to rank 0 only (the other ranks' beta holds
+  // their partial sums and the accessors refuse it)
+  const bool root_only = (o.flags & RHOSVD_F_ROOT_ONLY_CORE) && comm && comm->active();
+  const bool beta_here = !root_only || comm->rank == 0;
+  res->beta_valid = beta_here;
+  BetaAR bar{comm, nullptr, nullptr, root_only};
   bool chunked_ar = false;
   if (!chunks.done && total > 0 && comm && comm->active() && comm->kind == rhosvd_comm::NCCL) {
     cudaStream_t* ms = mode_streams();
@@ -1529,10 +1576,13 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
       RH_CUDA(cudaEventRecord(ev, bar.cs));
       RH_CUDA(cudaStreamWaitEvent(st, ev, 0));
       cudaEventDestroy(ev);
+    } else if (root_only) {
+      c.tm->mark(PH_COMM);
+      RH_CHECK(comm_reduce_root(comm, res->beta, total, st));
     } else {
       RH_CHECK(allreduce(c, res->beta, total));
     }
-    if (hin && (chunked_ar || !chunks.done)) RH_CHECK(beta_chunk_d2h(&bd, 0, 0, total, st));
+    if (hin && beta_here && (chunked_ar || !chunks.done)) RH_CHECK(beta_chunk_d2h(&bd, 0, 0, total, st));
     tm.mark(PH_CORE);
     RH_CHECK(k_sumsq(res->beta, total, w.part.p, w.scal.p + 12, st));
   } else {
@@ -1545,7 +1595,7 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
   RH_CUDA(cudaStreamSynchronize(st));
   if (cp) RH_CUDA(cudaStreamSynchronize(cp));
   RH_CUDA(cudaGetLastError());
-  rep.beta_norm = std::sqrt(bn2);
+  rep.beta_norm = beta_here ? std::sqrt(bn2) : std::nan("");
   double st1 = 0.0, st2 = 0.0;
   for (int l = 0; l < 3; ++l) {
     st1 += rep.tail[l];
@@ -1611,6 +1661,7 @@ int rhosvd_result_host_sigma(const rhosvd_result* r, int mode, const double** s,
 }
 int rhosvd_result_host_core(const rhosvd_result* r, const double** beta) {
   if (!r || !beta) return fail(RHOSVD_EINVAL, "bad args");
+  if (!r->beta_valid) return fail(RHOSVD_EINVAL, "RHOSVD_F_ROOT_ONLY_CORE: beta is on rank 0 only");
   if ((int64_t)r->ranks[0] * r->ranks[1] * r->ranks[2] > 0 && !r->hbeta)
     return fail(RHOSVD_EINVAL, "no host outputs (use rhosvd_c2t_host)");
   *beta = r->hbeta;
@@ -1636,6 +1687,7 @@ static int c2t_entry(const double* U1, const double* U2, const double* U3, int64
     return fail(RHOSVD_EINVAL, "unknown rank_mode");
   }
   if (n > 16384) return fail(RHOSVD_EINVAL, "n > 16384 not supported");
+  RH_CHECK(device_guard());
   std::lock_guard<std::mutex> lk(g_mu);
   cudaStream_t st = (cudaStream_t)stream;
   static bool pool_set = false;
@@ -1669,6 +1721,7 @@ extern "C" {
 int rhosvd_gram(const double* U, int64_t ldu, int64_t n, int64_t R, double* G, int64_t ldg, rhosvd_stream stream) {
   if (!U || !G || n < 1 || R < 0 || ldu < n || ldg < n) return fail(RHOSVD_EINVAL, "bad args");
   if ((ldu & 1) || ((uintptr_t)U & 15)) return fail(RHOSVD_EINVAL, "gram: ldu must be even, U 16B-aligned");
+  RH_CHECK(device_guard());
   std::lock_guard<std::mutex> lk(g_mu);
   GemmArgs g;
   g.M = n; g.N = n; g.K = R; g.A = U; g.lda = ldu; g.a_k = false; g.B = U; g.ldb = ldu; g.b_k = false;
@@ -1682,6 +1735,7 @@ int rhosvd_dgemm(char ta, char tb, int64_t M, int64_t N, int64_t K, double alpha
   if (!A || !B || !C || M < 0 || N < 0 || K < 0) return fail(RHOSVD_EINVAL, "bad args");
   if ((lda & 1) || (ldb & 1) || ((uintptr_t)A & 15) || ((uintptr_t)B & 15))
     return fail(RHOSVD_EINVAL, "dgemm: lda/ldb must be even and A/B 16B-aligned");
+  RH_CHECK(device_guard());
   std::lock_guard<std::mutex> lk(g_mu);
   GemmArgs g;
   g.M = M; g.N = N; g.K = K; g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc;
@@ -1697,6 +1751,7 @@ int rhosvd_dgemm(char ta, char tb, int64_t M, int64_t N, int64_t K, double alpha
 int rhosvd_syevj(int64_t b, double* A, int64_t lda, double* lambda, double* V, int64_t ldv, double tol,
                  int32_t* sweeps_out, rhosvd_stream stream) {
   if (!A || !lambda || !V || b < 0 || lda < b || ldv < b) return fail(RHOSVD_EINVAL, "bad args");
+  RH_CHECK(device_guard());
   std::lock_guard<std::mutex> lk(g_mu);
   int sw = 0;
   RH_CHECK(syevj(b, A, lda, lambda, V, ldv, tol > 0 ? tol : 1e-15, 1e-300, 80, WS().mw[0].dws, (cudaStream_t)stream, &sw));
@@ -1707,6 +1762,7 @@ int rhosvd_syevj(int64_t b, double* A, int64_t lda, double* lambda, double* V, i
 int rhosvd_chol_inv(int64_t b, const double* S, int64_t lds, double shift, double* Bp, int64_t ldb,
                     rhosvd_stream stream) {
   if (!S || !Bp || b < 0 || lds < b || ldb < b || !(shift >= 0.0)) return fail(RHOSVD_EINVAL, "bad args");
+  RH_CHECK(device_guard());
   std::lock_guard<std::mutex> lk(g_mu);
   return chol_inv_scaled(b, S, lds, shift, Bp, ldb, WS().mw[0].dws, (cudaStream_t)stream);
 }
@@ -1717,6 +1773,7 @@ int rhosvd_core(const double* W1, const double* W2, const double* W3, int64_t ld
     return fail(RHOSVD_EINVAL, "bad args");
   if ((ldw & 1) || ((uintptr_t)W1 & 15) || ((uintptr_t)W2 & 15) || ((uintptr_t)W3 & 15))
     return fail(RHOSVD_EINVAL, "core: ldw must be even, W 16B-aligned");
+  RH_CHECK(device_guard());
   std::lock_guard<std::mutex> lk(g_mu);
   cudaStream_t st = (cudaStream_t)stream;
   Workspace& w = WS();

@@ -707,6 +707,8 @@ int rhosvd_t2c(const rhosvd_result* res, double eps_rel, rhosvd_stream stream, r
   if (!out) return fail(RHOSVD_EINVAL, "out is null");
   *out = nullptr;
   if (!res || !(eps_rel >= 0.0 && eps_rel < 1.0)) return fail(RHOSVD_EINVAL, "t2c: need a result and 0 <= eps < 1");
+  RH_CHECK(device_guard());
+  if (!res->beta_valid) return fail(RHOSVD_EINVAL, "t2c: RHOSVD_F_ROOT_ONLY_CORE result on a rank != 0 holds no core");
   cudaStream_t st = (cudaStream_t)stream;
   const int r1 = res->ranks[0], r2 = res->ranks[1], r3 = res->ranks[2];
   auto* cp = new rhosvd_cp();

@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "librhosvd.so")
 
 RHOSVD_OK = 0
 RHOSVD_FIXED_RANK, RHOSVD_EPS = 0, 1
-RHOSVD_F_SIGN_FIX, RHOSVD_F_KEEP_W = 1, 2
+RHOSVD_F_SIGN_FIX, RHOSVD_F_KEEP_W, RHOSVD_F_ROOT_ONLY_CORE = 1, 2, 4
 STATUS = {0: "OK", -1: "EINVAL", -2: "ENONFINITE", -3: "ENOCONV", -4: "ENOMEM",
           -5: "ECUDA", -6: "ENCCL", -7: "EMISMATCH"}
 PHASES = ["normalize", "gram", "eigensolve", "rr_refine", "residual_rank", "projection",
@@ -139,7 +139,7 @@ def _need_cuda_f64(t, name):
 
 
 def make_opts(eps=None, ranks=None, oversample=16, block0=0, max_iters=30, refine_steps=1,
-              seed=12345, sign_fix=True):
+              seed=12345, sign_fix=True, root_only_core=False):
     o = Opts()
     lib().rhosvd_opts_default(C.byref(o))
     if (eps is None) == (ranks is None):
@@ -156,7 +156,7 @@ def make_opts(eps=None, ranks=None, oversample=16, block0=0, max_iters=30, refin
     o.max_iters = int(max_iters)
     o.refine_steps = int(refine_steps)
     o.seed = int(seed)
-    o.flags = RHOSVD_F_SIGN_FIX if sign_fix else 0
+    o.flags = (RHOSVD_F_SIGN_FIX if sign_fix else 0) | (RHOSVD_F_ROOT_ONLY_CORE if root_only_core else 0)
     return o
 
 
@@ -164,9 +164,10 @@ def make_opts(eps=None, ranks=None, oversample=16, block0=0, max_iters=30, refin
 class Comm:
     """Wraps rhosvd_comm (NCCL or host-callback all-reduce)."""
 
-    def __init__(self, handle, keep=None):
+    def __init__(self, handle, keep=None, rank=0, world=1):
         self.handle = handle
         self._keep = keep  # keep ctypes callback alive
+        self.rank, self.world = rank, world
 
     def close(self):
         if self.handle:
@@ -194,7 +195,7 @@ class Comm:
         raw = bytes(t.cpu().tolist())
         h = C.c_void_p()
         _check(lib().rhosvd_comm_init_nccl(raw, world, rank, C.byref(h)))
-        return Comm(h)
+        return Comm(h, rank=rank, world=world)
 
     @staticmethod
     def callback(group=None):
@@ -224,7 +225,7 @@ class Comm:
         cb = ALLREDUCE_FN(_ar)
         h = C.c_void_p()
         _check(lib().rhosvd_comm_init_callback(cb, None, world, rank, C.byref(h)))
-        return Comm(h, keep=cb)
+        return Comm(h, keep=cb, rank=rank, world=world)
 
 
 _cudart = None
@@ -420,9 +421,12 @@ def c2t(U, xi, eps=None, ranks=None, comm: Comm | None = None, stream=None, keep
                 wf = _wrap_dev(wp.value, rl * int(ldw.value), dev) if rl else torch.empty(0, dtype=torch.float64, device=dev)
                 Ws.append(wf.view(rl, int(ldw.value))[:, :Rl] if rl else torch.empty(0, Rl, dtype=torch.float64, device=dev))
         bp = C.c_void_p()
-        _check(L.rhosvd_result_core(h, C.byref(bp)))
         tot = ranks_[0] * ranks_[1] * ranks_[2]
-        beta = _wrap_dev(bp.value, tot, dev).view(*ranks_) if tot else torch.zeros(*ranks_, dtype=torch.float64, device=dev)
+        if opts.flags & RHOSVD_F_ROOT_ONLY_CORE and comm is not None and comm.rank != 0:
+            beta = None  # reduced to rank 0 only
+        else:
+            _check(L.rhosvd_result_core(h, C.byref(bp)))
+            beta = _wrap_dev(bp.value, tot, dev).view(*ranks_) if tot else torch.zeros(*ranks_, dtype=torch.float64, device=dev)
         rep = Report()
         _check(L.rhosvd_result_report(h, C.byref(rep)))
         return Result(ranks=ranks_, Z=Zs, sigma=sig, beta=beta, W=Ws if keep_w else None,

@@ -35,6 +35,9 @@ for p in (make_random_params(70, 517, seed=23, eps=1e-7), make_params(2)):
     assert torch.equal(got.beta, ref.beta)
     for a, b in zip(got.Z, ref.Z):
         assert torch.equal(a, b)
+    # RHOSVD_F_ROOT_ONLY_CORE: ncclReduce to rank 0 (a world-1 reduce is an identity)
+    ro = rhosvd.c2t([U1, U2, U3], xi, eps=p.eps, ranks=p.ranks, comm=comm, keep_w=False, root_only_core=True)
+    assert torch.equal(ro.beta, ref.beta)
     hU = [u.cpu().pin_memory() for u in (U1, U2, U3)]
     h = rhosvd.c2t_host(hU, xi.cpu().pin_memory(), eps=p.eps, ranks=p.ranks, comm=comm)
     assert torch.equal(h.beta, ref.beta.cpu())

@@ -43,7 +43,7 @@ def _params(case):
     return make_random_params(c["n"], c["R"], seed=c["seed"], eps=c["eps"])
 
 
-def _worker(rank, world, port, case, q, serial=False):
+def _worker(rank, world, port, case, q, serial=False, extra=None):
     import torch.distributed as dist
     if serial:  # per-mode eigensolves one after another instead of concurrent + comm thread
         os.environ["RHOSVD_SERIAL_MODES"] = "1"
@@ -57,17 +57,18 @@ def _worker(rank, world, port, case, q, serial=False):
         k0, k1 = shard_bounds(p.R, world, rank)
         U1, U2, U3, xi = make_config(p, k0, k1, backend="torch", device=torch.device("cuda:0"))
         comm = rhosvd.Comm.callback()
-        res = rhosvd.c2t([U1, U2, U3], xi, eps=p.eps, ranks=p.ranks, comm=comm, keep_w=False)
+        res = rhosvd.c2t([U1, U2, U3], xi, eps=p.eps, ranks=p.ranks, comm=comm, keep_w=False, **(extra or {}))
         comm.close()
         q.put(dict(rank=rank, ranks=list(res.ranks), sigma=[s.cpu().numpy() for s in res.sigma],
-                   Z=[z.cpu().numpy() for z in res.Z], beta=res.beta.cpu().numpy(),
+                   Z=[z.cpu().numpy() for z in res.Z], beta=None if res.beta is None else res.beta.cpu().numpy(),
                    R_global=res.report["R_global"], trace=res.report["trace"]))
     finally:
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case,serial", [("random", False), ("cfg2", False), ("random", True)])
-def test_r_sharded_world2_one_gpu(case, serial):
+@pytest.mark.parametrize("case,serial,extra", [("random", False, None), ("cfg2", False, None), ("random", True, None),
+                                               ("random", False, {"root_only_core": True})])
+def test_r_sharded_world2_one_gpu(case, serial, extra):
     import torch.multiprocessing as mp
     from oracle import rhosvd as oracle_rhosvd, sigma_rel_err, tucker_diff
     from paper_2201_12663_b200 import rhosvd
@@ -76,7 +77,7 @@ def test_r_sharded_world2_one_gpu(case, serial):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
-    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q, serial)) for r in range(2)]
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q, serial, extra)) for r in range(2)]
     for pr in procs:
         pr.start()
     out = {}
@@ -92,7 +93,10 @@ def test_r_sharded_world2_one_gpu(case, serial):
     assert g0["ranks"] == g1["ranks"]
     for l in range(3):  # every rank holds bit-identical outputs (identical reduced inputs)
         assert np.array_equal(g0["sigma"][l], g1["sigma"][l])
-    assert np.array_equal(g0["beta"], g1["beta"])
+    if extra and extra.get("root_only_core"):  # RHOSVD_F_ROOT_ONLY_CORE: the core lives on rank 0 only
+        assert g1["beta"] is None and g0["beta"] is not None
+    else:
+        assert np.array_equal(g0["beta"], g1["beta"])
 
     U1, U2, U3, xi = make_config(p)
     o = oracle_rhosvd([U1, U2, U3], xi, eps=p.eps, ranks=p.ranks)
