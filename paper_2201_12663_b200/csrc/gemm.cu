@@ -37,6 +37,9 @@ struct GParams {
   int splits, kchunk;
   int tiles_m, tiles_n, tiles, items;
   int n_off;      // first output column of this launch (column segments)
+  int nbatch, per_batch;  // batched form: items = nbatch * per_batch, per_batch = splits * tiles
+  int a_koff, b_koff;     // k-coordinate shift of batch b's operands (b * koff)
+  int64_t c_bstride;      // C offset of batch b (doubles)
   int stages;
   uint32_t a_bytes, stage_bytes, tx_bytes;
   uint32_t b_bytes;  // one k-slab of B (the stage holds KS slabs of A, then KS of B)
@@ -66,16 +69,19 @@ __global__ void __launch_bounds__(GTHREADS, 1)
     }
   };
   // producer cursor over this CTA's k-slab stream
-  int pit = blockIdx.x, pk = 0, pkend = 0, pm = 0, pn = 0;
+  int pit = blockIdx.x, pk = 0, pkend = 0, pm = 0, pn = 0, pka = 0, pkb = 0;
   auto set_item = [&]() {
     if (pit >= p.items) return;
-    const int split = pit / p.tiles;
+    const int bt = pit / p.per_batch, rit = pit - bt * p.per_batch;
+    const int split = rit / p.tiles;
     int tm, tn;
-    tile_of(pit % p.tiles, tm, tn);
+    tile_of(rit % p.tiles, tm, tn);
     pm = tm * BM;
     pn = p.n_off + tn * BN;
     pk = split * p.kchunk;
     pkend = min(p.K, pk + p.kchunk);
+    pka = bt * p.a_koff;
+    pkb = bt * p.b_koff;
   };
   auto issue_next = [&](int stage) {
     if (pit >= p.items) return;
@@ -86,10 +92,10 @@ __global__ void __launch_bounds__(GTHREADS, 1)
       unsigned char* sa_ = st + j * p.a_bytes;
       unsigned char* sb_ = st + KS * p.a_bytes + j * p.b_bytes;
       const int kk = pk + GBK * j;
-      if (AK) tma_load_2d(sa_, &tA, kk, pm, &full[stage]);
-      else tma_load_2d(sa_, &tA, pm, kk, &full[stage]);
-      if (BKM) tma_load_2d(sb_, &tB, kk, pn, &full[stage]);
-      else tma_load_2d(sb_, &tB, pn, kk, &full[stage]);
+      if (AK) tma_load_2d(sa_, &tA, kk + pka, pm, &full[stage]);
+      else tma_load_2d(sa_, &tA, pm, kk + pka, &full[stage]);
+      if (BKM) tma_load_2d(sb_, &tB, kk + pkb, pn, &full[stage]);
+      else tma_load_2d(sb_, &tB, pn, kk + pkb, &full[stage]);
     }
     pk += GBK * KS;
     if (pk >= pkend) {
@@ -132,9 +138,11 @@ __global__ void __launch_bounds__(GTHREADS, 1)
   uint32_t cs = 0, cph = 0;
   const uint32_t nst = (uint32_t)p.stages;
   for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
-    const int split = it / p.tiles;
+    const int bt = it / p.per_batch, rit = it - bt * p.per_batch;
+    const int split = rit / p.tiles;
     int tm, tn;
-    tile_of(it % p.tiles, tm, tn);
+    tile_of(rit % p.tiles, tm, tn);
+    double* const Cb = p.C + bt * p.c_bstride;
     const int m0 = tm * BM, n0 = p.n_off + tn * BN;
     const int kbeg = split * p.kchunk, kend = min(p.K, kbeg + p.kchunk);
     double acc[FM][FN][2];
@@ -200,7 +208,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
       continue;
     }
     if (p.splits > 1) {
-      double* out = p.part + (int64_t)split * p.M * p.N;
+      double* out = p.part + ((int64_t)bt * p.splits + split) * p.M * p.N;
 #pragma unroll
       for (int i = 0; i < FM; ++i)
 #pragma unroll
@@ -223,10 +231,10 @@ __global__ void __launch_bounds__(GTHREADS, 1)
             double v = p.alpha * acc[i][j][h];
             if (p.cs) v *= p.cs[n];
             if (p.rs) v *= p.rs[m];
-            double* c = p.C + (int64_t)n * p.ldc + m;
+            double* c = Cb + (int64_t)n * p.ldc + m;
             if (p.beta != 0.0) v = fma(p.beta, *c, v);
             *c = v;
-            if (p.upper && m < n) p.C[(int64_t)m * p.ldc + n] = v;  // mirror (M == N)
+            if (p.upper && m < n) Cb[(int64_t)m * p.ldc + n] = v;  // mirror (M == N)
           }
         }
   }
@@ -236,17 +244,20 @@ __global__ void __launch_bounds__(GTHREADS, 1)
 __global__ void splitk_reduce_kernel(GParams p) {
   int64_t idx = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   int64_t total = (int64_t)p.M * p.N;
-  if (idx >= total) return;
+  if (idx >= total * p.nbatch) return;
+  const int bt = (int)(idx / total);
+  idx -= bt * total;
   int m = (int)(idx % p.M), n = (int)(idx / p.M);
   int sm = m, sn = n;
   if (p.upper && m > n) { sm = n; sn = m; }  // read the computed upper entry
   int64_t src = (int64_t)sn * p.M + sm;
+  const double* part = p.part + (int64_t)bt * p.splits * total;
   double s = 0.0;
-  for (int k = 0; k < p.splits; ++k) s += p.part[(int64_t)k * total + src];
+  for (int k = 0; k < p.splits; ++k) s += part[(int64_t)k * total + src];
   double v = p.alpha * s;
   if (p.cs) v *= p.cs[n];
   if (p.rs) v *= p.rs[m];
-  double* c = p.C + (int64_t)n * p.ldc + m;
+  double* c = p.C + bt * p.c_bstride + (int64_t)n * p.ldc + m;
   if (p.beta != 0.0) v = fma(p.beta, *c, v);
   *c = v;
 }
@@ -299,10 +310,12 @@ template <int BM, int BN, bool AK, bool BKM, int KS>
 static int launch_cfg(const GemmArgs& g, GParams gp, cudaStream_t st) {
   auto kern = tma_gemm_kernel<BM, BN, AK, BKM, KS>;
   CUtensorMap tA, tB;
-  if (AK) RH_CHECK(make_tmap_2d(&tA, g.A, g.M, g.K, g.lda, GBK, BM, true));
-  else RH_CHECK(make_tmap_2d(&tA, g.A, g.K, g.M, g.lda, BM + 8, GBK, false));
-  if (BKM) RH_CHECK(make_tmap_2d(&tB, g.B, g.N, g.K, g.ldb, GBK, BN, true));
-  else RH_CHECK(make_tmap_2d(&tB, g.B, g.K, g.N, g.ldb, BN + 8, GBK, false));
+  // batched: the k-extent of the maps spans every batch (batch b at k + b * koff)
+  const int64_t KA = g.K + (int64_t)(gp.nbatch - 1) * gp.a_koff, KB = g.K + (int64_t)(gp.nbatch - 1) * gp.b_koff;
+  if (AK) RH_CHECK(make_tmap_2d(&tA, g.A, g.M, KA, g.lda, GBK, BM, true));
+  else RH_CHECK(make_tmap_2d(&tA, g.A, KA, g.M, g.lda, BM + 8, GBK, false));
+  if (BKM) RH_CHECK(make_tmap_2d(&tB, g.B, g.N, KB, g.ldb, GBK, BN, true));
+  else RH_CHECK(make_tmap_2d(&tB, g.B, KB, g.N, g.ldb, BN + 8, GBK, false));
   const uint32_t a_box = AK ? BM * 128u : (BM + 8) * GBK * 8u;
   const uint32_t b_box = BKM ? BN * 128u : (BN + 8) * GBK * 8u;
   gp.a_bytes = (uint32_t)round_up(a_box, 1024);
@@ -343,20 +356,56 @@ static int launch_edge(int bn, const GemmArgs& g, const GParams& gp, cudaStream_
   }
 }
 
+static bool gemm_big(int64_t M, int64_t N, int64_t K) {
+  return (cdiv(M, 128) * cdiv(N, 128) >= num_sms() / 2) || (M >= 128 && N >= 128 && K >= 2048);
+}
+
+int gemm_batch_splits(int64_t M, int64_t N, int64_t K, bool upper, int nb) {
+  // the fewest waves per unit of work over 1..8 K-splits (each split >= 2048 of K; a split
+  // costs one more M x N partial per batch, ~0.3 % here).  cfg 4's three 2048^2 Grams: 408
+  // upper tiles -> 5 splits = 2040 items on 148 SMs, 98.4 % of the last wave busy (one
+  // 136-tile Gram per launch: 92 %)
+  const int sms = num_sms();
+  const int BT = gemm_big(M, N, K) ? 128 : 64;
+  const int64_t tn = cdiv(N, BT), tiles = upper ? tn * (tn + 1) / 2 : cdiv(M, BT) * tn;
+  const int64_t tot = (int64_t)nb * tiles;
+  double best = 1e30;
+  int splits = 1;
+  for (int s2 = 1; s2 <= 8; ++s2) {
+    if (s2 > 1 && K / s2 < 2048) break;
+    const double cost = (double)cdiv(tot * s2, sms) * sms / ((double)tot * s2) * (1.0 + 0.003 * (s2 - 1));
+    if (cost < best * 0.999) {
+      best = cost;
+      splits = s2;
+    }
+  }
+  return splits;
+}
+
 int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
   if (g.M <= 0 || g.N <= 0) return RHOSVD_OK;
   if (g.M > INT32_MAX || g.N > INT32_MAX || g.K > INT32_MAX)
     return fail(RHOSVD_EINVAL, "gemm: dimension exceeds int32");
   if (g.upper_sym && g.M != g.N) return fail(RHOSVD_EINVAL, "gemm: upper_sym needs M == N");
   if (g.epi == EPI_RESID && g.K <= 0) return fail(RHOSVD_EINVAL, "gemm: residual needs K > 0");
+  const int nb = std::max(1, g.batch);
+  if (nb > 1) {
+    if (g.epi == EPI_RESID) return fail(RHOSVD_EINVAL, "gemm: batched form has no residual epilogue");
+    if (g.K <= 0 || g.K % 32 || g.a_koff % 32 || g.b_koff % 32 || g.a_koff < g.K || g.b_koff < g.K)
+      return fail(RHOSVD_EINVAL, "gemm: batched K / k offsets must be multiples of 32 with koff >= K");
+  }
   GParams gp{};
   gp.M = (int)g.M; gp.N = (int)g.N; gp.K = (int)std::max<int64_t>(g.K, 0);
+  gp.nbatch = nb;
+  gp.a_koff = (int)g.a_koff;
+  gp.b_koff = (int)g.b_koff;
+  gp.c_bstride = g.c_bstride;
   gp.C = g.C; gp.ldc = g.ldc; gp.alpha = g.alpha; gp.beta = g.beta; gp.cs = g.col_scale; gp.rs = g.row_scale;
   gp.upper = g.upper_sym ? 1 : 0; gp.epi = g.epi; gp.D = g.D; gp.ldd = g.ldd;
 
   // tile choice: 128 x 128 when there is enough output to fill the GPU
   const int sms = num_sms();
-  const bool big = (cdiv(g.M, 128) * cdiv(g.N, 128) >= sms / 2) || (g.M >= 128 && g.N >= 128 && g.K >= 2048);
+  const bool big = gemm_big(g.M, g.N, g.K);
   const int BT = big ? 128 : 64;
   const int tm = (int)cdiv(g.M, BT), tn = (int)cdiv(g.N, BT);
   gp.tiles_m = tm;
@@ -365,6 +414,7 @@ int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
 
   int splits = g.splits;
   if (g.epi == EPI_RESID) splits = 1;
+  if (splits <= 0 && nb > 1) splits = gemm_batch_splits(g.M, g.N, g.K, g.upper_sym, nb);
   if (splits <= 0) {
     // persistent grid: enough work items for every SM (~2 items each), splits >= 256 of K
     splits = 1;
@@ -390,13 +440,14 @@ int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
   splits = (int)std::max<int64_t>(1, cdiv(std::max<int64_t>(g.K, 1), kchunk));
   gp.splits = splits;
   gp.kchunk = kchunk;
-  gp.items = gp.tiles * splits;
+  gp.per_batch = gp.tiles * splits;
+  gp.items = gp.per_batch * nb;
 
   if (g.epi == EPI_RESID) {
     RH_CHECK(scr.ensure((size_t)gp.items * (GTHREADS / 32), st));
     gp.part = scr.ptr;
   } else if (splits > 1) {
-    RH_CHECK(scr.ensure((size_t)splits * g.M * g.N, st));
+    RH_CHECK(scr.ensure((size_t)nb * splits * g.M * g.N, st));
     gp.part = scr.ptr;
   }
   if (g.K <= 0) {  // empty contraction: C = beta C
@@ -422,8 +473,8 @@ int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
   }();
   const int64_t rem = g.N % 128;
   const int ebn = (int)round_up(rem, 32);
-  bool use_edge = big && edge_on && !g.upper_sym && g.epi != EPI_RESID && gemm_ks() == 2 && g.N > 128 && rem > 0 &&
-                  ebn < 128;
+  bool use_edge = big && edge_on && nb == 1 && !g.upper_sym && g.epi != EPI_RESID && gemm_ks() == 2 && g.N > 128 &&
+                  rem > 0 && ebn < 128;
   if (use_edge) {
     // waves of 128-tile time: the two launches each end on their own partial wave, so the
     // edge only pays when it removes more padding than it adds tail (an edge tile costs
@@ -437,13 +488,13 @@ int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
     GParams g1 = gp;
     g1.tiles_n = (int)(g.N / 128);
     g1.tiles = tm * g1.tiles_n;
-    g1.items = g1.tiles * splits;
+    g1.per_batch = g1.items = g1.tiles * splits;
     g1.n_off = 0;
     RH_CHECK((launch_layout<128, 128>(g, g1, st)));
     GParams g2 = gp;
     g2.tiles_n = 1;
     g2.tiles = tm;
-    g2.items = g2.tiles * splits;
+    g2.per_batch = g2.items = g2.tiles * splits;
     g2.n_off = (int)(g.N - rem);
     RH_CHECK(launch_edge(ebn, g, g2, st));
   } else if (big) {
@@ -457,12 +508,12 @@ int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
     count_launch();
     RH_LAUNCH_CHECK();
   } else if (splits > 1) {
-    int64_t total = g.M * g.N;
+    int64_t total = g.M * g.N * nb;
     splitk_reduce_kernel<<<(unsigned)cdiv(total, 256), 256, 0, st>>>(gp);
     count_launch();
     RH_LAUNCH_CHECK();
   }
-  if (flops_acc) *flops_acc += 2.0 * (double)g.M * (double)g.N * (double)g.K * (g.upper_sym ? 0.5 : 1.0);
+  if (flops_acc) *flops_acc += 2.0 * nb * (double)g.M * (double)g.N * (double)g.K * (g.upper_sym ? 0.5 : 1.0);
   return RHOSVD_OK;
 }
 

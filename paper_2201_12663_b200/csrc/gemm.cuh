@@ -33,6 +33,13 @@ struct GemmArgs {
   int64_t ldd = 0;
   double* resid_out = nullptr;        // EPI_RESID: one double (device), overwritten
   int splits = 0;                     // 0 = auto
+  // Batched form (one persistent launch over `batch` independent GEMMs, e.g. the three
+  // modes' Grams): batch b reads op(A) / op(B) at k-coordinates shifted by b * a_koff /
+  // b * b_koff (the k-extents must lie back to back in one allocation; K and the k
+  // offsets are multiples of 32 so no k-stage straddles two batches) and writes C +
+  // b * c_bstride.  Not for EPI_RESID.
+  int batch = 1;
+  int64_t a_koff = 0, b_koff = 0, c_bstride = 0;
 };
 
 // Scratch for split-K partials (grown on demand, stream-ordered).
@@ -44,5 +51,9 @@ struct Scratch {
 };
 
 int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc = nullptr);
+// K-split count the batched form picks for `nb` GEMMs of M x N x K (upper: symmetric
+// upper tiles).  A single GEMM called with this `splits` and the same K sums every output
+// element in the same order as its batch slot (bitwise identical results).
+int gemm_batch_splits(int64_t M, int64_t N, int64_t K, bool upper, int nb);
 
 }  // namespace rhosvd

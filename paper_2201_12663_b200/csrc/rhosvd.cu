@@ -1136,7 +1136,9 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
   tm.mark(PH_NORM);
   const int world = comm ? comm->world : 1;
   const int64_t LDN = round_up(n, 16);
-  const int64_t Rp = round_up(std::max<int64_t>(Rl, 1), 16);
+  // Rp: multiple of 32 (one GEMM k-stage), so the batched Gram's modes start on stage
+  // boundaries; padding columns of Uhat are zero
+  const int64_t Rp = round_up(std::max<int64_t>(Rl, 1), 32);
   res->n = n;
   res->ldz = LDN;
   res->Rl = Rl;
@@ -1183,10 +1185,20 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
   cudaEventCreate(&g0);
   cudaEventCreate(&g1);
   double* Uh[3];
+  // per-mode Gram (host-input paths, where mode l's Gram starts as soon as U_l lands):
+  // K = Rp and the batched form's split count, so every entry is summed exactly as in the
+  // one-launch batched Gram of the device-input path (bitwise identical G)
+  const int gram_splits = gemm_batch_splits(n, n, Rp, true, 3);
+  auto gram_args = [&](int l) {
+    GemmArgs g;
+    g.M = n; g.N = n; g.K = Rp; g.A = Uh[l]; g.lda = LDN; g.a_k = false; g.B = Uh[l]; g.ldb = LDN; g.b_k = false;
+    g.C = w.G.p + (size_t)l * LDN * LDN; g.ldc = LDN; g.upper_sym = true; g.splits = gram_splits;
+    return g;
+  };
   auto gram = [&](int l) -> int {
     double* G = w.G.p + (size_t)l * LDN * LDN;
     if (Rl > 0) {
-      RH_CHECK(mm(c, n, n, Rl, Uh[l], LDN, false, Uh[l], LDN, false, G, LDN, nullptr, true));
+      RH_CHECK(gemm(gram_args(l), c.m ? c.m->gsc : w.gsc, c.st, &c.flops));
     } else {
       RH_CUDA(cudaMemsetAsync(G, 0, (size_t)LDN * LDN * sizeof(double), st));
     }
@@ -1237,8 +1249,17 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
   // ---- S2 Gram (K1), all three modes, then all-reduce
   tm.mark(PH_GRAM);
   if (!early_gram) {
+    // the three modes' Grams as ONE persistent launch (batched GEMM: mode l reads Uhat at
+    // k + l Rp, writes G + l LDN^2): one wave schedule over 3x the tiles instead of three
+    // launches each ending on a partial wave
     cudaEventRecord(g0, st);
-    for (int l = 0; l < 3; ++l) RH_CHECK(gram(l));
+    if (Rl > 0) {
+      GemmArgs g = gram_args(0);
+      g.batch = 3; g.a_koff = g.b_koff = Rp; g.c_bstride = LDN * LDN;
+      RH_CHECK(gemm(g, w.gsc, st, &c.flops));
+    } else {
+      for (int l = 0; l < 3; ++l) RH_CHECK(gram(l));
+    }
     cudaEventRecord(g1, st);
   }
   RH_CHECK(allreduce(c, w.G.p, 3 * LDN * LDN));
@@ -1317,8 +1338,7 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
       RH_CUDA(cudaEventRecord(evN[l], ls));
       sig.fire();
       RH_CUDA(cudaEventRecord(evG[l][0], ls));
-      RH_CHECK(mm(cl, n, n, Rl, Uh[l], LDN, false, Uh[l], LDN, false, w.G.p + (size_t)l * LDN * LDN, LDN, nullptr,
-                  true));
+      RH_CHECK(gemm(gram_args(l), cl.m->gsc, ls, &cl.flops));
       RH_CUDA(cudaEventRecord(evG[l][1], ls));
       TL().mark(l, "Gram", ls);
       double tl = 0.0;
