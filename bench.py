@@ -42,6 +42,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--cpu-sample", type=int, default=0, help="terms in the oracle sample (0 = auto)")
+    ap.add_argument("--cpu-full", action="store_true", help="time the oracle on the FULL configuration (minutes)")
+    ap.add_argument("--cpu-only", action="store_true", help="only the cpu_baseline leg (writes its JSON)")
     ap.add_argument("--report", default="", help="write per-phase report JSON here (rank 0)")
     return ap.parse_args()
 
@@ -119,21 +121,74 @@ def fp64_peak():
 
 
 # ---------------------------------------------------------------- oracle sample (cpu_baseline / reference arm)
-def oracle_sample(cfg, sample_terms):
-    import numpy as np  # noqa: F401
+def oracle_ranks(cfg):
+    """The full problem's eps-ranks as the ORACLE found them (tests/golden/oracle_cfg{k}.json,
+    written by tools/make_oracle_fixtures.py from oracle/ only); None if not recorded."""
+    try:
+        return tuple(json.load(open(os.path.join(ROOT, "tests", "golden", f"oracle_cfg{cfg}.json")))["ranks"])
+    except Exception:
+        return None
+
+
+def oracle_sample(cfg, sample_terms, full=False):
+    """Time the CPU oracle (oracle.rhosvd as it stands) on config `cfg`.
+
+    full=False: the first `sample_terms` terms with the ranks FIXED to the full problem's
+    oracle eps-ranks, so the per-term work (the core's 2 r1 r2 r3 FLOP per term, 96 % of
+    cfg 4) matches the full configuration; an eps-mode run on a sample would pick smaller
+    ranks (cfg 4, 4000 terms: [499, 501, 502]) and about half the per-term work.
+    Returns (terms, seconds, ranks, per-phase seconds, how)."""
     from oracle import rhosvd as oracle_rhosvd
     from workloads import make_config, make_params
     p = make_params(cfg)
-    Rs = min(p.R, sample_terms)
+    Rs = p.R if full else min(p.R, sample_terms)
     U1, U2, U3, xi = make_config(p, 0, Rs)
+    ranks, eps = p.ranks, p.eps
+    how = "eps mode (the configuration's own rule)" if p.eps is not None else "the configuration's fixed ranks"
+    # untimed tiny oracle call: LAPACK's first-call set-up (~1 s) is not the oracle's work
+    from workloads import make_random_params
+    q = make_random_params(96, 300, seed=1, ranks=(3, 3, 3))  # large enough for threaded BLAS
+    oracle_rhosvd(list(make_config(q)[:3]), make_config(q)[3], ranks=q.ranks)
+    if not full and Rs < p.R and p.eps is not None and oracle_ranks(cfg):
+        ranks, eps = oracle_ranks(cfg), None
+        how = f"ranks fixed to the full problem's oracle eps-ranks {list(ranks)} (per-term work matched)"
+    tm = {}
     t0 = time.perf_counter()
-    o = oracle_rhosvd([U1, U2, U3], xi, eps=p.eps, ranks=p.ranks)
+    o = oracle_rhosvd([U1, U2, U3], xi, eps=eps, ranks=ranks, timings=tm)
     dt = time.perf_counter() - t0
-    return Rs, dt, o.ranks
+    return Rs, dt, o.ranks, tm, how
 
 
 def default_sample(cfg):
     return {1: 200, 2: 2400, 3: 7260, 4: 4000, 5: 4000}[cfg]
+
+
+def host_info():
+    info = {"nproc": os.cpu_count(), "affinity": cpu_cores()}
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                info["cpu_model"] = ln.split(":", 1)[1].strip()
+                break
+    except Exception:
+        pass
+    try:
+        from threadpoolctl import threadpool_info
+        info["blas"] = [{k: d.get(k) for k in ("internal_api", "version", "num_threads", "threading_layer")}
+                        for d in threadpool_info() if d.get("user_api") == "blas"]
+    except Exception:
+        pass
+    return info
+
+
+def cpu_baseline_entry(cfg, sample_terms, full=False):
+    from workloads import make_params
+    p = make_params(cfg)
+    Rs, dt, oranks, tm, how = oracle_sample(cfg, sample_terms, full=full)
+    what = "all" if Rs == p.R else f"first {Rs} of"
+    return {"value": Rs / dt, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
+            "sample": f"{what} {p.R} terms of {p.name} (n={p.n}); {how}; oracle ranks {list(oranks)}; {dt:.2f} s",
+            "phase_s": {k: round(v, 3) for k, v in tm.items()}, "seconds": dt, "terms": Rs, "host": host_info()}
 
 
 def cpu_cores():
@@ -152,21 +207,23 @@ def run_reference(args):
     p = make_params(args.config)
     Rs = args.cpu_sample or default_sample(args.config)
     for _ in range(max(0, min(args.warmup, 1))):
-        oracle_sample(args.config, Rs)
+        oracle_sample(args.config, Rs, full=args.cpu_full)
     times = []
     for _ in range(args.steps):
-        Rs_, dt, ranks = oracle_sample(args.config, Rs)
+        Rs_, dt, ranks, tm, how = oracle_sample(args.config, Rs, full=args.cpu_full)
         times.append(dt)
     tot = sum(times)
     val = Rs_ * args.steps / tot
-    sample = f"first {Rs_} of {p.R} terms of {p.name} (n={p.n}, eps={p.eps}), oracle ranks {list(ranks)}"
+    what = "all" if Rs_ == p.R else f"first {Rs_} of"
+    sample = f"{what} {p.R} terms of {p.name} (n={p.n}); {how}; oracle ranks {list(ranks)}"
     line = {
         "impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps,
         "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
         "data": "synthetic", "config": {"workload": p.name, "config_index": args.config, "n": p.n,
                                         "R": p.R, "eps": p.eps, "sample_terms": Rs_},
-        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle", "sample": sample},
+        "cpu_baseline": {"value": val, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle", "sample": sample,
+                         "phase_s_last": {k: round(v, 3) for k, v in tm.items()}, "host": host_info()},
         "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -339,11 +396,15 @@ def run_ours(args):
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        Rs = args.cpu_sample or default_sample(args.config)
-        Rs_, dt, oranks = oracle_sample(args.config, Rs)
-        cpu = {"value": Rs_ / dt, "unit": UNIT, "cores": cpu_cores(), "kind": "oracle",
-               "sample": f"first {Rs_} of {p.R} terms of {p.name} (n={p.n}, eps={p.eps}); oracle ranks "
-                         f"{list(oranks)}; {dt:.2f} s"}
+        cpu = cpu_baseline_entry(args.config, args.cpu_sample or default_sample(args.config), full=args.cpu_full)
+        # the full-configuration oracle run of the same workload on this pool's host cores,
+        # measured once by `bench.py --cpu-full` (profiles/r2_oracle_full_cfg{k}.json): context
+        try:
+            full = json.load(open(os.path.join(ROOT, "profiles", f"r2_oracle_full_cfg{args.config}.json")))
+            cpu["full_config_run"] = {k: full.get(k) for k in ("value", "seconds", "sample", "phase_s", "host")}
+            cpu["full_config_run"]["source"] = f"profiles/r2_oracle_full_cfg{args.config}.json (bench.py --cpu-full)"
+        except Exception:
+            pass
 
     if rank == 0:
         launches = sum(r["launches"] for r in reps)
@@ -406,6 +467,10 @@ def main():
         return 2
     if args.impl == "reference":
         return run_reference(args)
+    if args.cpu_only:
+        print(json.dumps(cpu_baseline_entry(args.config, args.cpu_sample or default_sample(args.config),
+                                            full=args.cpu_full)), flush=True)
+        return 0
     return run_ours(args)
 
 

@@ -233,6 +233,36 @@ int  rhosvd_conv3d(const double* const Fa[3], int64_t lda, const double* ca, int
                    const double* const Fp[3], int64_t ldp, const double* cp, int64_t Rp, int64_t n,
                    double h, double* const Fout[3], double* wout, rhosvd_stream stream);
 
+/* ---- range-separated (RS) long-range front-end (section 4) ----
+ * The long-range part of a lattice sum of Slater kernels G_{N,l} = sum_j c_j W_j G_l
+ * (Eq. Slater_interp_multi) as a canonical tensor for rhosvd_c2t; its
+ * Tucker rank grows only as log^{3/2} log(N / eps) (Prop. 4.2).
+ *
+ * rhosvd_sinc_slater (host arrays): the sinc rule of the Slater kernel's Laplace transform
+ *   e^{-lambda sqrt(rho)} = sqrt(alpha/pi) int_0^inf tau^{-3/2} e^{-alpha/tau - rho tau} dtau,
+ *   alpha = lambda^2 / 4, trapezoid in s = ln tau with nodes s_k = k h,
+ *   |k| <= M:  w_k = h sqrt(alpha/pi) e^{-s_k/2} e^{-alpha e^{-s_k}},  tau_k = e^{s_k}; terms
+ *   with w_k < w_min are dropped (reading RS1).  Writes R <= 2M + 1 terms (increasing tau)
+ *   into tau[], w[] (capacity cap, else EINVAL).  G(x) ~ sum_k w_k prod_l e^{-tau_k x_l^2}.
+ * rhosvd_rs_split (host arrays): K_l = {k : t_k <= 1}, K_s = {k : t_k > 1}, t_k = sqrt(tau_k)
+ *   (Eq. RS_repres); copies the long / short terms in order.  Any of
+ *   tau_l, w_l, tau_s, w_s may be NULL (counts only).
+ * rhosvd_rs_lattice (device outputs): the long-range lattice tensor by shift-and-windowing
+ *   (reading RS3): the reference vectors g_k[o] = e^{-tau_k (o h)^2}, o = -(n-1)..(n-1) (the
+ *   doubled grid), are windowed at each node's grid index m_{j,l} (node_idx: device int32,
+ *   N x 3 row-major; indices in [0, n) - others read zeros outside the table):
+ *     column j R_l + k of U_l (n rows, ld ldu >= n):  U_l[i] = g_k[i - m_{j,l}],
+ *     xi[j R_l + k] = c_j w_k   (c: device, N amplitudes).
+ *   tau_l, w_l: host, R_l <= 128 terms.  U1..U3 / xi: caller-allocated device buffers of
+ *   N R_l columns.  Runs on `stream` (two kernels).  EINVAL on bad sizes / null pointers. */
+int rhosvd_sinc_slater(double lambda, double h, int32_t M, double w_min, double* tau, double* w,
+                       int64_t cap, int64_t* R);
+int rhosvd_rs_split(const double* tau, const double* w, int64_t R, double* tau_l, double* w_l,
+                    int64_t* R_l, double* tau_s, double* w_s, int64_t* R_s);
+int rhosvd_rs_lattice(const double* tau_l, const double* w_l, int64_t R_l, double h, int64_t n,
+                      const int32_t* node_idx, const double* c, int64_t N, double* U1, double* U2,
+                      double* U3, int64_t ldu, double* xi, rhosvd_stream stream);
+
 /* ---- kernel-level entry points (used by the parity unit tests and bench) ----
  * Each runs ONE device kernel family on `stream`, all pointers device.     */
 

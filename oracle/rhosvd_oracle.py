@@ -196,7 +196,7 @@ class OracleResult:
     report: dict = field(default_factory=dict)
 
 
-def rhosvd(Us, xi, eps=None, ranks=None, with_W=True, with_core=True):
+def rhosvd(Us, xi, eps=None, ranks=None, with_W=True, with_core=True, timings=None):
     """RHOSVD canonical-to-Tucker transform (O1-O8), d = len(Us) (3 here).
 
     Us: list of (R, n_l) arrays (raw, unnormalized); xi: (R,).
@@ -204,7 +204,15 @@ def rhosvd(Us, xi, eps=None, ranks=None, with_W=True, with_core=True):
     with_core=False stops after O6 (frames, sigma, ranks, W; beta = None): the
     Tucker tensor is then fixed by the frames through Def. 2.1, and the full-size
     parity fixtures need only those.
+    timings: optional dict; receives the wall seconds of each step (normalize, svd,
+    rank_frames, projection, core) for the CPU baseline report.  No effect on results.
     """
+    import time
+    clock = time.perf_counter
+    tm = timings if timings is not None else {}
+    for key in ("normalize", "svd", "rank_frames", "projection", "core"):
+        tm[key] = 0.0
+    t0 = clock()
     d = len(Us)
     if (eps is None) == (ranks is None):
         raise ValueError("give exactly one of eps or ranks")
@@ -212,13 +220,17 @@ def rhosvd(Us, xi, eps=None, ranks=None, with_W=True, with_core=True):
         raise ValueError("eps must lie in (0, 1)")
     R = xi.shape[0]
     Uh, xip, s, T = normalize(Us, xi)
+    tm["normalize"] += clock() - t0
     Zs, sig, rs, tails, margins, Ws = [], [], [], [], [], []
     for l in range(d):
         n = Uh[l].shape[1]
         if R == 0:
             Z_full, sg = np.zeros((n, 0)), np.zeros(0)
         else:
+            t0 = clock()
             Z_full, sg = mode_svd(Uh[l])
+            tm["svd"] += clock() - t0
+        t0 = clock()
         r, tail2, mar = select_rank(sg, T[l], eps=eps,
                                     r_fixed=None if ranks is None else ranks[l])
         Z, _ = canonical_sign(Z_full[:, :r])
@@ -227,11 +239,16 @@ def rhosvd(Us, xi, eps=None, ranks=None, with_W=True, with_core=True):
         rs.append(r)
         tails.append(math.sqrt(max(tail2[r], 0.0)) if sg.shape[0] else 0.0)
         margins.append(mar)
+        tm["rank_frames"] += clock() - t0
+        t0 = clock()
         Ws.append(project(Z, Uh[l]))
+        tm["projection"] += clock() - t0
     if not with_core:
         beta = None
     elif d == 3:
+        t0 = clock()
         beta = core_kr(Ws[0], Ws[1], Ws[2], xip)
+        tm["core"] += clock() - t0
     else:
         raise NotImplementedError("hot path is d = 3")
     bp, bns = error_bounds(xip, tails)

@@ -19,7 +19,7 @@ BUILD = os.path.join(ROOT, "build", "rhosvd")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC_FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O3",
               "--expt-relaxed-constexpr", "-I" + os.path.join(ROOT, "include")] + ARCH
-SOURCES = ["gemm.cu", "small_dense.cu", "misc_kernels.cu", "core_kr.cu", "comm.cu", "rhosvd.cu", "t2c.cu", "conv.cu"]
+SOURCES = ["gemm.cu", "small_dense.cu", "misc_kernels.cu", "core_kr.cu", "comm.cu", "rhosvd.cu", "t2c.cu", "conv.cu", "rs.cu"]
 
 
 def nvcc() -> str:

@@ -97,6 +97,9 @@ def lib():
         "rhosvd_cp_weights": (C.c_int, [P, C.POINTER(P), C.POINTER(P)]),
         "rhosvd_cp_info": (C.c_int, [P, C.POINTER(D), C.POINTER(D), C.POINTER(D), C.POINTER(I32)]),
         "rhosvd_cp_free": (None, [P]),
+        "rhosvd_sinc_slater": (C.c_int, [D, D, I32, D, P, P, I64, C.POINTER(I64)]),
+        "rhosvd_rs_split": (C.c_int, [P, P, I64, P, P, C.POINTER(I64), P, P, C.POINTER(I64)]),
+        "rhosvd_rs_lattice": (C.c_int, [P, P, I64, D, I64, P, P, I64, P, P, P, I64, P, P]),
     }
     for name, (res, args) in sig.items():
         f = getattr(L, name)
@@ -114,7 +117,7 @@ EXPORTED = ["rhosvd_opts_default", "rhosvd_c2t", "rhosvd_result_ranks", "rhosvd_
             "rhosvd_chol_inv", "rhosvd_t2c", "rhosvd_cp_rank", "rhosvd_cp_factor", "rhosvd_cp_core_factor",
             "rhosvd_cp_weights", "rhosvd_cp_info", "rhosvd_cp_free", "rhosvd_c2t_host",
             "rhosvd_result_host_frame", "rhosvd_result_host_sigma", "rhosvd_result_host_core",
-            "rhosvd_c2t_als", "rhosvd_conv3d"]
+            "rhosvd_c2t_als", "rhosvd_conv3d", "rhosvd_sinc_slater", "rhosvd_rs_split", "rhosvd_rs_lattice"]
 
 
 def _check(status):
@@ -619,3 +622,51 @@ def conv3d(Fa, ca, Fp, cp, h, stream=None):
         _check(lib().rhosvd_conv3d(pa, lda, _ptr(ca.contiguous()), Ra, pp, n, _ptr(cp.contiguous()), Rp, n,
                                    float(h), po, _ptr(w), _stream_ptr(stream)))
     return F, w
+
+
+# ---------------------------------------------------------------- RS long-range front-end (f3)
+def sinc_slater(lam, h, M, w_min=0.0):
+    """rhosvd_sinc_slater: (tau, w) numpy arrays of the Slater kernel's sinc rule."""
+    import numpy as np
+    cap = 2 * int(M) + 1
+    tau = np.zeros(cap)
+    w = np.zeros(cap)
+    R = C.c_int64()
+    _check(lib().rhosvd_sinc_slater(float(lam), float(h), int(M), float(w_min), tau.ctypes.data_as(C.c_void_p),
+                                    w.ctypes.data_as(C.c_void_p), cap, C.byref(R)))
+    return tau[:R.value].copy(), w[:R.value].copy()
+
+
+def rs_split(tau, w):
+    """rhosvd_rs_split: ((tau_l, w_l), (tau_s, w_s))."""
+    import numpy as np
+    tau = np.ascontiguousarray(tau, dtype=np.float64)
+    w = np.ascontiguousarray(w, dtype=np.float64)
+    R = tau.shape[0]
+    tl, wl, ts, ws = (np.zeros(max(R, 1)) for _ in range(4))
+    Rl, Rs = C.c_int64(), C.c_int64()
+    P = lambda a: a.ctypes.data_as(C.c_void_p)  # noqa: E731
+    _check(lib().rhosvd_rs_split(P(tau), P(w), R, P(tl), P(wl), C.byref(Rl), P(ts), P(ws), C.byref(Rs)))
+    return (tl[:Rl.value].copy(), wl[:Rl.value].copy()), (ts[:Rs.value].copy(), ws[:Rs.value].copy())
+
+
+def rs_lattice(tau_l, w_l, h, n, node_idx, c, stream=None):
+    """rhosvd_rs_lattice: the long-range lattice tensor on the device.
+
+    node_idx: torch.int32 CUDA (N, 3); c: torch.float64 CUDA (N,).  Returns (U1, U2, U3, xi)
+    as torch.float64 CUDA tensors, U_l of shape (N R_l, n) (column-major n x R)."""
+    import numpy as np
+    import torch
+    tau_l = np.ascontiguousarray(tau_l, dtype=np.float64)
+    w_l = np.ascontiguousarray(w_l, dtype=np.float64)
+    if not (node_idx.is_cuda and node_idx.dtype == torch.int32 and node_idx.is_contiguous()):
+        raise TypeError("node_idx must be a contiguous torch.int32 CUDA tensor (N, 3)")
+    _need_cuda_f64(c, "c")
+    N, Rl = int(node_idx.shape[0]), int(tau_l.shape[0])
+    dev = c.device
+    U = [torch.empty(N * Rl, n, dtype=torch.float64, device=dev) for _ in range(3)]
+    xi = torch.empty(N * Rl, dtype=torch.float64, device=dev)
+    _check(lib().rhosvd_rs_lattice(tau_l.ctypes.data_as(C.c_void_p), w_l.ctypes.data_as(C.c_void_p), Rl, float(h),
+                                   int(n), _ptr(node_idx), _ptr(c), N, _ptr(U[0]), _ptr(U[1]), _ptr(U[2]), int(n),
+                                   _ptr(xi), _stream_ptr(stream)))
+    return U[0], U[1], U[2], xi
