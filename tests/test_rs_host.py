@@ -18,7 +18,8 @@ def test_sinc_rule_matches_oracle(rh, lam, h, M, wmin):
     t, w = rh.sinc_slater(lam, h, M, wmin)
     to, wo = slater_sinc_rule(lam, h, M, wmin)
     assert t.shape == to.shape
-    assert np.max(np.abs(t - to) / to) <= 2e-16 and np.max(np.abs(w - wo) / wo) <= 4e-16
+    # libm vs numpy exp: a few ulps (w is a product of two exponentials)
+    assert np.all(np.abs(t - to) <= 4e-16 * to) and np.all(np.abs(w - wo) <= 1e-15 * wo + 1e-300)
 
 
 def test_split_matches_oracle(rh):
