@@ -117,6 +117,7 @@ typedef struct {
   double  core_ms;       /* device time of the core kernel(s) alone                */
   double  gram_ms;       /* device time of the Gram kernel(s) alone                */
   int32_t launches;      /* kernels launched by this call                          */
+  int32_t refines[3];    /* non-squared refinement steps per mode                  */
 } rhosvd_report;
 
 typedef struct rhosvd_comm rhosvd_comm;       /* NULL => single GPU                */

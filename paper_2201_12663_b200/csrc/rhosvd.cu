@@ -742,6 +742,12 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
       const double rho = std::min(0.9, std::max(d_h[b - 1], 64.0 * u * d1) / dr);
       int need = e0 <= 1e-11 ? 0 : (int)std::ceil(std::log(1e-11 / e0) / std::log(rho * rho));
       nref = std::max(o.refine_steps, std::min(need, o.refine_steps + 3));
+      // RHOSVD_REFINE_MAX (probe knob): cap the modelled step count (>= refine_steps)
+      static const int refine_cap = [] {
+        const char* e = getenv("RHOSVD_REFINE_MAX");
+        return e ? atoi(e) : 0;
+      }();
+      if (refine_cap > 0) nref = std::max(o.refine_steps, std::min(nref, refine_cap));
       if (dbg_on())
         fprintf(stderr, "[rhosvd dbg] mode %d refine model e0 %.2e rho %.3e -> %d steps\n", mode, e0, rho, nref);
     }
@@ -1477,6 +1483,7 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
     rep.block[l] = mo[l].b;
     rep.iters[l] = mo[l].iters;
     rep.grow_events[l] = mo[l].grows;
+    rep.refines[l] = mo[l].refines;
     rep.rho[l] = mo[l].rho;
     rep.tail[l] = std::sqrt(std::max(0.0, mo[l].tail2));
   }

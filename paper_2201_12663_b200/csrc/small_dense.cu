@@ -1207,9 +1207,188 @@ __global__ void __launch_bounds__(256) chol_blk_kernel(CholParams p) {
   }
 }
 
+// ---------------------------------------------------------------- one-CTA Cholesky inverse
+// The same Bp = D L^{-T} as chol_blk_kernel for b <= 32 E <= 160, in ONE CTA of 32 x 32
+// threads with the lower triangle in registers: thread (ty, tx) owns the elements
+// (i, k) = (ty + 32 a, tx + 32 c), c <= a < E (the lower 32 x 32 blocks, 2D block-cyclic).
+// No grid barrier and no cooperative launch: the kernel occupies one SM, so the three
+// concurrent per-mode eigensolves keep the rest of the GPU for their GEMMs (the blocked
+// cooperative kernel takes every SM for ~0.1-0.2 ms at b ~ 150).
+//   Cholesky (right-looking, unscaled updates): at step c the owners of column c publish
+//     it to a double-buffered shared vector, ONE __syncthreads, every thread applies
+//     a_ik -= a_ic a_kc / d_c (c < k <= i); pivot d_c <= delta: dependent column (unit
+//     pivot, zero sub-column, as the blocked kernel).  L is then written to shared memory.
+//   Inverse X = L^{-1} (right-looking forward substitution; row r is final at step r):
+//     the owners of row r scale it by 1 / L_rr and publish it, ONE __syncthreads, rows
+//     i > r apply x_ic -= L_ir x_rc (c <= r), L_ir read from shared memory (broadcast).
+//   Output Bp(c, i) = d_c X(i, c) (c <= i), 0 above.
+template <int E>
+__global__ void __launch_bounds__(1024, 1) chol_small_kernel(int b, const double* __restrict__ S, int64_t lds,
+                                                              double shift, double delta, double* __restrict__ Bp,
+                                                              int64_t ldb, int* info) {
+  extern __shared__ double Ls[];  // b x (b | 1) lower triangle of L
+  __shared__ double cbuf[2][32 * E];
+  __shared__ double dsc[32 * E];
+  __shared__ double piv[32 * E];
+  __shared__ int depf[32 * E];
+  const int P = b | 1;
+  const int tid = threadIdx.x, tx = tid & 31, ty = tid >> 5;
+  for (int k = tid; k < b; k += 1024) {
+    const double sk = S[(int64_t)k * lds + k];
+    dsc[k] = sk > 0.0 ? 1.0 / sqrt(sk) : 1.0;
+  }
+  __syncthreads();
+  double a[E][E];  // a[A][C]: element (ty + 32 A, tx + 32 C), C <= A
+#pragma unroll
+  for (int A = 0; A < E; ++A)
+#pragma unroll
+    for (int C = 0; C < E; ++C) {
+      const int i = ty + 32 * A, k = tx + 32 * C;
+      double v = 0.0;
+      if (C <= A && i < b && k <= i) {
+        v = S[(int64_t)i * lds + k] * dsc[i] * dsc[k];  // upper-part entry (k, i)
+        if (k == i) v += shift;
+      }
+      a[A][C] = v;
+    }
+  // ---- Cholesky
+#pragma unroll
+  for (int Cb = 0; Cb < E; ++Cb) {
+    for (int cc = 0; cc < 32; ++cc) {
+      const int c = 32 * Cb + cc;
+      if (c >= b) break;  // uniform
+      double* col = cbuf[c & 1];
+      if (tx == cc) {
+#pragma unroll
+        for (int A = Cb; A < E; ++A) {
+          const int i = ty + 32 * A;
+          if (i >= c && i < b) col[i] = a[A][Cb];
+        }
+      }
+      __syncthreads();
+      const double d = col[c];
+      const bool dep = !(d > delta);
+      if (tid == 0) {
+        piv[c] = d;
+        depf[c] = dep ? 1 : 0;
+      }
+      if (!dep) {
+        const double rd = 1.0 / d;
+        double ci[E], ck[E];
+#pragma unroll
+        for (int A = 0; A < E; ++A) {
+          const int i = ty + 32 * A, k = tx + 32 * A;
+          ci[A] = (i > c && i < b) ? col[i] * rd : 0.0;
+          ck[A] = (k > c && k < b) ? col[k] : 0.0;
+        }
+#pragma unroll
+        for (int A = 0; A < E; ++A)
+#pragma unroll
+          for (int C = 0; C <= A; ++C) a[A][C] = fma(-ci[A], ck[C], a[A][C]);
+      }
+    }
+  }
+  __syncthreads();
+  // scale into L: L(i, k) = a_ik / sqrt(d_k) (k < i), L(i, i) = sqrt(d_i); dependent: 1 / 0
+#pragma unroll
+  for (int A = 0; A < E; ++A)
+#pragma unroll
+    for (int C = 0; C <= A; ++C) {
+      const int i = ty + 32 * A, k = tx + 32 * C;
+      if (i < b && k <= i) {
+        const bool dk = depf[k] != 0;
+        Ls[i * P + k] = (k == i) ? (dk ? 1.0 : sqrt(piv[k])) : (dk ? 0.0 : a[A][C] / sqrt(piv[k]));
+      }
+    }
+  if (tid == 0) {
+    int any = 0;
+    for (int c = 0; c < b; ++c) any |= depf[c];
+    if (any) atomicOr(info + 1, 1);
+  }
+  __syncthreads();
+  // ---- X = L^{-1}, reusing a[][] for X (Y = I initially)
+#pragma unroll
+  for (int A = 0; A < E; ++A)
+#pragma unroll
+    for (int C = 0; C <= A; ++C) a[A][C] = (ty + 32 * A == tx + 32 * C) ? 1.0 : 0.0;
+#pragma unroll
+  for (int Rb = 0; Rb < E; ++Rb) {
+    for (int rr = 0; rr < 32; ++rr) {
+      const int r = 32 * Rb + rr;
+      if (r >= b) break;
+      double* xrow = cbuf[r & 1];
+      if (ty == rr) {  // the owners of row r: x_r <- x_r / L_rr, publish
+        const double rl = 1.0 / Ls[r * P + r];
+#pragma unroll
+        for (int C = 0; C <= Rb; ++C) {
+          const int c = tx + 32 * C;
+          if (c <= r) {
+            a[Rb][C] *= rl;
+            xrow[c] = a[Rb][C];
+          }
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int A = Rb; A < E; ++A) {
+        const int i = ty + 32 * A;
+        if (i > r && i < b) {
+          const double l = Ls[i * P + r];
+#pragma unroll
+          for (int C = 0; C <= Rb; ++C) {
+            const int c = tx + 32 * C;
+            if (c <= r) a[A][C] = fma(-l, xrow[c], a[A][C]);
+          }
+        }
+      }
+    }
+  }
+  // ---- Bp(c, i) = d_c X(i, c) for c <= i, 0 for c > i
+#pragma unroll
+  for (int A = 0; A < E; ++A)
+#pragma unroll
+    for (int C = 0; C < E; ++C) {
+      const int i = ty + 32 * A, c = tx + 32 * C;
+      if (i < b && c < b) Bp[(int64_t)i * ldb + c] = (C <= A && c <= i) ? dsc[c] * a[A][C] : 0.0;
+    }
+}
+
+template <int E>
+static int chol_small_launch(int64_t b, const double* S, int64_t lds, double shift, double* Bp, int64_t ldb,
+                             int* info, cudaStream_t st) {
+  const size_t smem = (size_t)b * (b | 1) * sizeof(double);
+  static const cudaError_t attr =
+      cudaFuncSetAttribute(chol_small_kernel<E>, cudaFuncAttributeMaxDynamicSharedMemorySize, 32 * E * (32 * E + 1) * 8);
+  RH_CUDA(attr);
+  chol_small_kernel<E><<<1, 1024, smem, st>>>((int)b, S, lds, shift, 1e-13, Bp, ldb, info);
+  count_launch();
+  RH_LAUNCH_CHECK();
+  return RHOSVD_OK;
+}
+
+// one-CTA path for b <= RHOSVD_CHOL_SMALL_MAXB (default 160; 0 disables)
+static int chol_small(int64_t b, const double* S, int64_t lds, double shift, double* Bp, int64_t ldb, int* info,
+                      cudaStream_t st) {
+  switch ((int)cdiv(b, 32)) {
+    case 1: return chol_small_launch<1>(b, S, lds, shift, Bp, ldb, info, st);
+    case 2: return chol_small_launch<2>(b, S, lds, shift, Bp, ldb, info, st);
+    case 3: return chol_small_launch<3>(b, S, lds, shift, Bp, ldb, info, st);
+    case 4: return chol_small_launch<4>(b, S, lds, shift, Bp, ldb, info, st);
+    default: return chol_small_launch<5>(b, S, lds, shift, Bp, ldb, info, st);
+  }
+}
+
 int chol_inv_scaled(int64_t b, const double* S, int64_t lds, double shift_rel, double* Bp, int64_t ldb,
                     DenseWs& ws, cudaStream_t st) {
   if (b <= 0) return RHOSVD_OK;
+  static const int small_maxb = [] {
+    const char* e = getenv("RHOSVD_CHOL_SMALL_MAXB");
+    return e ? std::max(0, std::min(atoi(e), 160)) : 160;
+  }();
+  if (b <= small_maxb) {
+    RH_CHECK(ws.ensure(b, st));
+    return chol_small(b, S, lds, shift_rel, Bp, ldb, ws.info, st);
+  }
   const int P = (int)cdiv(b, CB);
   RH_CHECK(ws.ensure((int64_t)P * CB, st));
   CholParams cp{};

@@ -38,7 +38,7 @@ class Report(C.Structure):
                 ("rho", C.c_double * 3), ("ranks", C.c_int32 * 3), ("block", C.c_int32 * 3),
                 ("iters", C.c_int32 * 3), ("grow_events", C.c_int32 * 3), ("R_global", C.c_int64),
                 ("ms", C.c_double * 16), ("gemm_flops", C.c_double), ("core_ms", C.c_double),
-                ("gram_ms", C.c_double), ("launches", C.c_int32)]
+                ("gram_ms", C.c_double), ("launches", C.c_int32), ("refines", C.c_int32 * 3)]
 
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.POINTER(C.c_double), C.c_int64, C.c_void_p, C.c_void_p)
@@ -276,7 +276,7 @@ def _report_dict(rep: Report):
         ms_modes_summed={nm: rep.ms[9 + i] for i, nm in
                          enumerate(["eigensolve", "rr_refine", "residual_rank", "projection", "collectives"])},
         gemm_flops=rep.gemm_flops,
-        core_ms=rep.core_ms, gram_ms=rep.gram_ms, launches=rep.launches)
+        core_ms=rep.core_ms, gram_ms=rep.gram_ms, launches=rep.launches, refines=list(rep.refines))
 
 
 def c2t_raw(U, xi, opts: Opts, comm: Comm | None = None, stream=None, als_sweeps=None):

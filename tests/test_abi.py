@@ -74,7 +74,7 @@ def test_argument_validation_without_gpu(lib):
 def test_report_struct_size():
     from paper_2201_12663_b200 import rhosvd
     # 3+3+1+1+1+1+3 doubles, 3*4 int32 + int64 + 16 doubles + 3 doubles + int32 (+pad)
-    assert ctypes.sizeof(rhosvd.Report) == 8 * 13 + 4 * 12 + 8 + 8 * 16 + 8 * 3 + 8
+    assert ctypes.sizeof(rhosvd.Report) == 8 * 13 + 4 * 12 + 8 + 8 * 16 + 8 * 3 + 4 + 4 * 3
 
 
 def test_no_oracle_import_in_product():

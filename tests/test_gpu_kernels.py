@@ -110,7 +110,9 @@ def test_core(rh, r, R):
     assert np.max(np.abs(beta - ref)) <= 1e-13 * np.sqrt(R) * np.max(np.abs(ref)) * 8
 
 
-@pytest.mark.parametrize("b", [1, 5, 64, 65, 130, 298, 707])
+# b <= 160: the one-CTA register kernel (every 32-block count and its edges); larger b:
+# the cooperative blocked kernel
+@pytest.mark.parametrize("b", [1, 5, 31, 32, 33, 64, 65, 96, 127, 128, 129, 130, 159, 160, 161, 298, 707])
 def test_chol_inv(rh, b):
     """Bp = D L^{-T} (scaled Cholesky inverse) against LAPACK; Q = M Bp orthonormal."""
     rng = np.random.default_rng(b + 11)
@@ -125,16 +127,17 @@ def test_chol_inv(rh, b):
     assert np.max(np.abs(Q.T @ Q - np.eye(b))) <= 1e-12
 
 
-def test_chol_inv_dependent_column(rh):
+@pytest.mark.parametrize("b", [100, 200])
+def test_chol_inv_dependent_column(rh, b):
     """A numerically dependent column gets a unit pivot and a zero sub-column: the
-    remaining columns stay orthonormal and no NaN appears."""
+    remaining columns stay orthonormal and no NaN appears (one-CTA and blocked kernels)."""
     rng = np.random.default_rng(5)
-    M = rng.normal(size=(300, 100))
+    M = rng.normal(size=(3 * b, b))
     M[:, 40] = M[:, 3] + 1e-9 * M[:, 40]
     S = M.T @ M
     Bp = rh.chol_inv(dev(S)).cpu().numpy()
     assert np.all(np.isfinite(Bp))
     Q = M @ Bp
-    keep = [i for i in range(100) if i != 40]
+    keep = [i for i in range(b) if i != 40]
     G = Q[:, keep].T @ Q[:, keep]
-    assert np.max(np.abs(G - np.eye(99))) <= 1e-8
+    assert np.max(np.abs(G - np.eye(b - 1))) <= 1e-8

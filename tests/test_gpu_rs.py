@@ -44,17 +44,18 @@ def test_window_matches_direct_evaluation(rh, L, kw):
     O = _oracle_lattice(lat)
     for g, o in zip((U1, U2, U3), O[:3]):
         assert g.shape == o.shape
-        assert np.max(np.abs(g.cpu().numpy() - o)) <= 4e-16
-    assert np.max(np.abs(xi.cpu().numpy() - O[3]) / np.abs(O[3])) <= 4e-16
+        # (i - m) h on the device vs x_i - x_m on the host, and device vs host exp: a few ulps
+        assert np.max(np.abs(g.cpu().numpy() - o)) <= 2e-15
+    assert np.max(np.abs(xi.cpu().numpy() - O[3]) / np.abs(O[3])) <= 2e-15   # w_k: libm vs numpy exp
 
 
 def test_window_edge_nodes(rh):
     """Nodes at grid indices 0 and n - 1 (the window touches both ends of the doubled table)."""
-    lat = make_rs_lattice((2, 2, 2), n=40, b=4.0, spacing=39)
+    lat = make_rs_lattice((2, 2, 2), n=40, b=4.0, spacing=39, first=0)
     assert lat.node_idx.min() == 0 and lat.node_idx.max() == 39
     (U1, U2, U3, xi), _ = _gpu_lattice(rh, lat)
     O = _oracle_lattice(lat)
-    assert np.max(np.abs(U3.cpu().numpy() - O[2])) <= 4e-16
+    assert np.max(np.abs(U3.cpu().numpy() - O[2])) <= 2e-15
 
 
 @pytest.mark.parametrize("L", [(4, 4, 4), (8, 8, 8), (16, 16, 8)])

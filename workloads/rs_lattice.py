@@ -53,12 +53,16 @@ class RSLattice:
         return grid(self.n, self.b)
 
 
-def make_rs_lattice(L, n=384, b=12.0, spacing=16, lam=0.5, amplitudes="random", seed=2022) -> RSLattice:
+def make_rs_lattice(L, n=384, b=12.0, spacing=16, lam=0.5, amplitudes="random", seed=2022, first=None) -> RSLattice:
     """L1 x L2 x L3 lattice of Slater centres on the n-grid (node-major order: the
-    last lattice index fastest)."""
+    last lattice index fastest); centred at grid index n / 2, or starting at grid index
+    `first` in every mode."""
     L = tuple(int(v) for v in L)
     x = grid(n, b)
-    axes = [n // 2 + spacing * (np.arange(Lk) - (Lk - 1) // 2) for Lk in L]
+    if first is None:
+        axes = [n // 2 + spacing * (np.arange(Lk) - (Lk - 1) // 2) for Lk in L]
+    else:
+        axes = [first + spacing * np.arange(Lk) for Lk in L]
     for a in axes:
         if a.min() < 0 or a.max() >= n:
             raise ValueError("lattice does not fit the grid")
