@@ -408,6 +408,7 @@ struct CommSched {
   struct Req {
     double* p = nullptr;
     int64_t count = 0;
+    int root = -1;  // -1: sum all-reduce; >= 0: broadcast from this rank
     cudaStream_t st = nullptr;
     bool posted = false, done = false, finished = false;
     int status = RHOSVD_OK;
@@ -415,10 +416,10 @@ struct CommSched {
   } req[3];
   int dev = 0;
   // mode thread: run one all-reduce through the comm thread (blocks until done)
-  int post(int mode, double* p, int64_t count, cudaStream_t st) {
+  int post(int mode, double* p, int64_t count, cudaStream_t st, int root = -1) {
     std::unique_lock<std::mutex> lk(mu);
     Req& r = req[mode];
-    r.p = p; r.count = count; r.st = st; r.done = false; r.posted = true;
+    r.p = p; r.count = count; r.st = st; r.root = root; r.done = false; r.posted = true;
     cv.notify_all();
     cv.wait(lk, [&] { return r.done; });
     if (r.status != RHOSVD_OK) set_error(r.err);
@@ -443,7 +444,8 @@ struct CommSched {
           r.posted = false;
           if (comm_trace()) fprintf(stderr, "[rhosvd comm exec] rank %d mode %d count %lld\n", comm->rank, l, (long long)r.count);
           lk.unlock();
-          int s = comm_allreduce(comm, r.p, r.count, r.st);
+          int s = r.root >= 0 ? comm_broadcast(comm, r.p, r.count, r.root, r.st)
+                              : comm_allreduce(comm, r.p, r.count, r.st);
           std::string e = s != RHOSVD_OK ? std::string(rhosvd_last_error()) : std::string();
           lk.lock();
           r.status = s;
@@ -453,6 +455,39 @@ struct CommSched {
         }
       }
       l = (l + 1) % 3;
+    }
+  }
+};
+
+// Mode parallelism on a multi-rank communicator: the Gram-domain
+// subspace iteration of mode l (S3: G only - no R-dependent data, no collective) runs on
+// rank l mod p alone; its block Z (n x b) and the iteration state go to the other ranks by
+// broadcast, and the R-sharded refinement / Rayleigh-Ritz / residual (S4) continue on all
+// ranks.  Every rank first finishes the solves it owns (the latch), then posts its
+// broadcasts: no NCCL kernel of this call waits on the device while an owned solve runs.
+struct ModeLatch {
+  std::mutex mu;
+  std::condition_variable cv;
+  int pending = 0;  // owned modes whose subspace iteration has not finished
+  void done() {
+    std::lock_guard<std::mutex> lk(mu);
+    --pending;
+    cv.notify_all();
+  }
+  void wait() {
+    std::unique_lock<std::mutex> lk(mu);
+    cv.wait(lk, [&] { return pending <= 0; });
+  }
+};
+struct MPar {
+  bool owner = false;
+  int root = 0;
+  ModeLatch* latch = nullptr;
+  bool signalled = false;
+  void signal() {  // an owner's solve is over (once, on every path)
+    if (owner && !signalled) {
+      signalled = true;
+      latch->done();
     }
   }
 };
@@ -467,6 +502,7 @@ struct Ctx {
   ModeWs* m = nullptr;  // per-mode buffers (S3-S5); GEMM scratch comes from here when set
   CommSched* sched = nullptr;  // concurrent modes on a multi-rank communicator
   int mode = 0;
+  MPar* mp = nullptr;           // mode parallelism (multi-rank, concurrent modes)
 };
 
 // ------------------------------------------------------------------ GEMM shorthands
@@ -486,6 +522,13 @@ static int allreduce(Ctx& c, double* p, int64_t count) {
   c.tm->mark(PH_COMM);
   if (c.sched) return c.sched->post(c.mode, p, count, c.st);
   return comm_allreduce(c.comm, p, count, c.st);
+}
+static int broadcast(Ctx& c, double* p, int64_t count, int root) {
+  if (!c.comm || !c.comm->active()) return RHOSVD_OK;
+  if (comm_trace()) fprintf(stderr, "[rhosvd comm] rank %d mode %d bcast root %d count %lld\n", c.comm->rank, c.mode, root, (long long)count);
+  c.tm->mark(PH_COMM);
+  if (c.sched) return c.sched->post(c.mode, p, count, c.st, root);
+  return comm_broadcast(c.comm, p, count, root, c.st);
 }
 
 // RHOSVD_DEBUG=1: synchronise and scan a device array for non-finite values (debug only)
@@ -615,8 +658,6 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
 
   RH_CHECK(ensure_b(b));
   uint64_t seed = o.seed * 0x9E3779B97F4A7C15ull + (uint64_t)(mode + 1) * 0xD1B54A32D192ED03ull;
-  // random start block (Gaussian columns; the first step's G Omega is orthonormalised)
-  RH_CHECK(k_random(w.Z.p, LDN, n, 0, b, seed, st));
 
   // ---------------- subspace (simultaneous) iteration Z <- CholQR(G Z), block growth.
   // CholQR keeps leading spans, so span(z_1..z_j) converges to the dominant j-space for
@@ -657,6 +698,9 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
   int need_last = 0;     // modelled iteration count of the last convergence test
   bool capped = false;   // the last block stopped at max_iters before need_last
   int64_t r_est = rfix;
+  auto subspace_iteration = [&]() -> int {
+  // random start block (Gaussian columns; the first step's G Omega is orthonormalised)
+  RH_CHECK(k_random(w.Z.p, LDN, n, 0, b, seed, st));
   while (true) {
     ++it_total;
     ++itb;
@@ -698,6 +742,43 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
       capped = need > cap;
       break;
     }
+  }
+  return RHOSVD_OK;
+  };
+  if (!c.mp) {
+    RH_CHECK(subspace_iteration());
+  } else {
+    // mode parallelism: the owner iterates; then (after every solve this rank owns) the
+    // state header [status, b, r_est, itb, it_total, grows, need_last, capped, d_1..d_b]
+    // and the block Z go out by broadcast.  A failed owner still broadcasts its status, so
+    // every rank returns the same error instead of waiting for a Z that never comes.
+    int st_a = RHOSVD_OK;
+    std::string err_a;
+    if (c.mp->owner) {
+      st_a = subspace_iteration();
+      if (st_a != RHOSVD_OK) err_a = g_err;
+      c.mp->signal();
+    }
+    c.mp->latch->wait();
+    const int64_t hn = 8 + m;
+    RH_CHECK(w.H.ensure((size_t)std::max<int64_t>(hn, round_up(std::max<int64_t>(m, 2), 2) * m) + 64, st));
+    std::vector<double> hdr(hn, 0.0);
+    if (c.mp->owner) {
+      hdr[0] = st_a; hdr[1] = (double)b; hdr[2] = (double)r_est; hdr[3] = itb; hdr[4] = it_total;
+      hdr[5] = mo.grows; hdr[6] = need_last; hdr[7] = capped ? 1.0 : 0.0;
+      for (size_t k = 0; k < d_h.size() && (int64_t)k < m; ++k) hdr[8 + k] = d_h[k];
+      RH_CHECK(h2d_wait(w.H.p, hdr.data(), hn * sizeof(double), st));
+    }
+    RH_CHECK(broadcast(c, w.H.p, hn, c.mp->root));
+    RH_CHECK(d2h_wait(hdr.data(), w.H.p, hn * sizeof(double), st));
+    if ((int)hdr[0] != RHOSVD_OK)
+      return fail((int)hdr[0], c.mp->owner ? err_a : "mode " + std::to_string(mode) + ": owner rank failed");
+    b = (int64_t)hdr[1]; r_est = (int64_t)hdr[2]; itb = (int)hdr[3]; it_total = (int)hdr[4];
+    mo.grows = (int)hdr[5]; need_last = (int)hdr[6]; capped = hdr[7] != 0.0;
+    d_h.assign(hdr.begin() + 8, hdr.begin() + 8 + std::min<int64_t>(b, m));
+    if (b >= m) d_h.clear();  // full space: the owner kept no estimates
+    RH_CHECK(ensure_b(b));
+    RH_CHECK(broadcast(c, w.Z.p, LDN * b, c.mp->root));
   }
   mo.iters = it_total;
   // block truncation: smallest b' >= r + p with d_b' <= 0.02 d_r (leading columns carry
@@ -1309,6 +1390,21 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
       sched->dev = dev;
       comm_thread = std::thread([&] { sched->run(); });
     }
+    // mode parallelism (RHOSVD_MODE_PARALLEL=0 replicates the subspace iterations instead)
+    static const bool mpar_on = [] {
+      const char* e = getenv("RHOSVD_MODE_PARALLEL");
+      return !(e && e[0] == '0');
+    }();
+    ModeLatch latch;
+    MPar mpar[3];
+    const bool mode_parallel = mpar_on && sched && !streamed;
+    if (mode_parallel)
+      for (int l = 0; l < 3; ++l) {
+        mpar[l].root = l % comm->world;
+        mpar[l].owner = mpar[l].root == comm->rank;
+        mpar[l].latch = &latch;
+        if (mpar[l].owner) ++latch.pending;
+      }
     double mflops[3] = {0, 0, 0};
     int mlaunch[3] = {0, 0, 0};
     double mphase[3][16] = {{0}};
@@ -1374,6 +1470,7 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
       Ctx cl{ms[l], comm, w, &rep, &mtm};
       cl.m = &w.mw[l];
       cl.sched = sched.get();
+      cl.mp = mode_parallel ? &mpar[l] : nullptr;
       cl.mode = l;
       if (streamed) {
         mst[l] = prep_mode(cl, l);
@@ -1386,6 +1483,7 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
         }
       }
       mst[l] = solve_mode(cl, l, n, LDN, Rl, Rp, Rg, Uh[l], w.G.p + (size_t)l * LDN * LDN, rep.trace[l], o, mo[l]);
+      if (cl.mp) cl.mp->signal();  // an early error must not leave the other modes waiting
       if (cl.sched) cl.sched->finish(l);
       mtm.mark(-1);
       if (mst[l] != RHOSVD_OK) merr[l] = g_err;

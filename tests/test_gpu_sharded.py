@@ -43,10 +43,11 @@ def _params(case):
     return make_random_params(c["n"], c["R"], seed=c["seed"], eps=c["eps"])
 
 
-def _worker(rank, world, port, case, q, serial=False, extra=None):
+def _worker(rank, world, port, case, q, serial=False, extra=None, env=None):
     import torch.distributed as dist
     if serial:  # per-mode eigensolves one after another instead of concurrent + comm thread
         os.environ["RHOSVD_SERIAL_MODES"] = "1"
+    os.environ.update(env or {})
     os.environ["MASTER_ADDR"] = "127.0.0.1"
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
@@ -115,3 +116,36 @@ def test_r_sharded_world2_one_gpu(case, serial, extra):
         assert sigma_rel_err(g0["sigma"][l], one.sigma[l].cpu().numpy()) <= 1e-11
     d1, n1 = tucker_diff(g0["beta"], g0["Z"], one.beta.cpu().numpy(), [z.cpu().numpy() for z in one.Z])
     assert d1 <= 1e-10 * n1
+
+
+def _run_world2(case, env):
+    import torch.multiprocessing as mp
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, 2, port, case, q, False, None, env)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    out = {}
+    for _ in range(2):
+        d = q.get(timeout=180)
+        out[d["rank"]] = d
+    for pr in procs:
+        pr.join(timeout=120)
+        assert pr.exitcode == 0
+    return out
+
+
+@pytest.mark.parametrize("case", ["random", "cfg2"])
+def test_mode_parallel_matches_replicated(case):
+    """Mode parallelism (the subspace iteration of mode l on rank l mod 2 only, its block
+    broadcast) computes exactly what the replicated solve computes: bitwise equal outputs
+    on both ranks, and equal to RHOSVD_MODE_PARALLEL=0."""
+    par = _run_world2(case, {"RHOSVD_MODE_PARALLEL": "1"})
+    rep = _run_world2(case, {"RHOSVD_MODE_PARALLEL": "0"})
+    for r in (0, 1):
+        assert par[r]["ranks"] == rep[r]["ranks"]
+        assert np.array_equal(par[r]["beta"], rep[r]["beta"])
+        for l in range(3):
+            assert np.array_equal(par[r]["Z"][l], rep[r]["Z"][l])
+            assert np.array_equal(par[r]["sigma"][l], rep[r]["sigma"][l])
