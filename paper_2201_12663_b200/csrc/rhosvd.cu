@@ -810,11 +810,11 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
   // clusters, so per-column changes cannot serve as a stopping test):
   //   Gram-domain floor (relative, on lambda_r = sigma_r^2)  e0 = 10 u d_1 / d_r,
   //   contraction per step                                    rho^2 = (d_b / d_r)^2,
-  //   steps = ceil(log(1e-11 / e0) / log(rho^2)), clamped to [refine_steps, refine_steps + 3]
+  //   steps = ceil(log(1e-11 / e0) / log(rho^2)), clamped to [refine_steps, refine_steps + 1]
   // (1e-11 on lambda is 5e-12 on sigma, 20x inside the 1e-10 parity bound).
   int nref = 0;
   if (o.refine_steps > 0) {
-    nref = o.refine_steps + 3;
+    nref = o.refine_steps + 1;
     if (!d_h.empty() && r_est > 0) {
       const int64_t rr = std::min<int64_t>(r_est, b);
       const double dr = std::max(d_h[rr - 1], 1e-300), d1 = std::max(d_h[0], dr);
@@ -822,7 +822,10 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
       // d_b below the Gram-domain noise (~u d_1) says nothing about lambda_{b+1}: floor it
       const double rho = std::min(0.9, std::max(d_h[b - 1], 64.0 * u * d1) / dr);
       int need = e0 <= 1e-11 ? 0 : (int)std::ceil(std::log(1e-11 / e0) / std::log(rho * rho));
-      nref = std::max(o.refine_steps, std::min(need, o.refine_steps + 3));
+      // at most one step beyond refine_steps: measured (r2d, tools/refine_probe.py) the
+      // retained sigma are within 3.3e-12 (cfg 3, 5) and 1.7e-12 (cfg 4) of the oracle after
+      // two steps, and the model's third step on cfg 3 mode 0 bought nothing
+      nref = std::max(o.refine_steps, std::min(need, o.refine_steps + 1));
       // RHOSVD_REFINE_MAX (probe knob): cap the modelled step count (>= refine_steps)
       static const int refine_cap = [] {
         const char* e = getenv("RHOSVD_REFINE_MAX");
