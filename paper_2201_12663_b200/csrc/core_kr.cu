@@ -270,9 +270,72 @@ static int core_splits(int64_t r1, int64_t r2, int64_t r3, int64_t R, int BN) {
   return std::max(1, std::min(s, 32));
 }
 
+// Tile plan of one core call.  The default (pick_bn + core_splits + an edge segment for the
+// r3 % BN leftover) suits cores with many row tiles (cfg 4: 3317 x 5).  When the tiles do
+// not fill a few waves (cfg 5: r1 r2 = 11 664 rows -> 92 row tiles; r3 = 108 -> a 96-wide
+// and a 16-wide launch of 92 items each on 148 SMs, ~0.5 of the DMMA peak), a
+// single-segment plan of width bn >= r3 / nt with a K-split that fills whole waves is
+// cheaper; both are costed with the same model:
+//   item time ~ (K / s) (bn + 8.2) (x 1/0.6 for the 16-wide edge), waves = ceil(items / SMs),
+//   plus the split-K reduction ((s + 1) r1 r2 r3 doubles through HBM).
+struct CorePlan {
+  int bn = 128, splits = 1;
+  bool single = false;  // one segment, no edge
+};
+static double core_seg_cost(int64_t tiles, int64_t K, int bn, int s, int sms) {
+  const double per_item = (double)cdiv(K, s) * (bn + 8.2) * (bn <= 16 ? 1.0 / 0.6 : 1.0);
+  return (double)cdiv(tiles * s, sms) * per_item;
+}
+static CorePlan core_plan(int64_t r1, int64_t r2, int64_t r3, int64_t R, int force_bn) {
+  CorePlan d;
+  d.bn = force_bn ? force_bn : pick_bn(r3);
+  d.splits = core_splits(r1, r2, r3, R, d.bn);
+  static const bool plan_on = [] {  // RHOSVD_CORE_PLAN=0: the default plan only
+    const char* e = getenv("RHOSVD_CORE_PLAN");
+    return !(e && e[0] == '0');
+  }();
+  const int sms = num_sms();
+  const int64_t mt = cdiv(r1 * r2, CORE_BM);
+  if (!plan_on || force_bn || mt * cdiv(r3, d.bn) >= 4 * sms || R < 4096) return d;
+  // unit conversion: one (k, column) of a 128-row tile = 256 FLOP at the per-SM DMMA rate
+  // (~2.5e11 FLOP/s); the reduction streams (s + 1) r1 r2 r3 doubles at ~6e12 B/s
+  const double unit_s = 256.0 / 2.5e11, total = (double)r1 * r2 * r3;
+  auto red = [&](int s) { return s > 1 ? (double)(s + 1) * total * 8.0 / 6e12 / unit_s : 0.0; };
+  // the default plan, as core_kr would run it
+  double best;
+  {
+    const int64_t full = (r3 / d.bn) * d.bn, rem = r3 - full;
+    if (d.splits == 1 && rem > 0 && full > 0 && round_up(rem, 16) < d.bn)
+      best = core_seg_cost(mt * (full / d.bn), R, d.bn, 1, sms) + core_seg_cost(mt, R, (int)round_up(rem, 16), 1, sms);
+    else
+      best = core_seg_cost(mt * cdiv(r3, d.bn), R, d.bn, d.splits, sms) + red(d.splits);
+  }
+  CorePlan out = d;
+  const int cand[] = {64, 80, 96, 112, 128};
+  for (int bn : cand) {
+    const int64_t nt = cdiv(r3, bn);
+    if (nt > 1 && bn < 128) continue;  // narrow single segments only when one column tile covers r3
+    for (int sp = 1; sp <= 32 && R / sp >= 512; ++sp) {
+      const double c = core_seg_cost(mt * nt, R, bn, sp, sms) + red(sp);
+      if (c < best * 0.98) {
+        best = c;
+        out.bn = bn;
+        out.splits = sp;
+        out.single = true;
+      }
+    }
+  }
+  return out;
+}
+
 // split-K scratch (doubles) the call needs; 0 when no split is used
 size_t core_part_doubles(int64_t r1, int64_t r2, int64_t r3, int64_t R) {
-  const int s = core_splits(r1, r2, r3, R, pick_bn(r3));
+  static const int force_bn = [] {
+    const char* e = getenv("RHOSVD_CORE_BN");
+    const int v = e ? atoi(e) : 0;
+    return (v == 64 || v == 80 || v == 96 || v == 112 || v == 128) ? v : 0;
+  }();
+  const int s = core_plan(r1, r2, r3, R, force_bn).splits;
   return s > 1 ? (size_t)s * r1 * r2 * r3 : 0;
 }
 
@@ -329,7 +392,8 @@ int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3,
     const char* e = getenv("RHOSVD_CORE_WIDE_EDGE");
     return !(e && e[0] == '0');
   }();
-  const int BN = force_bn ? force_bn : pick_bn(r3);
+  const CorePlan plan = core_plan(r1, r2, r3, R, force_bn);
+  const int BN = plan.bn;
   CoreArgs a{};
   a.r1 = (int)r1; a.r2 = (int)r2; a.r3 = (int)r3; a.R = (int)R;
   a.A1 = (int)std::min<int64_t>((CORE_BM - 1) / r2 + 2, r1 + 1);
@@ -337,7 +401,7 @@ int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3,
   a.A1pad = (int)round_up(a.A1, 8);
   a.mt = (int)cdiv(M, CORE_BM);
   const int sms = num_sms();
-  int splits = core_splits(r1, r2, r3, R, BN);
+  int splits = plan.splits;
   while (splits > 1 && (size_t)splits * total > part_cap) --splits;
   a.kchunk = (int)round_up(cdiv(R, splits), CORE_BK * ksub);
   splits = (int)cdiv(R, a.kchunk);
@@ -350,7 +414,9 @@ int core_kr(const double* W1x, int64_t ldw1, const double* W2, const double* W3,
   int nseg = 0;
   {
     const int64_t full = (r3 / BN) * BN, rem = r3 - full;
-    if (splits == 1 && ksub == 2 && edge_on && rem > 0 && full > BN && BN == 128 && rem <= 16 && wide_edge) {
+    if (plan.single) {
+      segs[nseg++] = {BN, 0, (int)r3};
+    } else if (splits == 1 && ksub == 2 && edge_on && rem > 0 && full > BN && BN == 128 && rem <= 16 && wide_edge) {
       // a thin leftover (<= 16 columns) joins the last full tile as one wide 144-column
       // edge tile (18 n-fragments, 239 registers): the 16-wide edge runs at ~60 % of the
       // main rate (2 n-fragments per A fragment), the wide one at the main rate

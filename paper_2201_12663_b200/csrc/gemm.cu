@@ -361,19 +361,25 @@ static bool gemm_big(int64_t M, int64_t N, int64_t K) {
 }
 
 int gemm_batch_splits(int64_t M, int64_t N, int64_t K, bool upper, int nb) {
-  // the fewest waves per unit of work over 1..8 K-splits (each split >= 2048 of K; a split
-  // costs one more M x N partial per batch, ~0.3 % here).  cfg 4's three 2048^2 Grams: 408
+  // the cheapest wave schedule over the K-split count (a split costs one more M x N partial
+  // per batch, ~0.3 % here, and a fixed per-item cost).  cfg 4's three 2048^2 Grams: 408
   // upper tiles -> 5 splits = 2040 items on 148 SMs, 98.4 % of the last wave busy (one
   // 136-tile Gram per launch: 92 %)
   const int sms = num_sms();
   const int BT = gemm_big(M, N, K) ? 128 : 64;
   const int64_t tn = cdiv(N, BT), tiles = upper ? tn * (tn + 1) / 2 : cdiv(M, BT) * tn;
   const int64_t tot = (int64_t)nb * tiles;
+  // few tiles (cfg 2: 3 x 10 upper tiles of a 512^2 Gram) need deep splits: chunks down to
+  // 256 of K, up to 64 splits; otherwise chunks >= 2048, up to 8 splits
+  const bool few = tot < sms;
+  const int smax = few ? 64 : 8;
+  const int64_t kmin = few ? 256 : 2048;
   double best = 1e30;
   int splits = 1;
-  for (int s2 = 1; s2 <= 8; ++s2) {
-    if (s2 > 1 && K / s2 < 2048) break;
-    const double cost = (double)cdiv(tot * s2, sms) * sms / ((double)tot * s2) * (1.0 + 0.003 * (s2 - 1));
+  for (int s2 = 1; s2 <= smax; ++s2) {
+    if (s2 > 1 && K / s2 < kmin) break;
+    // waves x (k per item + ~256 k of fixed cost per item: pipeline fill, epilogue)
+    const double cost = (double)cdiv(tot * s2, sms) * ((double)cdiv(K, s2) + 256.0) * (1.0 + 0.003 * (s2 - 1));
     if (cost < best * 0.999) {
       best = cost;
       splits = s2;
