@@ -721,7 +721,13 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     if (epsmode && r_est + p > b && guard < 12) {
       // grow towards the predicted size, at most 2x per event (the log-linear tail
       // extrapolation of a small block overshoots: 128 -> r_est 1093 on cfg 4)
-      int64_t bn = std::min<int64_t>(m, std::min<int64_t>(2 * b, std::max<int64_t>((int64_t)(1.15 * r_est) + p, b + p)));
+      // (RHOSVD_GROW_MAX: the per-event growth factor cap, default 2)
+      static const int grow_max = [] {
+        const char* e = getenv("RHOSVD_GROW_MAX");
+        return e ? std::max(2, atoi(e)) : 2;
+      }();
+      int64_t bn = std::min<int64_t>(m, std::min<int64_t>((int64_t)grow_max * b,
+                                                           std::max<int64_t>((int64_t)(1.15 * r_est) + p, b + p)));
       if (dbg_on()) fprintf(stderr, "[rhosvd dbg] mode %d grow b %lld -> %lld (r_est %lld)\n", mode, (long long)b, (long long)bn, (long long)r_est);
       RH_CHECK(ensure_b(bn));
       RH_CHECK(k_random(w.Z.p, LDN, n, b, bn, seed + 7919ull * (uint64_t)(it_total + 1), st));
@@ -1464,7 +1470,11 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
             const char* e = getenv("RHOSVD_COOP_MODE_CAP");
             return e ? std::max(0, atoi(e)) : 2;
           }();
-          g_coop_cap = per2 ? std::max(1, num_sms() * per2 / 2) : 0;
+          static const int ctas = [] {  // RHOSVD_COOP_MODE_CTAS: absolute cap (probe knob)
+            const char* e = getenv("RHOSVD_COOP_MODE_CTAS");
+            return e ? std::max(0, atoi(e)) : 0;
+          }();
+          g_coop_cap = ctas ? ctas : (per2 ? std::max(1, num_sms() * per2 / 2) : 0);
         }
         ~CapGuard() { g_coop_cap = 0; }
       } cap_guard;
