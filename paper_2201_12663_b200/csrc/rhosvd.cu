@@ -858,6 +858,41 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     RH_CHECK(mm(c, n, b, Rl, Uh, LDN, false, w.W.p, Rp, true, w.M.p, LDN));
     TL().mark(mode, "M = Uhat W^T", st);
     RH_CHECK(allreduce(c, w.M.p, LDN * b));
+    // A-posteriori stopping test before the last modelled step (RHOSVD_REFINE_ADAPT=1,
+    // reported with RHOSVD_DEBUG): the Rayleigh-Ritz residual of the current block,
+    // R = M - Z (Z^T M) = (I - Z Z^T) G Z (non-squared: M came from Uhat), gives the
+    // subspace angle of column j as ||r_j|| / c_jj (c = Z^T M); the step about to be taken
+    // contracts it by rho_j = c_bb / c_jj, and the final Ritz value errs by about its
+    // square:  e = max_{j <= r} (rho_j ||r_j|| / c_jj)^2.  If e is already below the
+    // target, this is the last step.  Costs two b x b x n GEMMs per test.
+    static const int adapt = [] {
+      const char* e = getenv("RHOSVD_REFINE_ADAPT");
+      return e ? atoi(e) : 0;
+    }();
+    if ((adapt || dbg_on()) && b > 1) {
+      const int64_t ldb2 = ldbs(b);
+      RH_CHECK(mm(c, b, b, n, w.Z.p, LDN, true, w.M.p, LDN, true, w.S.p, ldb2));  // C = Z^T M
+      RH_CUDA(cudaMemcpyAsync(w.T1.p, w.M.p, (size_t)LDN * b * sizeof(double), cudaMemcpyDeviceToDevice, st));
+      GemmArgs gr;
+      gr.M = n; gr.N = b; gr.K = b; gr.A = w.Z.p; gr.lda = LDN; gr.a_k = false; gr.B = w.S.p; gr.ldb = ldb2;
+      gr.b_k = true; gr.C = w.T1.p; gr.ldc = LDN; gr.alpha = -1.0; gr.beta = 1.0;
+      RH_CHECK(gemm(gr, w.gsc, st, &c.flops));                                          // R = M - Z C
+      RH_CHECK(k_coldot(w.T1.p, w.T1.p, LDN, n, b, w.inv.p, st));                       // ||r_j||^2
+      RH_CHECK(k_coldot(w.Z.p, w.M.p, LDN, n, b, w.tail2.p, st));                       // c_jj
+      std::vector<double> rn(b), cd(b);
+      RH_CHECK(d2h_wait(rn.data(), w.inv.p, b * sizeof(double), st));
+      RH_CHECK(d2h_wait(cd.data(), w.tail2.p, b * sizeof(double), st));
+      const int64_t jr = std::max<int64_t>(1, std::min<int64_t>(r_est > 0 ? r_est : b, b));
+      double est = 0.0;
+      for (int64_t j = 0; j < jr; ++j) {
+        const double cj = std::max(cd[j], 1e-300), rho = std::min(1.0, std::max(cd[b - 1], 0.0) / cj);
+        est = std::max(est, rho * rho * std::max(rn[j], 0.0) / (cj * cj));
+      }
+      if (dbg_on())
+        fprintf(stderr, "[rhosvd dbg] mode %d refine step %d: a-posteriori estimate %.3e (steps planned %d)\n", mode,
+                rs + 1, est, nref);
+      if (adapt && est <= 1e-11 && rs + 1 < nref) nref = rs + 1;
+    }
     RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldb, ORTH_CQR2));
     TL().mark(mode, "refine CholQR2", st);
     ++mo.refines;
