@@ -53,10 +53,10 @@ int h2d_wait(void* dst, const void* src, size_t bytes, cudaStream_t st);
 // count of kernels launched by the library (per-thread; reset by rhosvd_c2t)
 extern thread_local int g_launches;
 // cap on cooperative grids launched from this thread (0 = none): the three concurrent
-// per-mode solves share the GPU, so each caps its grid-synchronised kernels at one CTA per
-// SM (RHOSVD_COOP_MODE_CAP, in CTAs per 2 SMs, default 2).  cfg 4 eigensolve: no cap 151,
-// 1 CTA/SM 138-142, 1.5/SM 141-145, 2/SM 147-149 ms: a full-GPU cooperative grid blocks
-// the other modes' kernels for its whole duration.
+// per-mode solves share the GPU, so each caps its grid-synchronised kernels at a third of
+// the SMs by default (rhosvd.cu CapGuard; RHOSVD_COOP_MODE_CTAS / RHOSVD_COOP_MODE_CAP).
+// History: a full-GPU cooperative grid blocks the other modes' kernels for its whole
+// duration (cfg 4 eigensolve: no cap 151 ms, 1 CTA/SM 138-142 ms, a third of the SMs 126).
 extern thread_local int g_coop_cap;
 inline void count_launch(int k = 1) { g_launches += k; }
 

@@ -858,18 +858,21 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     RH_CHECK(mm(c, n, b, Rl, Uh, LDN, false, w.W.p, Rp, true, w.M.p, LDN));
     TL().mark(mode, "M = Uhat W^T", st);
     RH_CHECK(allreduce(c, w.M.p, LDN * b));
-    // A-posteriori stopping test before the last modelled step (RHOSVD_REFINE_ADAPT=1,
-    // reported with RHOSVD_DEBUG): the Rayleigh-Ritz residual of the current block,
+    // A-posteriori stopping test before the last modelled step (default on;
+    // RHOSVD_REFINE_ADAPT=0 runs the modelled count): the Rayleigh-Ritz residual of the current block,
     // R = M - Z (Z^T M) = (I - Z Z^T) G Z (non-squared: M came from Uhat), gives the
     // subspace angle of column j as ||r_j|| / c_jj (c = Z^T M); the step about to be taken
     // contracts it by rho_j = c_bb / c_jj, and the final Ritz value errs by about its
     // square:  e = max_{j <= r} (rho_j ||r_j|| / c_jj)^2.  If e is already below the
     // target, this is the last step.  Costs two b x b x n GEMMs per test.
+    // Measured (r2i, tools/refine_probe.py): after step 1 the estimate is 6e-16 - 1.9e-12
+    // on cfg 3 / 5 (one step suffices: sigma within 3.4e-12 of the oracle) and 1e-10 -
+    // 2e-10 on cfg 4 (two steps: 1.7e-12; one step would leave 2.9e-11).
     static const int adapt = [] {
       const char* e = getenv("RHOSVD_REFINE_ADAPT");
-      return e ? atoi(e) : 0;
+      return e ? atoi(e) : 1;
     }();
-    if ((adapt || dbg_on()) && b > 1) {
+    if (((adapt && rs + 1 < nref) || dbg_on()) && b > 1) {
       const int64_t ldb2 = ldbs(b);
       RH_CHECK(mm(c, b, b, n, w.Z.p, LDN, true, w.M.p, LDN, true, w.S.p, ldb2));  // C = Z^T M
       RH_CUDA(cudaMemcpyAsync(w.T1.p, w.M.p, (size_t)LDN * b * sizeof(double), cudaMemcpyDeviceToDevice, st));
@@ -1499,17 +1502,23 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
     auto run = [&](int l) {
       cudaSetDevice(dev);
       g_launches = 0;
-      struct CapGuard {  // cooperative grids of this mode: 1.5 CTAs per SM (see common.cuh)
+      struct CapGuard {  // cooperative grids of this mode (see common.cuh)
         CapGuard() {
-          static const int per2 = [] {  // RHOSVD_COOP_MODE_CAP: CTAs per 2 SMs (0 = no cap)
+          // default: a third of the SMs, so the three modes' grid-synchronised kernels
+          // (block Jacobi, blocked Cholesky) run side by side instead of one after another
+          // (r2h: cfg 2 eigensolve 8.4 -> 7.7 ms, cfg 4 129 -> 126 ms).  RHOSVD_COOP_MODE_CTAS
+          // sets an absolute cap; RHOSVD_COOP_MODE_CAP a cap in CTAs per 2 SMs (0 = none).
+          static const int per2 = [] {
             const char* e = getenv("RHOSVD_COOP_MODE_CAP");
-            return e ? std::max(0, atoi(e)) : 2;
+            return e ? std::max(0, atoi(e)) : -1;
           }();
-          static const int ctas = [] {  // RHOSVD_COOP_MODE_CTAS: absolute cap (probe knob)
+          static const int ctas = [] {
             const char* e = getenv("RHOSVD_COOP_MODE_CTAS");
             return e ? std::max(0, atoi(e)) : 0;
           }();
-          g_coop_cap = ctas ? ctas : (per2 ? std::max(1, num_sms() * per2 / 2) : 0);
+          g_coop_cap = ctas ? ctas
+                            : per2 < 0 ? std::max(1, num_sms() / 3)
+                                       : (per2 ? std::max(1, num_sms() * per2 / 2) : 0);
         }
         ~CapGuard() { g_coop_cap = 0; }
       } cap_guard;
