@@ -1273,18 +1273,19 @@ __global__ void __launch_bounds__(1024, 1) chol_small_kernel(int b, const double
         depf[c] = dep ? 1 : 0;
       }
       if (!dep) {
+        // blocks left of column block Cb are final (k < 32 Cb <= c): only A, C >= Cb update
         const double rd = 1.0 / d;
         double ci[E], ck[E];
 #pragma unroll
-        for (int A = 0; A < E; ++A) {
+        for (int A = Cb; A < E; ++A) {
           const int i = ty + 32 * A, k = tx + 32 * A;
           ci[A] = (i > c && i < b) ? col[i] * rd : 0.0;
           ck[A] = (k > c && k < b) ? col[k] : 0.0;
         }
 #pragma unroll
-        for (int A = 0; A < E; ++A)
+        for (int A = Cb; A < E; ++A)
 #pragma unroll
-          for (int C = 0; C <= A; ++C) a[A][C] = fma(-ci[A], ck[C], a[A][C]);
+          for (int C = Cb; C <= A; ++C) a[A][C] = fma(-ci[A], ck[C], a[A][C]);
       }
     }
   }
@@ -1329,16 +1330,19 @@ __global__ void __launch_bounds__(1024, 1) chol_small_kernel(int b, const double
         }
       }
       __syncthreads();
+      double xv[E];  // x_rc for this thread's columns c = tx + 32 C <= r (0 beyond r)
+#pragma unroll
+      for (int C = 0; C <= Rb; ++C) {
+        const int c = tx + 32 * C;
+        xv[C] = (c <= r) ? xrow[c] : 0.0;
+      }
 #pragma unroll
       for (int A = Rb; A < E; ++A) {
         const int i = ty + 32 * A;
         if (i > r && i < b) {
           const double l = Ls[i * P + r];
 #pragma unroll
-          for (int C = 0; C <= Rb; ++C) {
-            const int c = tx + 32 * C;
-            if (c <= r) a[A][C] = fma(-l, xrow[c], a[A][C]);
-          }
+          for (int C = 0; C <= Rb; ++C) a[A][C] = fma(-l, xv[C], a[A][C]);
         }
       }
     }

@@ -32,6 +32,7 @@ def _free_port():
 CASES = {
     "random": dict(n=70, R=517, seed=23, eps=1e-7),
     "cfg2": dict(config=2),
+    "cfg3": dict(config=3),
 }
 
 
@@ -67,8 +68,8 @@ def _worker(rank, world, port, case, q, serial=False, extra=None, env=None):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("case,serial,extra", [("random", False, None), ("cfg2", False, None), ("random", True, None),
-                                               ("random", False, {"root_only_core": True})])
+@pytest.mark.parametrize("case,serial,extra", [("random", False, None), ("cfg2", False, None), ("cfg3", False, None),
+                                               ("random", True, None), ("random", False, {"root_only_core": True})])
 def test_r_sharded_world2_one_gpu(case, serial, extra):
     import torch.multiprocessing as mp
     from oracle import rhosvd as oracle_rhosvd, sigma_rel_err, tucker_diff
