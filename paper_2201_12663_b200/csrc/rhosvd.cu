@@ -728,6 +728,9 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
       }();
       int64_t bn = std::min<int64_t>(m, std::min<int64_t>((int64_t)grow_max * b,
                                                            std::max<int64_t>((int64_t)(1.15 * r_est) + p, b + p)));
+      // stay on the one-CTA Cholesky (b <= 160) when the prediction leaves room there
+      // (cfg 3: r_est 134 -> 170 would put every later CholQR on the cooperative kernel)
+      if (bn > 160 && b < 160 && r_est + p + 8 <= 160) bn = 160;
       if (dbg_on()) fprintf(stderr, "[rhosvd dbg] mode %d grow b %lld -> %lld (r_est %lld)\n", mode, (long long)b, (long long)bn, (long long)r_est);
       RH_CHECK(ensure_b(bn));
       RH_CHECK(k_random(w.Z.p, LDN, n, b, bn, seed + 7919ull * (uint64_t)(it_total + 1), st));

@@ -14,8 +14,9 @@
 //  * rhosvd_rs_split (host): K_l = {k : t_k <= 1}, K_s = {k : t_k > 1}.
 //  * rhosvd_rs_lattice (device): reference table g_k[o] = e^{-tau_k (o h)^2} on the doubled
 //    grid o = -(n-1)..(n-1) (one kernel), then every lattice column (node j, long term k)
-//    of every mode is the window g_k[i - m_{j,l}], i = 0..n-1, of that table (a coalesced
-//    gather: HBM-bound, 3 n 8 bytes written per output column), xi = c_j w_k.
+//    of every mode is the window g_k[i - m_{j,l}], i = 0..n-1, of that table (one warp per
+//    column, a coalesced gather: HBM-bound, 3 n 8 bytes written per output column; the
+//    table, R_l (2n - 1) doubles, stays in L2), xi = c_j w_k.
 #include <cmath>
 #include <cstring>
 
@@ -43,14 +44,17 @@ __global__ void rs_reference_kernel(const RsRef p, double* g, int64_t ldg) {
   g[k * ldg + o] = exp(-p.tau[k] * (d * d));
 }
 
-// one CTA row of 256 threads per output column (j, k), all three modes; xi = c_j w_k
+// one warp per output column (j, k), all three modes (8 columns per 256-thread CTA); the
+// lanes stream the n rows: every warp store is one coalesced 256-byte segment
 __global__ void __launch_bounds__(256) rs_window_kernel(const RsRef p, const double* __restrict__ g, int64_t ldg,
                                                          const int32_t* __restrict__ node_idx,
                                                          const double* __restrict__ c, int64_t N,
                                                          double* __restrict__ U1, double* __restrict__ U2,
                                                          double* __restrict__ U3, int64_t ldu,
                                                          double* __restrict__ xi) {
-  const int64_t col = blockIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t col = (int64_t)blockIdx.x * 8 + (threadIdx.x >> 5);
+  if (col >= N * p.Rl) return;
   const int64_t j = col / p.Rl;
   const int k = (int)(col - j * p.Rl);
   const double* gk = g + k * ldg + (p.n - 1);
@@ -61,15 +65,15 @@ __global__ void __launch_bounds__(256) rs_window_kernel(const RsRef p, const dou
     double* dst = U[l] + col * ldu;
     if (m >= 0 && m < p.n) {
       const double* src = gk - m;
-      for (int i = threadIdx.x; i < p.n; i += blockDim.x) dst[i] = src[i];
+      for (int i = lane; i < p.n; i += 32) dst[i] = src[i];
     } else {  // a node off the grid: its window is read only where it overlaps the table
-      for (int i = threadIdx.x; i < p.n; i += blockDim.x) {
+      for (int i = lane; i < p.n; i += 32) {
         const int64_t o = (int64_t)i - m + (p.n - 1);
         dst[i] = (o >= 0 && o < 2LL * p.n - 1) ? gk[(int64_t)i - m] : 0.0;
       }
     }
   }
-  if (threadIdx.x == 0) xi[col] = c[j] * p.w[k];
+  if (lane == 0) xi[col] = c[j] * p.w[k];
 }
 
 }  // namespace rhosvd
@@ -141,7 +145,7 @@ int rhosvd_rs_lattice(const double* tau_l, const double* w_l, int64_t R_l, doubl
   count_launch();
   cudaError_t e = cudaGetLastError();
   if (e == cudaSuccess) {
-    rs_window_kernel<<<(unsigned)(N * R_l), 256, 0, st>>>(p, g, ldg, node_idx, c, N, U1, U2, U3, ldu, xi);
+    rs_window_kernel<<<(unsigned)cdiv(N * R_l, 8), 256, 0, st>>>(p, g, ldg, node_idx, c, N, U1, U2, U3, ldu, xi);
     count_launch();
     e = cudaGetLastError();
   }
