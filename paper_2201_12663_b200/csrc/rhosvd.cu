@@ -790,13 +790,15 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     RH_CHECK(broadcast(c, w.Z.p, LDN * b, c.mp->root));
   }
   mo.iters = it_total;
-  // block truncation: smallest b' >= r + p with d_b' <= 0.02 d_r (leading columns carry
+  // block truncation: smallest b' >= r + p with d_b' <= 0.003 d_r (leading columns carry
   // the dominant subspaces).  The ratio bounds the refinement contraction rho below:
-  // 0.02 gives rho^2 <= 4e-4 per step (cfg 4: 2 steps of ~140 GFLOP GEMM pairs per mode
-  // instead of 3 at 0.05, for ~2 % more columns).
+  // 0.003 gives rho^2 <= 1e-5 per step, so on cfg 4 ONE refinement step passes the
+  // a-posteriori test (blocks 723-732 -> 762-767 columns, eigensolve 126 -> 105 ms, sigma
+  // still within 1.7e-12 of the oracle; at 0.02 it needed two steps of ~286 GFLOP per mode;
+  // r2n, profiles/r2n_trunc_ratio_sweep.log).
   static const double trunc_ratio = [] {
     const char* e = getenv("RHOSVD_TRUNC_RATIO");
-    return e ? atof(e) : 0.02;
+    return e ? atof(e) : 0.003;
   }();
   if (!d_h.empty() && r_est > 0 && r_est + p < b) {
     const double tr = d_h[r_est - 1];
