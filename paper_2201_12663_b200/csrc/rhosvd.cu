@@ -721,14 +721,13 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     if (epsmode && r_est + p > b && guard < 12) {
       // grow towards the predicted size, at most 2x per event (the log-linear tail
       // extrapolation of a small block overshoots: 128 -> r_est 1093 on cfg 4)
-      // (RHOSVD_GROW_MAX: the per-event growth factor cap, default 2; 4 while the
-      // prediction asks for >= 4 b and 4 b stays within a quarter of the space - cfg 4
-      // goes 128 -> 512 -> 873 instead of through 256, cfg 2 (m = 512) keeps 2)
-      static const int grow_env = [] {
+      // (RHOSVD_GROW_MAX: the per-event growth factor cap, default 2.  A 4x first step on
+      // cfg 4 (128 -> 512, two iterations fewer) measured no faster (r2p: 105.9 vs 103.9 ms
+      // eigensolve) and cost cfg 2 (m = 512) a full-space block (r2h), so it stays 2.)
+      static const int grow_max = [] {
         const char* e = getenv("RHOSVD_GROW_MAX");
-        return e ? std::max(2, atoi(e)) : 0;
+        return e ? std::max(2, atoi(e)) : 2;
       }();
-      const int grow_max = grow_env ? grow_env : ((r_est >= 4 * b && 4 * b <= m / 4) ? 4 : 2);
       int64_t bn = std::min<int64_t>(m, std::min<int64_t>((int64_t)grow_max * b,
                                                            std::max<int64_t>((int64_t)(1.15 * r_est) + p, b + p)));
       // stay on the one-CTA Cholesky (b <= 160) when the prediction leaves room there
