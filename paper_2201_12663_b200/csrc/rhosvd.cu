@@ -482,12 +482,20 @@ struct ModeLatch {
 struct MPar {
   bool owner = false;
   int root = 0;
-  ModeLatch* latch = nullptr;
-  bool signalled = false;
-  void signal() {  // an owner's solve is over (once, on every path)
+  ModeLatch* latch = nullptr;   // subspace iterations (S3)
+  ModeLatch* latch2 = nullptr;  // final Rayleigh-Ritz Jacobi (S4)
+  int owned = 1;  // modes this rank owns
+  bool signalled = false, signalled2 = false;
+  void signal() {  // an owner's subspace iteration is over (once, on every path)
     if (owner && !signalled) {
       signalled = true;
       latch->done();
+    }
+  }
+  void signal2() {  // an owner's Jacobi is over (once, on every path)
+    if (owner && !signalled2) {
+      signalled2 = true;
+      latch2->done();
     }
   }
 };
@@ -920,11 +928,38 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     RH_CHECK(allreduce(c, w.S.p, ldb * b));
     TL().mark(mode, "W W^T", st);
     c.tm->mark(PH_RR);
-    {
+    if (!c.mp) {
       int sw = 0;
       RH_CHECK(syevj(b, w.S.p, ldb, w.th.p, w.V.p, ldb, 1e-15, 1e-300, 80, w.dws, st, &sw));
       if (dbg_on()) fprintf(stderr, "[rhosvd dbg] mode %d rr b %lld sweeps %d\n", mode, (long long)b, sw);
       if (sw < 0) return fail(RHOSVD_ENOCONV, "Jacobi on W W^T did not converge");
+      TL().mark(mode, "Jacobi", st);
+    } else {
+      // mode parallelism: the b x b Jacobi of mode l (replicated input after the all-reduce)
+      // runs on its owner rank with the whole GPU; [status, sweeps], the eigenvalues and the
+      // eigenvectors go out by broadcast once every Jacobi this rank owns has finished
+      int st_j = RHOSVD_OK, sw = 0;
+      std::string err_j;
+      if (c.mp->owner) {
+        // the rank's owned Jacobis share the GPU (p >= 3: one Jacobi with every SM)
+        const int cap_saved = g_coop_cap;
+        g_coop_cap = std::max(1, num_sms() / std::max(1, c.mp->owned));
+        st_j = syevj(b, w.S.p, ldb, w.th.p, w.V.p, ldb, 1e-15, 1e-300, 80, w.dws, st, &sw);
+        g_coop_cap = cap_saved;
+        if (st_j != RHOSVD_OK) err_j = g_err;
+        else if (sw < 0) st_j = RHOSVD_ENOCONV, err_j = "Jacobi on W W^T did not converge";
+        c.mp->signal2();
+      }
+      c.mp->latch2->wait();
+      double h2[2] = {(double)st_j, (double)sw};
+      if (c.mp->owner) RH_CHECK(h2d_wait(w.H.p, h2, sizeof(h2), st));
+      RH_CHECK(broadcast(c, w.H.p, 2, c.mp->root));
+      RH_CHECK(d2h_wait(h2, w.H.p, sizeof(h2), st));
+      if ((int)h2[0] != RHOSVD_OK)
+        return fail((int)h2[0], c.mp->owner ? err_j : "mode " + std::to_string(mode) + ": owner rank's Jacobi failed");
+      RH_CHECK(broadcast(c, w.th.p, b, c.mp->root));
+      RH_CHECK(broadcast(c, w.V.p, ldb * b, c.mp->root));
+      if (dbg_on()) fprintf(stderr, "[rhosvd dbg] mode %d rr b %lld sweeps %d (rank %d)\n", mode, (long long)b, (int)h2[1], c.mp->root);
       TL().mark(mode, "Jacobi", st);
     }
     c.tm->mark(PH_RANK);
@@ -1449,7 +1484,7 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
       const char* e = getenv("RHOSVD_MODE_PARALLEL");
       return !(e && e[0] == '0');
     }();
-    ModeLatch latch;
+    ModeLatch latch, latch2;
     MPar mpar[3];
     const bool mode_parallel = mpar_on && sched && !streamed;
     if (mode_parallel)
@@ -1457,8 +1492,11 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
         mpar[l].root = l % comm->world;
         mpar[l].owner = mpar[l].root == comm->rank;
         mpar[l].latch = &latch;
-        if (mpar[l].owner) ++latch.pending;
+        mpar[l].latch2 = &latch2;
+        if (mpar[l].owner) ++latch.pending, ++latch2.pending;
       }
+    if (mode_parallel)
+      for (int l = 0; l < 3; ++l) mpar[l].owned = std::max(1, latch.pending);
     double mflops[3] = {0, 0, 0};
     int mlaunch[3] = {0, 0, 0};
     double mphase[3][16] = {{0}};
@@ -1547,7 +1585,7 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
         }
       }
       mst[l] = solve_mode(cl, l, n, LDN, Rl, Rp, Rg, Uh[l], w.G.p + (size_t)l * LDN * LDN, rep.trace[l], o, mo[l]);
-      if (cl.mp) cl.mp->signal();  // an early error must not leave the other modes waiting
+      if (cl.mp) cl.mp->signal(), cl.mp->signal2();  // an early error must not leave the other modes waiting
       if (cl.sched) cl.sched->finish(l);
       mtm.mark(-1);
       if (mst[l] != RHOSVD_OK) merr[l] = g_err;
