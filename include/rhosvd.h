@@ -37,8 +37,11 @@
  * *out handle is set to NULL and rhosvd_last_error() (thread-local) holds a
  * message.  In multi-rank mode every rank returns the same status.
  *
- * Thread safety: calls on different streams/handles may run concurrently;
- * one rhosvd_comm must not be used by two calls at once.
+ * Thread safety: calls on different streams/handles may be made concurrently
+ * from several threads; the library serialises them (host side by a mutex,
+ * device side by making each call's stream wait for the previous call's work,
+ * since workspaces are process-wide).  One rhosvd_comm must not be used by two
+ * calls at once.
  *
  * Devices: one CUDA device per process.  The first call pins the current device
  * (workspaces, output caches and kernel attributes are process-wide); a call made

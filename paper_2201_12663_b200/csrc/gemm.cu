@@ -41,6 +41,7 @@ struct GParams {
   int a_koff, b_koff;     // k-coordinate shift of batch b's operands (b * koff)
   int64_t c_bstride;      // C offset of batch b (doubles)
   int stages;
+  int* ctr;  // [0] next dynamic item - gridDim.x, [1] CTAs finished (self-resetting)
   uint32_t a_bytes, stage_bytes, tx_bytes;
   uint32_t b_bytes;  // one k-slab of B (the stage holds KS slabs of A, then KS of B)
 };
@@ -68,10 +69,26 @@ __global__ void __launch_bounds__(GTHREADS, 1)
       tn = tile / p.tiles_m;
     }
   };
-  // producer cursor over this CTA's k-slab stream
-  int pit = blockIdx.x, pk = 0, pkend = 0, pm = 0, pn = 0, pka = 0, pkb = 0;
+  // Dynamic item schedule: a CTA's first item is blockIdx.x, later ones come from a global
+  // counter (p.ctr[0], self-resetting: the last CTA to leave zeroes it).  With three
+  // concurrent per-mode eigensolves a GEMM shares the GPU with the other modes'
+  // latency-bound kernels; under the former static stride (item += gridDim.x) the CTAs
+  // that could only start once those kernels left an SM still owned their items, and the
+  // GEMM ended late.  Every item's result is written to its own slot (C tile, split-K
+  // partial or residual partial), so the schedule does not change any bit of the output.
+  // The producer records the item of every ring stage it fills in slot[stage]; consumers
+  // read it at each item's first k-step (after the stage's full-barrier wait, which
+  // orders it); slot = -1 (a stage armed without data) ends the loop.
+  int* slot = (int*)(empty + p.stages);
+  int pit = blockIdx.x, pk = 0, pkend = 0, pm = 0, pn = 0, pka = 0, pkb = 0, pnext = 0;
+  bool pdone = false, pend_sent = false;
   auto set_item = [&]() {
-    if (pit >= p.items) return;
+    if (pit >= p.items) {
+      pdone = true;
+      return;
+    }
+    // the item after this one, fetched now so the atomic's latency is off the TMA path
+    pnext = (int)gridDim.x + atomicAdd(p.ctr, 1);
     const int bt = pit / p.per_batch, rit = pit - bt * p.per_batch;
     const int split = rit / p.tiles;
     int tm, tn;
@@ -82,10 +99,26 @@ __global__ void __launch_bounds__(GTHREADS, 1)
     pkend = min(p.K, pk + p.kchunk);
     pka = bt * p.a_koff;
     pkb = bt * p.b_koff;
+    if (p.epi == EPI_RESID) {
+      // the residual form reads the item's D tile at its start: prefetch it to L2 now,
+      // one or more k-steps before the consumers get there
+      const int rows = min(BM, p.M - pm) & ~1;
+      if (rows > 0)
+        for (int c = 0; c < BN && pn + c < p.N; ++c)
+          l2_prefetch_bulk(p.D + (int64_t)(pn + c) * p.ldd + pm, (uint32_t)rows * 8u);
+    }
   };
   auto issue_next = [&](int stage) {
-    if (pit >= p.items) return;
+    if (pdone) {
+      if (!pend_sent) {  // end marker: arm the stage with no data
+        pend_sent = true;
+        slot[stage] = -1;
+        mbar_arrive(&full[stage]);
+      }
+      return;
+    }
     unsigned char* st = ring + (size_t)stage * p.stage_bytes;
+    slot[stage] = pit;
     mbar_arrive_expect_tx(&full[stage], p.tx_bytes);
 #pragma unroll
     for (int j = 0; j < KS; ++j) {
@@ -99,7 +132,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
     }
     pk += GBK * KS;
     if (pk >= pkend) {
-      pit += gridDim.x;
+      pit = pnext;
       set_item();
     }
   };
@@ -137,7 +170,17 @@ __global__ void __launch_bounds__(GTHREADS, 1)
   // incrementally: no integer division on the per-stage path
   uint32_t cs = 0, cph = 0;
   const uint32_t nst = (uint32_t)p.stages;
-  for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
+  while (true) {
+    // first k-step of the next item: refill the previous stage, wait for this one, read
+    // its item (the loop below starts on the stage already waited for)
+    if (producer && g >= 1) {
+      const uint32_t sp = cs == 0 ? nst - 1 : cs - 1, php = cs == 0 ? cph ^ 1u : cph;
+      mbar_wait(&empty[sp], php);
+      issue_next((int)sp);
+    }
+    mbar_wait(&full[cs], cph);
+    const int it = *(volatile int*)&slot[cs];
+    if (it < 0) break;
     const int bt = it / p.per_batch, rit = it - bt * p.per_batch;
     const int split = rit / p.tiles;
     int tm, tn;
@@ -146,18 +189,36 @@ __global__ void __launch_bounds__(GTHREADS, 1)
     const int m0 = tm * BM, n0 = p.n_off + tn * BN;
     const int kbeg = split * p.kchunk, kend = min(p.K, kbeg + p.kchunk);
     double acc[FM][FN][2];
+    if (p.epi == EPI_RESID) {
+      // residual form: the accumulators start at -D, so after the k-loop they hold
+      // op(A)op(B) - D and the epilogue is a sum of squares with no global loads (the
+      // short-K residual GEMM used to stall on its D loads after the last DMMA); the
+      // producer prefetched the D tile to L2 when it fetched the item.
 #pragma unroll
-    for (int i = 0; i < FM; ++i)
+      for (int i = 0; i < FM; ++i)
 #pragma unroll
-      for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+        for (int j = 0; j < FN; ++j)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int m = m0 + wm0 + i * 8 + fr, n = n0 + wn0 + j * 8 + 2 * fc + h;
+            acc[i][j][h] = (m < p.M && n < p.N) ? -p.D[(int64_t)n * p.ldd + m] : 0.0;
+          }
+    } else {
+#pragma unroll
+      for (int i = 0; i < FM; ++i)
+#pragma unroll
+        for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
+    }
     for (int k0 = kbeg; k0 < kend; k0 += GBK * KS, ++g) {
-      if (producer && g >= 1) {
-        const uint32_t sp = cs == 0 ? nst - 1 : cs - 1, php = cs == 0 ? cph ^ 1u : cph;
-        mbar_wait(&empty[sp], php);
-        issue_next((int)sp);
+      if (k0 != kbeg) {
+        if (producer) {
+          const uint32_t sp = cs == 0 ? nst - 1 : cs - 1, php = cs == 0 ? cph ^ 1u : cph;
+          mbar_wait(&empty[sp], php);
+          issue_next((int)sp);
+        }
+        mbar_wait(&full[cs], cph);
       }
       const uint32_t s = cs;
-      mbar_wait(&full[s], cph);
 #pragma unroll
       for (int js = 0; js < KS; ++js) {
       const uint32_t sa = ring_s + s * p.stage_bytes + js * p.a_bytes;
@@ -189,19 +250,14 @@ __global__ void __launch_bounds__(GTHREADS, 1)
 
     // ---- epilogue
     if (p.epi == EPI_RESID) {
+      // acc = op(A)op(B) - D (zero outside the matrix: zero-filled operands, zero start)
       double ss = 0.0;
 #pragma unroll
       for (int i = 0; i < FM; ++i)
 #pragma unroll
         for (int j = 0; j < FN; ++j)
 #pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            int m = m0 + wm0 + i * 8 + fr, n = n0 + wn0 + j * 8 + 2 * fc + h;
-            if (m < p.M && n < p.N) {
-              double e = p.D[(int64_t)n * p.ldd + m] - acc[i][j][h];
-              ss = fma(e, e, ss);
-            }
-          }
+          for (int h = 0; h < 2; ++h) ss = fma(acc[i][j][h], acc[i][j][h], ss);
       ss = warp_sum(ss);
       // per-warp partials in fixed slots; summed in fixed order by sum_fixed_order_kernel
       if (lane == 0) p.part[(int64_t)it * (GTHREADS / 32) + warp] = ss;
@@ -237,6 +293,15 @@ __global__ void __launch_bounds__(GTHREADS, 1)
             if (p.upper && m < n) Cb[(int64_t)m * p.ldc + n] = v;  // mirror (M == N)
           }
         }
+  }
+  // the last CTA out resets the schedule counter for the next launch on this scratch
+  if (tid == 0) {
+    __threadfence();
+    if (atomicAdd(p.ctr + 1, 1) == (int)gridDim.x - 1) {
+      p.ctr[0] = 0;
+      p.ctr[1] = 0;
+      __threadfence();
+    }
   }
 }
 
@@ -291,10 +356,22 @@ int Scratch::ensure(size_t doubles, cudaStream_t st) {
   cap = want;
   return RHOSVD_OK;
 }
+int Scratch::ensure_ctr(cudaStream_t st) {
+  if (ctr) return RHOSVD_OK;
+  cudaError_t e = cudaMallocAsync((void**)&ctr, 4 * sizeof(int), st);
+  if (e != cudaSuccess) {
+    ctr = nullptr;
+    return fail(RHOSVD_ENOMEM, std::string("gemm counter alloc: ") + cudaGetErrorString(e));
+  }
+  RH_CUDA(cudaMemsetAsync(ctr, 0, 4 * sizeof(int), st));
+  return RHOSVD_OK;
+}
 void Scratch::release(cudaStream_t st) {
   if (ptr) cudaFreeAsync(ptr, st);
   ptr = nullptr;
   cap = 0;
+  if (ctr) cudaFreeAsync(ctr, st);
+  ctr = nullptr;
 }
 
 // k-slabs per pipeline stage (one mbarrier round trip each): 2, RHOSVD_GEMM_KS=1 for 1
@@ -324,7 +401,8 @@ static int launch_cfg(const GemmArgs& g, GParams gp, cudaStream_t st) {
   gp.tx_bytes = KS * (a_box + b_box);
   const size_t budget = 227 * 1024 - 1024 - 256;
   gp.stages = (int)std::min<size_t>(8, budget / gp.stage_bytes);
-  const size_t smem = 1024 + (size_t)gp.stages * gp.stage_bytes + 2 * gp.stages * sizeof(uint64_t);
+  const size_t smem = 1024 + (size_t)gp.stages * gp.stage_bytes + 2 * gp.stages * sizeof(uint64_t) +
+                      gp.stages * sizeof(int);
   static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                         227 * 1024);  // per instantiation, thread-safe
   RH_CUDA(attr);
@@ -388,6 +466,40 @@ int gemm_batch_splits(int64_t M, int64_t N, int64_t K, bool upper, int nb) {
   return splits;
 }
 
+// K-split count of a single GEMM: the cheapest wave schedule, in units of one tile's
+// k-step time per SM: waves x (k per item + ~256 k of fixed per-item cost: pipeline fill,
+// epilogue) + the split-K partials' HBM round trip ((s + 1) M N doubles at ~6.5 TB/s).
+// Chunks stay >= 256 of K, at most 64 splits.  (The former rule - ~2 items per SM when
+// the tiles do not fill the GPU - ran cfg 5's M = Uhat W^T (32 tiles, K = 100 000) as
+// 10 splits = 3 waves where 9 splits fit in 2, and cfg 4's (96 tiles) as 4 splits = 3
+// waves where 3 fit in 2.)
+// Small GEMMs (< 30 GFLOP: the latency-bound Gram-domain and small-config products, which
+// run three at a time under the concurrent modes) keep the older rule, ~2 items per SM
+// when the tiles do not fill the GPU: the model's fixed cost made cfg 3's few-tile
+// products use fewer splits, and its eigensolve got 0.4 ms slower (r2p).
+static int gemm_plain_splits(int64_t tiles, int BT, int64_t M, int64_t N, int64_t K) {
+  const int sms = num_sms();
+  if (2.0 * (double)M * (double)N * (double)K < 3e10) {
+    if (tiles >= sms) return 1;
+    const int64_t want = cdiv(2LL * sms, tiles), maxs = std::max<int64_t>(1, K / 256);
+    return (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(want, maxs), 64));
+  }
+  // seconds per k-unit of one BT x BT tile on one SM at the DMMA rate (37.2 TF / 148)
+  const double t_k = 2.0 * BT * BT / (37.2e12 / 148.0);
+  double best = 1e300;
+  int splits = 1;
+  for (int s2 = 1; s2 <= 64; ++s2) {
+    if (s2 > 1 && K / s2 < 256) break;
+    double cost = (double)cdiv(tiles * s2, sms) * ((double)cdiv(K, s2) + 256.0) * (1.0 + 0.003 * (s2 - 1));
+    if (s2 > 1) cost += (double)(s2 + 1) * (double)M * (double)N * 8.0 / 6.5e12 / t_k;
+    if (cost < best * 0.999) {
+      best = cost;
+      splits = s2;
+    }
+  }
+  return splits;
+}
+
 int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
   if (g.M <= 0 || g.N <= 0) return RHOSVD_OK;
   if (g.M > INT32_MAX || g.N > INT32_MAX || g.K > INT32_MAX)
@@ -421,27 +533,7 @@ int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
   int splits = g.splits;
   if (g.epi == EPI_RESID) splits = 1;
   if (splits <= 0 && nb > 1) splits = gemm_batch_splits(g.M, g.N, g.K, g.upper_sym, nb);
-  if (splits <= 0) {
-    // persistent grid: enough work items for every SM (~2 items each), splits >= 256 of K
-    splits = 1;
-    if (gp.tiles < sms) {
-      int64_t want = cdiv(2LL * sms, gp.tiles);
-      int64_t maxs = std::max<int64_t>(1, g.K / 256);
-      splits = (int)std::max<int64_t>(1, std::min<int64_t>(std::min<int64_t>(want, maxs), 64));
-    } else if (g.K >= 4 * 2048) {
-      // wave quantisation: with a few items per SM the last wave idles SMs (528 Gram tiles
-      // on 148 SMs run 4 waves for 3.57 of work); split K if that evens the waves out
-      double best = (double)cdiv(gp.tiles, sms) * sms / gp.tiles;
-      for (int s2 = 2; s2 <= 4; ++s2) {
-        if (g.K / s2 < 2048) break;
-        const double cost = (double)cdiv((int64_t)gp.tiles * s2, sms) * sms / ((double)gp.tiles * s2) * 1.01;
-        if (cost < best * 0.97) {
-          best = cost;
-          splits = s2;
-        }
-      }
-    }
-  }
+  if (splits <= 0) splits = gemm_plain_splits(gp.tiles, BT, g.M, g.N, g.K);
   int kchunk = (int)round_up(cdiv(std::max<int64_t>(g.K, 1), splits), GBK * gemm_ks());
   splits = (int)std::max<int64_t>(1, cdiv(std::max<int64_t>(g.K, 1), kchunk));
   gp.splits = splits;
@@ -449,6 +541,8 @@ int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
   gp.per_batch = gp.tiles * splits;
   gp.items = gp.per_batch * nb;
 
+  RH_CHECK(scr.ensure_ctr(st));
+  gp.ctr = scr.ctr;
   if (g.epi == EPI_RESID) {
     RH_CHECK(scr.ensure((size_t)gp.items * (GTHREADS / 32), st));
     gp.part = scr.ptr;

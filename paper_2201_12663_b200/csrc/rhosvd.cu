@@ -312,6 +312,24 @@ static Workspace& WS() {
   return w;
 }
 static std::mutex g_mu;
+// Device-side order across entry points: g_mu serialises the host side, and every entry's
+// stream also waits for the previous entry's device work (the workspaces, the GEMM
+// scratch and its tile-schedule counters are process-wide), so calls made on different
+// streams never overlap on the device.  Constructed under g_mu.
+struct StreamOrder {
+  cudaStream_t st;
+  static cudaEvent_t& last() {
+    static cudaEvent_t e = nullptr;
+    return e;
+  }
+  explicit StreamOrder(cudaStream_t s) : st(s) {
+    if (last()) cudaStreamWaitEvent(st, last(), 0);
+  }
+  ~StreamOrder() {
+    if (!last()) cudaEventCreateWithFlags(&last(), cudaEventDisableTiming);
+    cudaEventRecord(last(), st);
+  }
+};
 
 // ------------------------------------------------------------------ phase timer
 struct PhaseTimer {
@@ -1917,6 +1935,7 @@ static int c2t_entry(const double* U1, const double* U2, const double* U3, int64
   RH_CHECK(device_guard());
   std::lock_guard<std::mutex> lk(g_mu);
   cudaStream_t st = (cudaStream_t)stream;
+  StreamOrder order(st);
   static bool pool_set = false;
   if (!pool_set) {
     int dev = 0;
@@ -1950,6 +1969,7 @@ int rhosvd_gram(const double* U, int64_t ldu, int64_t n, int64_t R, double* G, i
   if ((ldu & 1) || ((uintptr_t)U & 15)) return fail(RHOSVD_EINVAL, "gram: ldu must be even, U 16B-aligned");
   RH_CHECK(device_guard());
   std::lock_guard<std::mutex> lk(g_mu);
+  StreamOrder order((cudaStream_t)stream);
   GemmArgs g;
   g.M = n; g.N = n; g.K = R; g.A = U; g.lda = ldu; g.a_k = false; g.B = U; g.ldb = ldu; g.b_k = false;
   g.C = G; g.ldc = ldg; g.upper_sym = true;
@@ -1964,6 +1984,7 @@ int rhosvd_dgemm(char ta, char tb, int64_t M, int64_t N, int64_t K, double alpha
     return fail(RHOSVD_EINVAL, "dgemm: lda/ldb must be even and A/B 16B-aligned");
   RH_CHECK(device_guard());
   std::lock_guard<std::mutex> lk(g_mu);
+  StreamOrder order((cudaStream_t)stream);
   GemmArgs g;
   g.M = M; g.N = N; g.K = K; g.A = A; g.lda = lda; g.B = B; g.ldb = ldb; g.C = C; g.ldc = ldc;
   g.alpha = alpha; g.beta = beta;
@@ -1980,6 +2001,7 @@ int rhosvd_syevj(int64_t b, double* A, int64_t lda, double* lambda, double* V, i
   if (!A || !lambda || !V || b < 0 || lda < b || ldv < b) return fail(RHOSVD_EINVAL, "bad args");
   RH_CHECK(device_guard());
   std::lock_guard<std::mutex> lk(g_mu);
+  StreamOrder order((cudaStream_t)stream);
   int sw = 0;
   RH_CHECK(syevj(b, A, lda, lambda, V, ldv, tol > 0 ? tol : 1e-15, 1e-300, 80, WS().mw[0].dws, (cudaStream_t)stream, &sw));
   if (sweeps_out) *sweeps_out = sw;
@@ -1991,6 +2013,7 @@ int rhosvd_chol_inv(int64_t b, const double* S, int64_t lds, double shift, doubl
   if (!S || !Bp || b < 0 || lds < b || ldb < b || !(shift >= 0.0)) return fail(RHOSVD_EINVAL, "bad args");
   RH_CHECK(device_guard());
   std::lock_guard<std::mutex> lk(g_mu);
+  StreamOrder order((cudaStream_t)stream);
   return chol_inv_scaled(b, S, lds, shift, Bp, ldb, WS().mw[0].dws, (cudaStream_t)stream);
 }
 
@@ -2003,6 +2026,7 @@ int rhosvd_core(const double* W1, const double* W2, const double* W3, int64_t ld
   RH_CHECK(device_guard());
   std::lock_guard<std::mutex> lk(g_mu);
   cudaStream_t st = (cudaStream_t)stream;
+  StreamOrder order(st);
   Workspace& w = WS();
   int64_t ldx = round_up(std::max<int64_t>(R, 2), 2);
   RH_CHECK(w.W1x.ensure((size_t)r1 * ldx + 64, st));

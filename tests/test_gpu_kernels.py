@@ -112,7 +112,7 @@ def test_core(rh, r, R):
 
 # b <= 160: the one-CTA register kernel (every 32-block count and its edges); larger b:
 # the cooperative blocked kernel
-@pytest.mark.parametrize("b", [1, 5, 31, 32, 33, 64, 65, 96, 127, 128, 129, 130, 159, 160, 161, 298, 707])
+@pytest.mark.parametrize("b", [1, 5, 31, 32, 33, 64, 65, 96, 127, 128, 129, 130, 159, 160, 161, 298, 449, 707, 873])
 def test_chol_inv(rh, b):
     """Bp = D L^{-T} (scaled Cholesky inverse) against LAPACK; Q = M Bp orthonormal."""
     rng = np.random.default_rng(b + 11)
@@ -127,17 +127,19 @@ def test_chol_inv(rh, b):
     assert np.max(np.abs(Q.T @ Q - np.eye(b))) <= 1e-12
 
 
-@pytest.mark.parametrize("b", [100, 200])
-def test_chol_inv_dependent_column(rh, b):
+# dependent column in the second / first 32-half of a diagonal block and in a later
+# panel (blocked kernel), and in the one-CTA kernel
+@pytest.mark.parametrize("b,col", [(100, 40), (200, 40), (200, 10), (300, 130)])
+def test_chol_inv_dependent_column(rh, b, col):
     """A numerically dependent column gets a unit pivot and a zero sub-column: the
     remaining columns stay orthonormal and no NaN appears (one-CTA and blocked kernels)."""
     rng = np.random.default_rng(5)
     M = rng.normal(size=(3 * b, b))
-    M[:, 40] = M[:, 3] + 1e-9 * M[:, 40]
+    M[:, col] = M[:, 3] + 1e-9 * M[:, col]
     S = M.T @ M
     Bp = rh.chol_inv(dev(S)).cpu().numpy()
     assert np.all(np.isfinite(Bp))
     Q = M @ Bp
-    keep = [i for i in range(b) if i != 40]
+    keep = [i for i in range(b) if i != col]
     G = Q[:, keep].T @ Q[:, keep]
     assert np.max(np.abs(G - np.eye(b - 1))) <= 1e-8

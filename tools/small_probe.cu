@@ -1,5 +1,7 @@
 // small_probe.cu - single-CTA timing of the b x b building blocks (clock64 cycles).
 __device__ long long g_stamp[8];
+__device__ long long g_t2[4];
+#define RHOSVD_PROBE_T g_t2
 #define RHOSVD_PROBE_STAMP(i) do { __syncthreads(); if (threadIdx.x == 0) g_stamp[i] = clock64(); } while (0)
 #include "../paper_2201_12663_b200/csrc/small_dense.cu"
 
@@ -9,6 +11,10 @@ thread_local int g_launches = 0;
 int fail(int s, const std::string& m) { g_err = m; return s; }
 void set_error(const std::string& m) { g_err = m; }
 int num_sms() { return 148; }
+thread_local int g_coop_cap = 0;
+int d2h_wait(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+  return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st) == cudaSuccess && cudaStreamSynchronize(st) == cudaSuccess ? 0 : -1;
+}
 }
 using namespace rhosvd;
 
@@ -69,6 +75,23 @@ __global__ void probe(double* g, long long* out) {
     t1 = clock64();
     if (tid == 0) out[5] = t1 - t0;
   }
+  // (g) warp_chol32 with runtime delta / width (as inside chol_diag_block)
+  for (int e = tid; e < 32 * 32; e += blockDim.x) { int r = e >> 5, c = e & 31; s2[r * CLD + c] = (r == c) ? 40.0 : 0.5 + 0.01 * ((r * 7 + c * 3) % 13); }
+  __syncthreads();
+  {
+    const double dl = g[50000];
+    const int wv = (int)g[50001];
+    t0 = clock64();
+    if (tid < 32) warp_chol32(s2, dl, wv);
+    __syncthreads();
+    t1 = clock64();
+    if (tid == 0) out[6] = t1 - t0;
+    t0 = clock64();
+    if (tid < 32) warp_inv32(s2, s1);
+    __syncthreads();
+    t1 = clock64();
+    if (tid == 0) out[7] = t1 - t0;
+  }
   // (e) sqrt + div chain
   double x = 2.0 + tid;
   t0 = clock64();
@@ -84,6 +107,8 @@ int main() {
   double h[4096];
   for (int i = 0; i < 4096; ++i) h[i] = (i % 64 == i / 64) ? 64.0 : 0.01 * (i % 17);
   cudaMemcpy(g, h, sizeof(h), cudaMemcpyHostToDevice);
+  double hp[2] = {1e-13, 32.0};
+  cudaMemcpy(g + 50000, hp, sizeof(hp), cudaMemcpyHostToDevice);
   size_t smem = 3 * CB * CLD * 8;
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   for (int rep = 0; rep < 3; ++rep) {
@@ -92,8 +117,12 @@ int main() {
     cudaMemcpy(ho, o, sizeof(ho), cudaMemcpyDeviceToHost);
     long long st[8];
     cudaMemcpyFromSymbol(st, g_stamp, sizeof(st));
-    printf("diag parts: chol %lld, scale %lld, inverse+writes %lld\n", st[1] - st[0], st[2] - st[1], st[3] - st[2]);
-    printf("chol32 %lld  inv32 %lld  mm32 %lld  mm64 %lld  32x(sqrt+div) %lld  diag64 %lld cycles\n", ho[0], ho[1], ho[2], ho[3], ho[4], ho[5]);
+    long long t2[4];
+    cudaMemcpyFromSymbol(t2, g_t2, sizeof(t2));
+    printf("in diag block: warp_chol32 %lld warp_inv32 %lld cycles\n", t2[0], t2[1]);
+    printf("diag parts: chol11+inv11 %lld, L21 %lld, A22 %lld, chol22+inv22 %lld, inv21 %lld, writes %lld\n", st[4] - st[0],
+           st[5] - st[4], st[6] - st[5], st[1] - st[6], st[2] - st[1], st[3] - st[2]);
+    printf("chol32 %lld  inv32 %lld  mm32 %lld  mm64 %lld  32x(sqrt+div) %lld  diag64 %lld  chol32(runtime args) %lld inv32 %lld cycles\n", ho[0], ho[1], ho[2], ho[3], ho[4], ho[5], ho[6], ho[7]);
   }
   printf("%s\n", cudaGetErrorString(cudaGetLastError()));
   return 0;
