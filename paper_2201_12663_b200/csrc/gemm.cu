@@ -41,7 +41,6 @@ struct GParams {
   int a_koff, b_koff;     // k-coordinate shift of batch b's operands (b * koff)
   int64_t c_bstride;      // C offset of batch b (doubles)
   int stages;
-  int* ctr;  // [0] next dynamic item - gridDim.x, [1] CTAs finished (self-resetting)
   uint32_t a_bytes, stage_bytes, tx_bytes;
   uint32_t b_bytes;  // one k-slab of B (the stage holds KS slabs of A, then KS of B)
 };
@@ -69,26 +68,13 @@ __global__ void __launch_bounds__(GTHREADS, 1)
       tn = tile / p.tiles_m;
     }
   };
-  // Dynamic item schedule: a CTA's first item is blockIdx.x, later ones come from a global
-  // counter (p.ctr[0], self-resetting: the last CTA to leave zeroes it).  With three
-  // concurrent per-mode eigensolves a GEMM shares the GPU with the other modes'
-  // latency-bound kernels; under the former static stride (item += gridDim.x) the CTAs
-  // that could only start once those kernels left an SM still owned their items, and the
-  // GEMM ended late.  Every item's result is written to its own slot (C tile, split-K
-  // partial or residual partial), so the schedule does not change any bit of the output.
-  // The producer records the item of every ring stage it fills in slot[stage]; consumers
-  // read it at each item's first k-step (after the stage's full-barrier wait, which
-  // orders it); slot = -1 (a stage armed without data) ends the loop.
-  int* slot = (int*)(empty + p.stages);
-  int pit = blockIdx.x, pk = 0, pkend = 0, pm = 0, pn = 0, pka = 0, pkb = 0, pnext = 0;
-  bool pdone = false, pend_sent = false;
+  // producer cursor over this CTA's k-slab stream (static stride over the items: a
+  // work-fetching schedule was tried in r2p - bitwise the same results, but the
+  // concurrent per-mode eigensolves ran 0-1 % slower and their step times spread
+  // 886-899 ms instead of 889-891, so the static stride stays)
+  int pit = blockIdx.x, pk = 0, pkend = 0, pm = 0, pn = 0, pka = 0, pkb = 0;
   auto set_item = [&]() {
-    if (pit >= p.items) {
-      pdone = true;
-      return;
-    }
-    // the item after this one, fetched now so the atomic's latency is off the TMA path
-    pnext = (int)gridDim.x + atomicAdd(p.ctr, 1);
+    if (pit >= p.items) return;
     const int bt = pit / p.per_batch, rit = pit - bt * p.per_batch;
     const int split = rit / p.tiles;
     int tm, tn;
@@ -109,16 +95,8 @@ __global__ void __launch_bounds__(GTHREADS, 1)
     }
   };
   auto issue_next = [&](int stage) {
-    if (pdone) {
-      if (!pend_sent) {  // end marker: arm the stage with no data
-        pend_sent = true;
-        slot[stage] = -1;
-        mbar_arrive(&full[stage]);
-      }
-      return;
-    }
+    if (pit >= p.items) return;
     unsigned char* st = ring + (size_t)stage * p.stage_bytes;
-    slot[stage] = pit;
     mbar_arrive_expect_tx(&full[stage], p.tx_bytes);
 #pragma unroll
     for (int j = 0; j < KS; ++j) {
@@ -132,7 +110,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
     }
     pk += GBK * KS;
     if (pk >= pkend) {
-      pit = pnext;
+      pit += gridDim.x;
       set_item();
     }
   };
@@ -170,17 +148,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
   // incrementally: no integer division on the per-stage path
   uint32_t cs = 0, cph = 0;
   const uint32_t nst = (uint32_t)p.stages;
-  while (true) {
-    // first k-step of the next item: refill the previous stage, wait for this one, read
-    // its item (the loop below starts on the stage already waited for)
-    if (producer && g >= 1) {
-      const uint32_t sp = cs == 0 ? nst - 1 : cs - 1, php = cs == 0 ? cph ^ 1u : cph;
-      mbar_wait(&empty[sp], php);
-      issue_next((int)sp);
-    }
-    mbar_wait(&full[cs], cph);
-    const int it = *(volatile int*)&slot[cs];
-    if (it < 0) break;
+  for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
     const int bt = it / p.per_batch, rit = it - bt * p.per_batch;
     const int split = rit / p.tiles;
     int tm, tn;
@@ -210,15 +178,13 @@ __global__ void __launch_bounds__(GTHREADS, 1)
         for (int j = 0; j < FN; ++j) acc[i][j][0] = acc[i][j][1] = 0.0;
     }
     for (int k0 = kbeg; k0 < kend; k0 += GBK * KS, ++g) {
-      if (k0 != kbeg) {
-        if (producer) {
-          const uint32_t sp = cs == 0 ? nst - 1 : cs - 1, php = cs == 0 ? cph ^ 1u : cph;
-          mbar_wait(&empty[sp], php);
-          issue_next((int)sp);
-        }
-        mbar_wait(&full[cs], cph);
+      if (producer && g >= 1) {
+        const uint32_t sp = cs == 0 ? nst - 1 : cs - 1, php = cs == 0 ? cph ^ 1u : cph;
+        mbar_wait(&empty[sp], php);
+        issue_next((int)sp);
       }
       const uint32_t s = cs;
+      mbar_wait(&full[s], cph);
 #pragma unroll
       for (int js = 0; js < KS; ++js) {
       const uint32_t sa = ring_s + s * p.stage_bytes + js * p.a_bytes;
@@ -294,15 +260,6 @@ __global__ void __launch_bounds__(GTHREADS, 1)
           }
         }
   }
-  // the last CTA out resets the schedule counter for the next launch on this scratch
-  if (tid == 0) {
-    __threadfence();
-    if (atomicAdd(p.ctr + 1, 1) == (int)gridDim.x - 1) {
-      p.ctr[0] = 0;
-      p.ctr[1] = 0;
-      __threadfence();
-    }
-  }
 }
 
 // Fixed-order split-K reduction + epilogue (and symmetric mirror).
@@ -356,22 +313,10 @@ int Scratch::ensure(size_t doubles, cudaStream_t st) {
   cap = want;
   return RHOSVD_OK;
 }
-int Scratch::ensure_ctr(cudaStream_t st) {
-  if (ctr) return RHOSVD_OK;
-  cudaError_t e = cudaMallocAsync((void**)&ctr, 4 * sizeof(int), st);
-  if (e != cudaSuccess) {
-    ctr = nullptr;
-    return fail(RHOSVD_ENOMEM, std::string("gemm counter alloc: ") + cudaGetErrorString(e));
-  }
-  RH_CUDA(cudaMemsetAsync(ctr, 0, 4 * sizeof(int), st));
-  return RHOSVD_OK;
-}
 void Scratch::release(cudaStream_t st) {
   if (ptr) cudaFreeAsync(ptr, st);
   ptr = nullptr;
   cap = 0;
-  if (ctr) cudaFreeAsync(ctr, st);
-  ctr = nullptr;
 }
 
 // k-slabs per pipeline stage (one mbarrier round trip each): 2, RHOSVD_GEMM_KS=1 for 1
@@ -401,8 +346,7 @@ static int launch_cfg(const GemmArgs& g, GParams gp, cudaStream_t st) {
   gp.tx_bytes = KS * (a_box + b_box);
   const size_t budget = 227 * 1024 - 1024 - 256;
   gp.stages = (int)std::min<size_t>(8, budget / gp.stage_bytes);
-  const size_t smem = 1024 + (size_t)gp.stages * gp.stage_bytes + 2 * gp.stages * sizeof(uint64_t) +
-                      gp.stages * sizeof(int);
+  const size_t smem = 1024 + (size_t)gp.stages * gp.stage_bytes + 2 * gp.stages * sizeof(uint64_t);
   static const cudaError_t attr = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                         227 * 1024);  // per instantiation, thread-safe
   RH_CUDA(attr);
@@ -541,8 +485,6 @@ int gemm(const GemmArgs& g, Scratch& scr, cudaStream_t st, double* flops_acc) {
   gp.per_batch = gp.tiles * splits;
   gp.items = gp.per_batch * nb;
 
-  RH_CHECK(scr.ensure_ctr(st));
-  gp.ctr = scr.ctr;
   if (g.epi == EPI_RESID) {
     RH_CHECK(scr.ensure((size_t)gp.items * (GTHREADS / 32), st));
     gp.part = scr.ptr;

@@ -46,9 +46,7 @@ struct GemmArgs {
 struct Scratch {
   double* ptr = nullptr;
   size_t cap = 0;  // doubles
-  int* ctr = nullptr;  // dynamic tile-schedule counters of the GEMM kernel (self-resetting)
   int ensure(size_t doubles, cudaStream_t st);
-  int ensure_ctr(cudaStream_t st);
   void release(cudaStream_t st);
 };
 

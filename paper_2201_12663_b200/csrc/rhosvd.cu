@@ -941,22 +941,6 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
   double sel[4];
   double rho_h = 0.0;
   {
-    // rho = ||Uhat - Z W||_F^2 (fused residual epilogue; E never stored).  It needs only Z
-    // and W, so it runs before the b x b eigensolve: under the concurrent modes this GEMM
-    // can fill the SMs another mode's cooperative Jacobi leaves free.
-    {
-      GemmArgs g;
-      g.M = n; g.N = Rl; g.K = b; g.A = w.Z.p; g.lda = LDN; g.a_k = false; g.B = w.W.p; g.ldb = Rp; g.b_k = false;
-      g.epi = EPI_RESID; g.D = Uh; g.ldd = LDN; g.resid_out = scal + 16 + mode;
-      if (Rl > 0) {
-        RH_CHECK(gemm(g, w.gsc, st, &c.flops));
-      } else {
-        RH_CUDA(cudaMemsetAsync(scal + 16 + mode, 0, sizeof(double), st));
-      }
-      RH_CHECK(allreduce(c, scal + 16 + mode, 1));
-      TL().mark(mode, "residual", st);
-      c.tm->mark(PH_RANK);
-    }
     // W W^T = P Lambda P^T (high relative accuracy Jacobi)
     RH_CHECK(mm(c, b, b, Rl, w.W.p, Rp, true, w.W.p, Rp, true, w.S.p, ldb, nullptr, true));
     RH_CHECK(allreduce(c, w.S.p, ldb * b));
@@ -997,6 +981,20 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
       TL().mark(mode, "Jacobi", st);
     }
     c.tm->mark(PH_RANK);
+    // rho = ||Uhat - Z W||_F^2 (fused residual epilogue; E never stored)
+    {
+      GemmArgs g;
+      g.M = n; g.N = Rl; g.K = b; g.A = w.Z.p; g.lda = LDN; g.a_k = false; g.B = w.W.p; g.ldb = Rp; g.b_k = false;
+      g.epi = EPI_RESID; g.D = Uh; g.ldd = LDN; g.resid_out = scal + 16 + mode;
+      if (Rl > 0) {
+        RH_CHECK(gemm(g, w.gsc, st, &c.flops));
+      } else {
+        RH_CUDA(cudaMemsetAsync(scal + 16 + mode, 0, sizeof(double), st));
+      }
+      RH_CHECK(allreduce(c, scal + 16 + mode, 1));
+      TL().mark(mode, "residual", st);
+      c.tm->mark(PH_RANK);
+    }
     RH_CHECK(k_select_rank(w.th.p, b, scal + 16 + mode, T, epsmode ? o.eps : 0.0, (int)rfix, 8, w.tail2.p,
                            scal + 24 + 4 * mode, w.inv.p, st));
     RH_CHECK(d2h_wait(sel, scal + 24 + 4 * mode, 3 * sizeof(double), st));
