@@ -121,6 +121,19 @@ def test_p5_p6_p8_bound_telescoped_error_and_core_bruteforce(seed):
     assert bns <= bp + 1e-15 * bp
 
 
+def test_p5_error_bounds_hand_values():
+    """error_bounds against hand-computed values of Thm. 2.2:
+    ||xi'|| = ||(3, 4)|| = 5, tails (1, 2, 2): the paper's sum form 5 (1 + 2 + 2) = 25, the
+    orthogonal form (A12) 5 sqrt(1 + 4 + 4) = 15; a single truncated mode makes the two
+    equal; no truncation gives 0."""
+    from oracle.rhosvd_oracle import error_bounds
+    bp, bns = error_bounds(np.array([3.0, 4.0]), np.array([1.0, 2.0, 2.0]))
+    assert bp == 25.0 and bns == 15.0
+    bp, bns = error_bounds(np.array([0.6, 0.8, 0.0]), np.array([0.0, 0.5, 0.0]))
+    assert abs(bp - 0.5) <= 1e-16 and abs(bns - 0.5) <= 1e-16
+    assert error_bounds(np.array([1.0, -2.0]), np.zeros(3)) == (0.0, 0.0)
+
+
 # ---------------------------------------------------------------- P7
 def test_p7_cor21_A_orthogonal_first_factor():
     rng = np.random.default_rng(7)
