@@ -85,14 +85,6 @@ __global__ void __launch_bounds__(GTHREADS, 1)
     pkend = min(p.K, pk + p.kchunk);
     pka = bt * p.a_koff;
     pkb = bt * p.b_koff;
-    if (p.epi == EPI_RESID) {
-      // the residual form reads the item's D tile at its start: prefetch it to L2 now,
-      // one or more k-steps before the consumers get there
-      const int rows = min(BM, p.M - pm) & ~1;
-      if (rows > 0)
-        for (int c = 0; c < BN && pn + c < p.N; ++c)
-          l2_prefetch_bulk(p.D + (int64_t)(pn + c) * p.ldd + pm, (uint32_t)rows * 8u);
-    }
   };
   auto issue_next = [&](int stage) {
     if (pit >= p.items) return;
@@ -160,8 +152,19 @@ __global__ void __launch_bounds__(GTHREADS, 1)
     if (p.epi == EPI_RESID) {
       // residual form: the accumulators start at -D, so after the k-loop they hold
       // op(A)op(B) - D and the epilogue is a sum of squares with no global loads (the
-      // short-K residual GEMM used to stall on its D loads after the last DMMA); the
-      // producer prefetched the D tile to L2 when it fetched the item.
+      // short-K residual GEMM used to stall on its D loads after the last DMMA).  Every
+      // thread with a column of the NEXT item's D tile prefetches it to L2 now (one bulk
+      // prefetch per column, spread over the CTA: a 128-prefetch loop in the producer
+      // thread delayed warp 0 and with it the ring, cfg 5 residual 4.6 -> 5.4 ms).
+      {
+        const int nit = it + (int)gridDim.x;
+        if (nit < p.items && tid < BN) {
+          const int nm0 = (nit % p.tiles_m) * BM, nn0 = p.n_off + (nit / p.tiles_m) * BN;
+          const int rows = min(BM, p.M - nm0) & ~1;
+          if (rows > 0 && nn0 + tid < p.N)
+            l2_prefetch_bulk(p.D + (int64_t)(nn0 + tid) * p.ldd + nm0, (uint32_t)rows * 8u);
+        }
+      }
 #pragma unroll
       for (int i = 0; i < FM; ++i)
 #pragma unroll
@@ -379,7 +382,10 @@ static int launch_edge(int bn, const GemmArgs& g, const GParams& gp, cudaStream_
 }
 
 static bool gemm_big(int64_t M, int64_t N, int64_t K) {
-  return (cdiv(M, 128) * cdiv(N, 128) >= num_sms() / 2) || (M >= 128 && N >= 128 && K >= 2048);
+  // (long-K products with N a little under 128, e.g. cfg 5's M = Uhat W^T with b = 124:
+  // the 128 x 128 engine with 4 padded columns beats 64 x 64 tiles, DMMA pipe 84 -> 9x %)
+  return (cdiv(M, 128) * cdiv(N, 128) >= num_sms() / 2) || (M >= 128 && N >= 128 && K >= 2048) ||
+         (M >= 128 && N >= 96 && K >= 16384);
 }
 
 int gemm_batch_splits(int64_t M, int64_t N, int64_t K, bool upper, int nb) {
