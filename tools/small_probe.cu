@@ -16,6 +16,100 @@ int d2h_wait(void* dst, const void* src, size_t bytes, cudaStream_t st) {
   return cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st) == cudaSuccess && cudaStreamSynchronize(st) == cudaSuccess ? 0 : -1;
 }
 }
+
+namespace rhosvd {
+// ---- experiment: 2 x 2 warp-level diagonal factor with NON-inlined warp helpers
+__device__ __noinline__ unsigned nl_chol32(double* T, double delta, int wvalid) {
+  const int lane = threadIdx.x & 31;
+  double a[32];
+#pragma unroll
+  for (int k = 0; k < 32; ++k) a[k] = (k <= lane) ? T[lane * CLD + k] : 0.0;
+  unsigned dep = 0u;
+#pragma unroll
+  for (int c = 0; c < 32; ++c) {
+    const double d = __shfl_sync(0xffffffffu, a[c], c);
+    const bool skip = (c >= wvalid) || !(d > delta);
+    dep |= (skip ? 1u : 0u) << c;
+    const double rp = jb_rsqrt(skip ? 1.0 : d);
+    const double lc = skip ? 0.0 : a[c] * rp;
+    a[c] = (lane > c) ? lc : (lane == c ? (skip ? 1.0 : d * rp) : a[c]);
+#pragma unroll
+    for (int k = c + 1; k < 32; ++k) {
+      const double lkc = __shfl_sync(0xffffffffu, lc, k);
+      if (lane >= k) a[k] = fma(-lc, lkc, a[k]);
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < 32; ++k) T[lane * CLD + k] = (k <= lane) ? a[k] : 0.0;
+  __syncwarp();
+  return dep;
+}
+__device__ __noinline__ void nl_inv32(const double* L, double* X) {
+  const int lane = threadIdx.x & 31;
+  const double rdl = 1.0 / L[lane * CLD + lane];
+  double x[32];
+#pragma unroll
+  for (int i = 0; i < 32; ++i) {
+    double s = (i == lane) ? 1.0 : 0.0;
+#pragma unroll
+    for (int k = 0; k < i; ++k) s = fma(-L[i * CLD + k], x[k], s);
+    const double rd = __shfl_sync(0xffffffffu, rdl, i);
+    x[i] = (i >= lane) ? s * rd : 0.0;
+  }
+#pragma unroll
+  for (int i = 0; i < 32; ++i) X[i * CLD + lane] = x[i];
+  __syncwarp();
+}
+__device__ void diag_v2(double* sm, double* inv, double delta, int w, long long* tt) {
+  const int tid = threadIdx.x;
+  __shared__ unsigned depw[2];
+  long long t0 = clock64();
+  if (tid < 32) {
+    const unsigned d0 = nl_chol32(sm, delta, min(w, 32));
+    nl_inv32(sm, inv);
+    if (tid == 0) depw[0] = d0;
+  }
+  __syncthreads();
+  long long t1 = clock64();
+  const int r = tid >> 3, c0 = tid & 7;
+  double acc[4];
+  mm32<true>(sm + 32 * CLD, inv, acc);
+  const unsigned d0 = depw[0];
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    const int c = c0 + 8 * q;
+    sm[(32 + r) * CLD + c] = ((d0 >> c) & 1u) ? 0.0 : acc[q];
+    sm[r * CLD + 32 + c] = 0.0;
+  }
+  __syncthreads();
+  mm32<true>(sm + 32 * CLD, sm + 32 * CLD, acc);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) sm[(32 + r) * CLD + 32 + c0 + 8 * q] -= acc[q];
+  __syncthreads();
+  long long t2 = clock64();
+  if (tid < 32) {
+    const unsigned d1 = nl_chol32(sm + 32 * CLD + 32, delta, max(0, w - 32));
+    nl_inv32(sm + 32 * CLD + 32, inv + 32 * CLD + 32);
+    if (tid == 0) depw[1] = d1;
+  }
+  __syncthreads();
+  long long t3 = clock64();
+  mm32<false>(sm + 32 * CLD, inv, acc);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) inv[r * CLD + 32 + c0 + 8 * q] = acc[q];
+  __syncthreads();
+  mm32<false>(inv + 32 * CLD + 32, inv + 32, acc);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) inv[(32 + r) * CLD + c0 + 8 * q] = -acc[q];
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < 4; ++q) inv[r * CLD + 32 + c0 + 8 * q] = 0.0;
+  __syncthreads();
+  long long t4 = clock64();
+  if (tid == 0) { tt[0] = t1 - t0; tt[1] = t2 - t1; tt[2] = t3 - t2; tt[3] = t4 - t3; tt[4] = t4 - t0; }
+}
+}
 using namespace rhosvd;
 
 __global__ void probe(double* g, long long* out) {
@@ -92,6 +186,13 @@ __global__ void probe(double* g, long long* out) {
     t1 = clock64();
     if (tid == 0) out[7] = t1 - t0;
   }
+  // (h) 2 x 2 warp-level diagonal factor with non-inlined warp helpers
+  for (int e = tid; e < CB * CB; e += blockDim.x) {
+    int r = e >> 6, c = e & 63;
+    s0[r * CLD + c] = (r == c) ? 64.0 : 0.01 * ((r * 7 + c * 3) % 13);
+  }
+  __syncthreads();
+  diag_v2(s0, s1, g[50000], (int)g[50001] * 2, out + 10);
   // (e) sqrt + div chain
   double x = 2.0 + tid;
   t0 = clock64();
@@ -103,7 +204,7 @@ __global__ void probe(double* g, long long* out) {
 
 int main() {
   double* g; long long* o;
-  cudaMalloc(&g, 65536 * 8); cudaMalloc(&o, 16 * 8);
+  cudaMalloc(&g, 65536 * 8); cudaMalloc(&o, 32 * 8);
   double h[4096];
   for (int i = 0; i < 4096; ++i) h[i] = (i % 64 == i / 64) ? 64.0 : 0.01 * (i % 17);
   cudaMemcpy(g, h, sizeof(h), cudaMemcpyHostToDevice);
@@ -113,13 +214,14 @@ int main() {
   cudaFuncSetAttribute(probe, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   for (int rep = 0; rep < 3; ++rep) {
     probe<<<1, 256, smem>>>(g, o);
-    long long ho[16];
+    long long ho[32];
     cudaMemcpy(ho, o, sizeof(ho), cudaMemcpyDeviceToHost);
     long long st[8];
     cudaMemcpyFromSymbol(st, g_stamp, sizeof(st));
     long long t2[4];
     cudaMemcpyFromSymbol(t2, g_t2, sizeof(t2));
     printf("in diag block: warp_chol32 %lld warp_inv32 %lld cycles\n", t2[0], t2[1]);
+    printf("diag_v2 (noinline warp helpers): chol11+inv11 %lld, L21+A22 %lld, chol22+inv22 %lld, inv21 %lld, total %lld cycles\n", ho[10], ho[11], ho[12], ho[13], ho[14]);
     printf("diag parts: chol11+inv11 %lld, L21 %lld, A22 %lld, chol22+inv22 %lld, inv21 %lld, writes %lld\n", st[4] - st[0],
            st[5] - st[4], st[6] - st[5], st[1] - st[6], st[2] - st[1], st[3] - st[2]);
     printf("chol32 %lld  inv32 %lld  mm32 %lld  mm64 %lld  32x(sqrt+div) %lld  diag64 %lld  chol32(runtime args) %lld inv32 %lld cycles\n", ho[0], ho[1], ho[2], ho[3], ho[4], ho[5], ho[6], ho[7]);
