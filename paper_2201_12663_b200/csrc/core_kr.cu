@@ -246,7 +246,11 @@ static int pick_bn(int64_t r3) {
       cols = (double)r3;
       tiles = (double)full;
     } else if (full > 0 && round_up(rem, 16) < bn) {
-      cols = (double)(full * bn + round_up(rem, 16));
+      // a narrow edge runs fewer DMMAs per fragment load: its columns cost 1 + (64 - w) / 128
+      // of a wide tile's (cfg 2, r3 = 282: 2 x 128 + a 32-wide edge 3.57 ms, 3 x 96 padded
+      // 3.37 ms - the unweighted count tied them and kept the edge)
+      const double w = (double)round_up(rem, 16);
+      cols = (double)(full * bn) + w * (w < 64.0 ? 1.0 + (64.0 - w) / 128.0 : 1.0);
       tiles = (double)full + 1.0;
     } else {
       cols = (double)(full + 1) * bn;
