@@ -792,7 +792,12 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     int st_a = RHOSVD_OK;
     std::string err_a;
     if (c.mp->owner) {
+      // the rank's owned iterations share the GPU (p >= 3: one mode with every SM), as the
+      // final Jacobi below does; the non-owned modes only wait here
+      const int cap_saved = g_coop_cap;
+      g_coop_cap = std::max(1, num_sms() / std::max(1, c.mp->owned));
       st_a = subspace_iteration();
+      g_coop_cap = cap_saved;
       if (st_a != RHOSVD_OK) err_a = g_err;
       c.mp->signal();
     }

@@ -624,6 +624,289 @@ __global__ void __launch_bounds__(NT) t2c_slice_block_kernel(T2CBlockParams p) {
   }
 }
 
+// ---------------------------------------------------------------- large slices, QR-preconditioned
+// The Drmac-Veselic preconditioning of t2c_slice_qr_kernel for slices beyond shared memory:
+// the block one-sided Jacobi above needs ~25 sweeps on cfg 2 / cfg 4 core slices.
+//   1. Householder QR with column pivoting B P = Q R on the global working copy (one CTA
+//      per slice; warp per column for the norms and the reflector, Q never formed);
+//   2. R^T (columns = the rows of R, length r2) into a second buffer, and the block
+//      one-sided Jacobi of t2c_slice_block_kernel on its columns (same pair-buffer rounds,
+//      de Rijk order, tolerance on rows of length r2);
+//   3. sigma_k = ||w_k||, v_k = P w_k / sigma_k, u_k = B v_k / sigma_k from the original
+//      slice (eight u's per pass over B, columns gathered through P), renormalised, sign
+//      rule on u - the shared-memory QR kernel's outputs and conventions.
+struct T2CBlockQRParams {
+  const double* Bo;  // original slices, column-major: Bo[(m r2 + b) r1 + a] = beta[a][b][m]
+  double* Bw;        // QR working copy, same layout
+  double* Rt;        // per slice: R^T, r2 rows x rr columns (column-major, ld r2)
+  int r1, r2, r3, ldp, CB, nb;  // ldp: smem pitch >= r2 (odd); nb: even block count over rr
+  double thr, tol;
+  double* Us;
+  double* Vs;
+  double* sg;
+  int* cnt;
+  int* sweeps;
+  double* drop;
+};
+
+template <int NT>
+__global__ void __launch_bounds__(NT) t2c_slice_blockqr_kernel(T2CBlockQRParams p) {
+  extern __shared__ double sbq[];
+  const int r1 = p.r1, r2 = p.r2, ld = p.ldp, CB = p.CB, nb = p.nb;
+  const int rr = min(r1, r2);
+  double* P = sbq;                              // 2 CB columns, pitch ld (QR: Householder vector)
+  double* sig = P + (size_t)2 * CB * ld;        // r2
+  int* ord = reinterpret_cast<int*>(sig + r2);  // r2
+  int* perm = ord + r2;                         // r2
+  __shared__ int srot, spiv;
+  __shared__ double sfro, salpha, svn2;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = NT / 32;
+  for (int m = blockIdx.x; m < p.r3; m += gridDim.x) {
+    const double* Bo = p.Bo + (size_t)m * r2 * r1;
+    double* B = p.Bw + (size_t)m * r2 * r1;
+    double* W = p.Rt + (size_t)m * r2 * rr;
+    for (int e = tid; e < r1 * r2; e += NT) B[e] = Bo[e];
+    for (int j = tid; j < r2; j += NT) perm[j] = j;
+    if (warp == 0) {
+      double s = 0.0;
+      for (int e = lane; e < r1 * r2; e += 32) s = fma(Bo[e], Bo[e], s);
+      s = warp_sum(s);
+      if (lane == 0) sfro = s;
+    }
+    __syncthreads();
+    // ---- 1. Householder QR with column pivoting (largest remaining norm, lowest index on ties)
+    double* hv = P;
+    for (int k = 0; k < rr; ++k) {
+      for (int j = k + warp; j < r2; j += nw) {
+        double s = 0.0;
+        for (int i = k + lane; i < r1; i += 32) s = fma(B[(size_t)j * r1 + i], B[(size_t)j * r1 + i], s);
+        s = warp_sum(s);
+        if (lane == 0) sig[j] = s;
+      }
+      __syncthreads();
+      if (warp == 0) {
+        double best = -1.0;
+        int bi = 0x7fffffff;
+        for (int j = k + lane; j < r2; j += 32)
+          if (sig[j] > best) { best = sig[j]; bi = j; }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+          const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+          if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+        }
+        if (lane == 0) spiv = bi;
+      }
+      __syncthreads();
+      const int pv = spiv;
+      if (pv != k) {
+        for (int i = tid; i < r1; i += NT) {
+          const double t = B[(size_t)k * r1 + i];
+          B[(size_t)k * r1 + i] = B[(size_t)pv * r1 + i];
+          B[(size_t)pv * r1 + i] = t;
+        }
+        if (tid == 0) {
+          const int t = perm[k];
+          perm[k] = perm[pv];
+          perm[pv] = t;
+        }
+      }
+      __syncthreads();
+      if (warp == 0) {  // reflector for column k, rows k..r1-1: H x = alpha e_1
+        double s = 0.0;
+        for (int i = k + lane; i < r1; i += 32) s = fma(B[(size_t)k * r1 + i], B[(size_t)k * r1 + i], s);
+        s = warp_sum(s);
+        const double x0 = B[(size_t)k * r1 + k];
+        const double nrm = sqrt(s);
+        const double alpha = (x0 >= 0.0) ? -nrm : nrm;
+        for (int i = k + lane; i < r1; i += 32) hv[i] = (i == k) ? x0 - alpha : B[(size_t)k * r1 + i];
+        if (lane == 0) {
+          salpha = alpha;
+          svn2 = s - x0 * x0 + (x0 - alpha) * (x0 - alpha);
+        }
+      }
+      __syncthreads();
+      const double vn2 = svn2;
+      if (vn2 > 0.0) {
+        for (int j = k + 1 + warp; j < r2; j += nw) {
+          double w = 0.0;
+          for (int i = k + lane; i < r1; i += 32) w = fma(hv[i], B[(size_t)j * r1 + i], w);
+          w = warp_sum(w);
+          const double f = 2.0 * w / vn2;
+          for (int i = k + lane; i < r1; i += 32) B[(size_t)j * r1 + i] = fma(-f, hv[i], B[(size_t)j * r1 + i]);
+        }
+        for (int i = k + tid; i < r1; i += NT) B[(size_t)k * r1 + i] = (i == k) ? salpha : 0.0;
+      }
+      __syncthreads();
+    }
+    // ---- 2. W = R^T (column r = row r of R: W[r r2 + c] = R[r][c], zero left of the diagonal)
+    for (int e = tid; e < r2 * rr; e += NT) {
+      const int r = e / r2, c = e % r2;
+      W[e] = (c >= r) ? B[(size_t)c * r1 + r] : 0.0;
+    }
+    __syncthreads();
+    // block one-sided Jacobi on the rr columns of W (length r2)
+    const int rows = r2, cols = rr;
+    const double tiny2 = 256.0 * 1.2325951644078309e-32 * sfro;
+    int sw = 0;
+    bool conv = false;
+    for (; sw < T2C_MAX_SWEEPS && !conv; ++sw) {
+      for (int k = warp; k < cols; k += nw) {
+        double s = 0.0;
+        for (int i = lane; i < rows; i += 32) s = fma(W[(size_t)k * rows + i], W[(size_t)k * rows + i], s);
+        s = warp_sum(s);
+        if (lane == 0) sig[k] = s;
+      }
+      if (tid == 0) srot = 0;
+      __syncthreads();
+      for (int k = tid; k < cols; k += NT) {  // de Rijk: decreasing-norm order
+        const double v = sig[k];
+        int r = 0;
+        for (int j = 0; j < cols; ++j) r += (sig[j] > v) || (sig[j] == v && j < k);
+        ord[r] = k;
+      }
+      __syncthreads();
+      for (int rd = 0; rd < nb - 1; ++rd) {
+        for (int k = 0; k < nb / 2; ++k) {
+          const int b1 = t2c_rr(k, rd, nb), b2 = t2c_rr(nb - 1 - k, rd, nb);
+          const int I = min(b1, b2), J = max(b1, b2);
+          for (int e = tid; e < 2 * CB * ld; e += NT) {
+            const int l = e / ld, a = e % ld;
+            const int pos = l < CB ? I * CB + l : J * CB + (l - CB);
+            P[e] = (a < rows && pos < cols) ? W[(size_t)ord[pos] * rows + a] : 0.0;
+          }
+          __syncthreads();
+          const int m2 = 2 * CB;
+          for (int st = 0; st < m2 - 1; ++st) {
+            for (int q = warp; q < CB; q += nw) {
+              const int c1 = t2c_rr(q, st, m2), c2 = t2c_rr(m2 - 1 - q, st, m2);
+              double* bp = P + (size_t)min(c1, c2) * ld;
+              double* bq = P + (size_t)max(c1, c2) * ld;
+              double al = 0.0, be = 0.0, ga = 0.0;
+              for (int i = lane; i < rows; i += 32) {
+                const double x = bp[i], y = bq[i];
+                al = fma(x, x, al);
+                be = fma(y, y, be);
+                ga = fma(x, y, ga);
+              }
+              al = warp_sum(al);
+              be = warp_sum(be);
+              ga = warp_sum(ga);
+              if (al > tiny2 && be > tiny2 && fabs(ga) > p.tol * sqrt(al * be)) {
+                const double zeta = (be - al) / (2.0 * ga);
+                const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+                const double c = rsqrt(1.0 + t * t), s = c * t;
+                for (int i = lane; i < rows; i += 32) {
+                  const double x = bp[i], y = bq[i];
+                  bp[i] = c * x - s * y;
+                  bq[i] = s * x + c * y;
+                }
+                if (lane == 0) atomicAdd(&srot, 1);
+              }
+            }
+            __syncthreads();
+          }
+          for (int e = tid; e < 2 * CB * ld; e += NT) {
+            const int l = e / ld, a = e % ld;
+            const int pos = l < CB ? I * CB + l : J * CB + (l - CB);
+            if (a < rows && pos < cols) W[(size_t)ord[pos] * rows + a] = P[e];
+          }
+          __syncthreads();
+        }
+      }
+      conv = (srot == 0);
+      __syncthreads();
+    }
+    // ---- 3. sigma_k = ||w_k||, descending order (ties: lower index), kept count
+    for (int k = warp; k < cols; k += nw) {
+      double s = 0.0;
+      for (int i = lane; i < rows; i += 32) s = fma(W[(size_t)k * rows + i], W[(size_t)k * rows + i], s);
+      s = warp_sum(s);
+      if (lane == 0) sig[k] = sqrt(s);
+    }
+    __syncthreads();
+    for (int k = tid; k < cols; k += NT) {
+      const double v = sig[k];
+      int r = 0;
+      for (int j = 0; j < cols; ++j) r += (sig[j] > v) || (sig[j] == v && j < k);
+      ord[r] = k;
+    }
+    __syncthreads();
+    int keep = 0;
+    for (int j = 0; j < cols; ++j) keep += sig[ord[j]] > p.thr;
+    double* Us = p.Us + (size_t)m * r2 * r1;
+    double* Vs = p.Vs + (size_t)m * r2 * r2;
+    double* sg = p.sg + (size_t)m * r2;
+    // u_j = B v_j / sigma_j = (B P) w_j / sigma_j^2, eight at a time: w's staged in the pair
+    // buffer (original column order: Pw[perm[c]] = w[c]), one thread per row a of B
+    const int JT = min(8, 2 * CB * ld / max(r2, 1));
+    for (int j0 = 0; j0 < keep; j0 += JT) {
+      const int jn = min(JT, keep - j0);
+      for (int e = tid; e < jn * r2; e += NT) {
+        const int jj = e / r2, c = e % r2;
+        P[(size_t)jj * r2 + perm[c]] = W[(size_t)ord[j0 + jj] * rows + c];
+      }
+      __syncthreads();
+      for (int a = tid; a < r1; a += NT) {
+        double acc[8];
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj) acc[jj] = 0.0;
+        for (int b = 0; b < r2; ++b) {
+          const double x = Bo[(size_t)b * r1 + a];
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            if (jj < jn) acc[jj] = fma(x, P[(size_t)jj * r2 + b], acc[jj]);
+        }
+#pragma unroll
+        for (int jj = 0; jj < 8; ++jj)
+          if (jj < jn) {
+            const double s = sig[ord[j0 + jj]];
+            Us[(size_t)(j0 + jj) * r1 + a] = acc[jj] / (s * s);
+          }
+      }
+      __syncthreads();
+    }
+    // renormalise u, sign rule (largest |u_a| positive, lowest index on ties), v = +-P w / sigma
+    for (int j = warp; j < keep; j += nw) {
+      double* uo = Us + (size_t)j * r1;
+      double un = 0.0, best = -1.0;
+      int bi = 0x7fffffff;
+      for (int a = lane; a < r1; a += 32) {
+        const double x = uo[a];
+        un = fma(x, x, un);
+        const double ax = fabs(x);
+        if (ax > best || (ax == best && a < bi)) { best = ax; bi = a; }
+      }
+      un = warp_sum(un);
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const double ob = __shfl_xor_sync(0xffffffffu, best, o);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+        if (ob > best || (ob == best && oi < bi)) { best = ob; bi = oi; }
+      }
+      const double bval = uo[bi];
+      const double sgn = ((bval < 0.0) ? -1.0 : 1.0) * (un > 0.0 ? 1.0 / sqrt(un) : 0.0);
+      __syncwarp();
+      for (int a = lane; a < r1; a += 32) uo[a] *= sgn;
+      const int r = ord[j];
+      const double s = sig[r];
+      const double vs = (bval < 0.0 ? -1.0 : 1.0) / s;
+      double* vo = Vs + (size_t)j * r2;
+      for (int c = lane; c < r2; c += 32) vo[perm[c]] = vs * W[(size_t)r * rows + c];
+      if (lane == 0) sg[j] = s;
+    }
+    __syncthreads();
+    if (tid == 0) {
+      p.cnt[m] = keep;
+      p.sweeps[m] = conv ? sw : -1;
+      double d = 0.0;
+      for (int j = cols - 1; j >= keep; --j) d = fma(sig[ord[j]], sig[ord[j]], d);
+      p.drop[m] = d;
+    }
+    __syncthreads();
+  }
+}
+
 // Bc[(m r2 + b) r1 + a] = beta[(a r2 + b) r3 + m]  (slice-major, column-major copy)
 __global__ void t2c_transpose_cm_kernel(const double* beta, int r1, int r2, int r3, double* Bc) {
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -809,9 +1092,36 @@ int rhosvd_t2c(const rhosvd_result* res, double eps_rel, rhosvd_stream stream, r
     e = cudaGetLastError();
   } else {
     // column-major slice copies: the original (for v = B^T u / sigma) and the working copy
+    static const bool qr_big = [] {
+      const char* e2 = getenv("RHOSVD_T2C_QR");
+      return !(e2 && e2[0] == '0');
+    }();
+    const int rrq = std::min(r1, r2);
+    const int ldq = r2 | 1;  // pair-buffer pitch of the R^T columns (length r2)
+    int CBq = 32;
+    while (CBq > 4 && (size_t)2 * CBq * ldq * sizeof(double) + (size_t)r2 * 16 + 64 > 200 * 1024) CBq /= 2;
+    const size_t smem_q = (size_t)2 * CBq * ldq * sizeof(double) + (size_t)r2 * (sizeof(double) + 2 * sizeof(int)) + 64;
+    const bool use_bqr = qr_big && smem_q <= 220 * 1024 && (size_t)2 * CBq * ldq >= (size_t)r1;
     double* Bw = nullptr;
+    double* Rtq = nullptr;
     e = cudaMalloc(&Bw, (size_t)r1 * r2 * r3 * sizeof(double));
-    if (e == cudaSuccess) {
+    if (e == cudaSuccess && use_bqr) e = cudaMalloc(&Rtq, (size_t)r2 * rrq * r3 * sizeof(double));
+    if (e == cudaSuccess && use_bqr) {
+      const int64_t tot = (int64_t)r1 * r2 * r3;
+      t2c_transpose_cm_kernel<<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(res->beta, r1, r2, r3, Bt);
+      const int nbk = (int)cdiv(rrq, CBq);
+      const double tol_qr = tol_mult * std::sqrt((double)std::max(std::max(r1, r2), 1)) * 1.1102230246251565e-16;
+      T2CBlockQRParams bq{Bt, Bw, Rtq, r1, r2, r3, ldq, CBq, nbk + (nbk & 1), cp->thr, tol_qr, Us, Vs, sg, cnt, sweeps,
+                          drop};
+      static const cudaError_t attr3 =
+          cudaFuncSetAttribute(t2c_slice_blockqr_kernel<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+      (void)attr3;
+      t2c_slice_blockqr_kernel<1024><<<std::min(r3, num_sms()), 1024, smem_q, st>>>(bq);
+      e = cudaGetLastError();
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      cudaFree(Rtq);
+      cudaFree(Bw);
+    } else if (e == cudaSuccess) {
       const int64_t tot = (int64_t)r1 * r2 * r3;
       t2c_transpose_cm_kernel<<<(unsigned)cdiv(tot, 256), 256, 0, st>>>(res->beta, r1, r2, r3, Bt);
       const int nbk = (int)cdiv(r2, CB);
@@ -843,6 +1153,8 @@ int rhosvd_t2c(const rhosvd_result* res, double eps_rel, rhosvd_stream stream, r
       cudaFree(Bw);
     } else {
       cudaGetLastError();
+      cudaFree(Rtq);
+      cudaFree(Bw);
     }
   }
   std::vector<int> hc(r3), hs(r3);

@@ -126,14 +126,15 @@ def test_t2c_cfg2(rh):
 
 
 def test_t2c_plain_kernel_subprocess():
-    """The shared-memory path defaults to the QR-preconditioned kernel; RHOSVD_T2C_QR=0
-    selects the plain one-sided Jacobi kernel (read once per process), so the random and
-    baseline cases run once more with it in a subprocess."""
+    """Both paths (shared-memory slices and the global-memory block path for large slices)
+    default to the QR-preconditioned kernels; RHOSVD_T2C_QR=0 selects the plain one-sided
+    Jacobi kernels (read once per process), so the random, baseline, large-slice and cfg 2
+    cases run once more with them in a subprocess."""
     import os
     import subprocess
     import sys
     here = os.path.dirname(os.path.abspath(__file__))
     env = dict(os.environ, RHOSVD_T2C_QR="0")
     r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-m", "gpu", os.path.join(here, "test_gpu_t2c.py"),
-                        "-k", "random or baseline_configs"], env=env, capture_output=True, text=True, timeout=900)
+                        "-k", "random or baseline_configs or large_slices or cfg2"], env=env, capture_output=True, text=True, timeout=900)
     assert r.returncode == 0, (r.stdout[-3000:], r.stderr[-2000:])
