@@ -761,7 +761,18 @@ int syevj(int64_t b, const double* A, int64_t lda, double* lambda, double* Vout,
     int64_t want = (int64_t)bj.h * (bj.h - 1) / 2 + cdiv(bj.bp, BJ_VT) * bj.h;
     // one CTA per SM: the grid barriers (two per round) cost more with 3 CTAs per SM than
     // the extra phase-2 items per CTA (b = 732: 444 CTAs 51.5 ms, 296: 38.5, 148: 36.3, 74: 51.3)
+    // the Jacobi's cooperative grid takes twice the per-mode cap (RHOSVD_JAC_CAP_MULT): it is
+    // throughput-bound (2.5x slower at 49 CTAs than at 148), unlike the latency-bound
+    // Cholesky, so under the concurrent modes it should not be held to a third of the SMs
+    // (r2r, cfg 4 eigensolve 98.8 -> 90.0 ms, cfg 2 8.2 -> 7.6; x3 = the whole GPU: 93.3)
+    static const int jac_mult = [] {
+      const char* e = getenv("RHOSVD_JAC_CAP_MULT");
+      return e ? std::max(1, atoi(e)) : 2;
+    }();
+    const int cap_saved = g_coop_cap;
+    if (g_coop_cap > 0) g_coop_cap = std::min(num_sms(), g_coop_cap * jac_mult);
     int grid = coop_grid((const void*)jacobi_block_kernel, threads, smem, std::min<int64_t>(want, num_sms()));
+    g_coop_cap = cap_saved;
     static const int tsm = [] {
       const char* e = getenv("RHOSVD_TS");
       return (e && e[0] == '1') ? 1 : 0;
