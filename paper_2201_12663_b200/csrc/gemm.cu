@@ -14,6 +14,7 @@
 // K-splits).  Split-K writes fixed-order partials that a second kernel sums in order:
 // results are bitwise reproducible (no FP64 atomics).
 #include <algorithm>
+#include <type_traits>
 
 #include "gemm.cuh"
 #include "tma.cuh"
@@ -68,17 +69,55 @@ __global__ void __launch_bounds__(GTHREADS, 1)
       tn = tile / p.tiles_m;
     }
   };
-  // producer cursor over this CTA's k-slab stream (static stride over the items: a
-  // work-fetching schedule was tried in r2p - bitwise the same results, but the
-  // concurrent per-mode eigensolves ran 0-1 % slower and their step times spread
-  // 886-899 ms instead of 889-891, so the static stride stays)
-  int pit = blockIdx.x, pk = 0, pkend = 0, pm = 0, pn = 0, pka = 0, pkb = 0;
+  // Item order.  Plain GEMMs: static stride, item = (batch, split, tile) with the tile
+  // fastest.  Symmetric (upper) 128 x 128 form: the off-diagonal items of every batch
+  // first, the diagonal ones (cheaper: 36 of 64 DMMAs per sub-partition, see below) last,
+  // dealt to the CTAs in a snake (odd rounds in reverse CTA order), so the CTAs that take
+  // one item more than the others take diagonal ones.  cfg 4 (3 x 136 tiles x 5 splits on
+  // 148 SMs): the busiest CTA runs 12 off-diagonal + 2 diagonal items instead of 14.  The
+  // split-K partials and their fixed-order sum are independent of the item order, so G is
+  // bitwise unchanged.
+  constexpr bool kDiag = (BM == 128 && BN == 128);
+  const bool snake = kDiag && p.upper;
+  auto item_at = [&](int round) {
+    const int G = (int)gridDim.x, b = (int)blockIdx.x;
+    return round * G + ((snake && (round & 1)) ? G - 1 - b : b);
+  };
+  auto decode = [&](int it, int& bt, int& split, int& tm, int& tn) {
+    if (snake) {
+      const int nd = p.tiles_n, nf = p.tiles - nd, full = p.nbatch * p.splits * nf;
+      if (it < full) {
+        bt = it / (p.splits * nf);
+        const int r = it - bt * p.splits * nf;
+        split = r / nf;
+        const int f = r - split * nf;  // off-diagonal tile f: tm < tn, tn (tn - 1) / 2 <= f
+        tn = (int)((1.0f + sqrtf(8.0f * f + 1.0f)) * 0.5f);
+        while (tn * (tn - 1) / 2 > f) --tn;
+        while ((tn + 1) * tn / 2 <= f) ++tn;
+        tm = f - tn * (tn - 1) / 2;
+      } else {
+        const int j = it - full;
+        bt = j / (p.splits * nd);
+        const int r = j - bt * p.splits * nd;
+        split = r / nd;
+        tm = tn = r - split * nd;
+      }
+      return;
+    }
+    bt = it / p.per_batch;
+    const int rit = it - bt * p.per_batch;
+    split = rit / p.tiles;
+    tile_of(rit % p.tiles, tm, tn);
+  };
+  // producer cursor over this CTA's k-slab stream (a work-fetching schedule was tried in
+  // r2p - bitwise the same results, but the concurrent per-mode eigensolves ran 0-1 %
+  // slower and their step times spread 886-899 ms instead of 889-891, so the static
+  // schedule stays)
+  int pround = 0, pit = item_at(0), pk = 0, pkend = 0, pm = 0, pn = 0, pka = 0, pkb = 0;
   auto set_item = [&]() {
     if (pit >= p.items) return;
-    const int bt = pit / p.per_batch, rit = pit - bt * p.per_batch;
-    const int split = rit / p.tiles;
-    int tm, tn;
-    tile_of(rit % p.tiles, tm, tn);
+    int bt, split, tm, tn;
+    decode(pit, bt, split, tm, tn);
     pm = tm * BM;
     pn = p.n_off + tn * BN;
     pk = split * p.kchunk;
@@ -102,7 +141,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
     }
     pk += GBK * KS;
     if (pk >= pkend) {
-      pit += gridDim.x;
+      pit = item_at(++pround);
       set_item();
     }
   };
@@ -134,20 +173,44 @@ __global__ void __launch_bounds__(GTHREADS, 1)
                   : (uint32_t)((k * BPITCH + wn0 + fr) * 8);
   }
   constexpr uint32_t ASTEP = AK ? 1024u : 64u, BSTEP = BKM ? 1024u : 64u;  // next 8 rows
+  // Diagonal tiles of the symmetric (upper) form, 128 x 128 only: the strictly lower half
+  // is not needed, so the warps take 16-row strips of the tile instead of 64 x 32 blocks
+  // (the same 64 accumulators: fragment (i', j') of the strip, i' < 2, j' < 16, lives in
+  // acc[e >> 2][e & 3], e = 16 i' + j') and skip the fragment columns left of the strip
+  // (8 j' + 7 < 16 s: every entry below the diagonal).  Strip s = warp for warps 0-3 and
+  // 11 - warp for warps 4-7, so the two warps of each SM sub-partition (warp w and w + 4)
+  // hold strips s and 7 - s: 36 of 64 DMMAs per k-step on every sub-partition, where the
+  // 64 x 32 blocks left a full 64 on two of them (the tile's DMMA time is set by the
+  // busiest sub-partition's tensor pipe).  Diagonal tiles are 12 % of cfg 4's upper tiles.
+  const int dstrip = warp < 4 ? warp : 11 - warp;
+  uint32_t daoff[GBK / 4], dboff[GBK / 4];
+#pragma unroll
+  for (int q = 0; q < GBK / 4; ++q) {
+    const int k = 4 * q + fc, wmd = 16 * dstrip;
+    daoff[q] = AK ? (uint32_t)((wmd + fr) * 128) + sw128_off(fr, k) - fr * 128 : (uint32_t)((k * APITCH + wmd + fr) * 8);
+    dboff[q] = BKM ? (uint32_t)(fr * 128) + sw128_off(fr, k) - fr * 128 : (uint32_t)((k * BPITCH + fr) * 8);
+  }
   const uint32_t ring_s = smem_u32(ring);
   uint32_t g = 0;
   // ring position of k-tile g (stage g % stages, parity (g / stages) & 1), advanced
   // incrementally: no integer division on the per-stage path
   uint32_t cs = 0, cph = 0;
   const uint32_t nst = (uint32_t)p.stages;
-  for (int it = blockIdx.x; it < p.items; it += gridDim.x) {
-    const int bt = it / p.per_batch, rit = it - bt * p.per_batch;
-    const int split = rit / p.tiles;
-    int tm, tn;
-    tile_of(rit % p.tiles, tm, tn);
+  for (int round = 0;; ++round) {
+    const int it = item_at(round);
+    if (it >= p.items) break;
+    int bt, split, tm, tn;
+    decode(it, bt, split, tm, tn);
     double* const Cb = p.C + bt * p.c_bstride;
     const int m0 = tm * BM, n0 = p.n_off + tn * BN;
     const int kbeg = split * p.kchunk, kend = min(p.K, kbeg + p.kchunk);
+    const bool diag = kDiag && p.upper && tm == tn;
+    // output coordinates of accumulator fragment (i, j): the 64 x 32 warp block, or on a
+    // diagonal tile fragment (e >> 4, e & 15) of the warp's 16-row strip, e = FN i + j
+    auto frag_m = [&](int i, int j) {
+      return diag ? m0 + 16 * dstrip + 8 * ((FN * i + j) >> 4) + fr : m0 + wm0 + i * 8 + fr;
+    };
+    auto frag_n = [&](int i, int j) { return diag ? n0 + 8 * ((FN * i + j) & 15) + 2 * fc : n0 + wn0 + j * 8 + 2 * fc; };
     double acc[FM][FN][2];
     if (p.epi == EPI_RESID) {
       // residual form: the accumulators start at -D, so after the k-loop they hold
@@ -188,6 +251,43 @@ __global__ void __launch_bounds__(GTHREADS, 1)
       }
       const uint32_t s = cs;
       mbar_wait(&full[s], cph);
+      if (kDiag && diag) {
+        // one unrolled body per strip (a warp-uniform switch): predicated-off DMMAs still
+        // occupied the tensor pipe (measured: no gain with a predicate per fragment pair)
+        auto body = [&](auto S) {
+          constexpr int ST = decltype(S)::value;
+#pragma unroll
+          for (int js = 0; js < KS; ++js) {
+            const uint32_t sa = ring_s + s * p.stage_bytes + js * p.a_bytes;
+            const uint32_t sb = ring_s + s * p.stage_bytes + KS * p.a_bytes + js * p.b_bytes;
+#pragma unroll
+            for (int q = 0; q < GBK / 4; ++q) {
+              double af[2], bf[16 - 2 * ST];
+#pragma unroll
+              for (int i = 0; i < 2; ++i) af[i] = lds_f64(sa + daoff[q] + i * ASTEP);
+#pragma unroll
+              for (int j = 2 * ST; j < 16; ++j) bf[j - 2 * ST] = lds_f64(sb + dboff[q] + j * BSTEP);
+#pragma unroll
+              for (int i = 0; i < 2; ++i)
+#pragma unroll
+                for (int j = 2 * ST; j < 16; ++j) {
+                  const int e = 16 * i + j;
+                  dmma_8x8x4(acc[e >> 2][e & 3][0], acc[e >> 2][e & 3][1], af[i], bf[j - 2 * ST]);
+                }
+            }
+          }
+        };
+        switch (dstrip) {
+          case 0: body(std::integral_constant<int, 0>{}); break;
+          case 1: body(std::integral_constant<int, 1>{}); break;
+          case 2: body(std::integral_constant<int, 2>{}); break;
+          case 3: body(std::integral_constant<int, 3>{}); break;
+          case 4: body(std::integral_constant<int, 4>{}); break;
+          case 5: body(std::integral_constant<int, 5>{}); break;
+          case 6: body(std::integral_constant<int, 6>{}); break;
+          default: body(std::integral_constant<int, 7>{}); break;
+        }
+      } else {
 #pragma unroll
       for (int js = 0; js < KS; ++js) {
       const uint32_t sa = ring_s + s * p.stage_bytes + js * p.a_bytes;
@@ -203,6 +303,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
         for (int i = 0; i < FM; ++i)
 #pragma unroll
           for (int j = 0; j < FN; ++j) dmma_8x8x4(acc[i][j][0], acc[i][j][1], af[i], bf[j]);
+      }
       }
       }
       __syncwarp();
@@ -240,7 +341,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
         for (int j = 0; j < FN; ++j)
 #pragma unroll
           for (int h = 0; h < 2; ++h) {
-            int m = m0 + wm0 + i * 8 + fr, n = n0 + wn0 + j * 8 + 2 * fc + h;
+            int m = frag_m(i, j), n = frag_n(i, j) + h;
             if (m < p.M && n < p.N) out[(int64_t)n * p.M + m] = acc[i][j][h];
           }
       continue;
@@ -251,7 +352,7 @@ __global__ void __launch_bounds__(GTHREADS, 1)
       for (int j = 0; j < FN; ++j)
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
-          int m = m0 + wm0 + i * 8 + fr, n = n0 + wn0 + j * 8 + 2 * fc + h;
+          int m = frag_m(i, j), n = frag_n(i, j) + h;
           if (m < p.M && n < p.N && (!p.upper || m <= n)) {
             double v = p.alpha * acc[i][j][h];
             if (p.cs) v *= p.cs[n];
