@@ -211,8 +211,9 @@ struct BJParams {
   double* lam;
   double tol, abstol;
   int max_sweeps, inner_sweeps;
+  int band_d, band_max;  // banded pre-phase: block distance D (0: off), at most band_max band sweeps
   unsigned* bar;
-  int* cnt;     // max_sweeps rotation counters
+  int* cnt;     // [0, 120) rotations per sweep, [120, 128) per band sweep, [128, 256) tests
   int* info;
   unsigned long long* ts;  // optional: [0] phase 1, [1] barrier 1, [2] phase 2, [3] barrier 2 (ns, CTA 0)
 };
@@ -224,8 +225,48 @@ __device__ __forceinline__ unsigned long long gtimer() {
 }
 
 __device__ __forceinline__ int bj_g(int l, int I, int J) { return l < BJ_W ? I * BJ_W + l : J * BJ_W + (l - BJ_W); }
-__device__ __forceinline__ void bj_pair(int k, int step, int m, int& I, int& J) {
-  int i1 = rr_index(k, step, m), i2 = rr_index(m - 1 - k, step, m);
+// Band round (d, par) of the banded pre-phase: block i with (i / d) % 2 == par and
+// i + d < m pairs with i + d (these pairs are disjoint: i + d has the other parity); the
+// blocks left over pair with each other in increasing order.  Pair k of the round.
+__device__ __forceinline__ void bj_band_pair(int k, int d, int par, int m, int& I, int& J) {
+  int cnt = 0;
+  for (int i = 0; i + d < m; ++i)
+    if (((i / d) & 1) == par) {
+      if (cnt == k) {
+        I = i;
+        J = i + d;
+        return;
+      }
+      ++cnt;
+    }
+  int first = -1;
+  for (int i = 0; i < m; ++i) {
+    const bool left = ((i / d) & 1) == par && i + d < m, right = i >= d && (((i - d) / d) & 1) == par;
+    if (left || right) continue;
+    if (first < 0) {
+      first = i;
+    } else {
+      if (cnt == k) {
+        I = first;
+        J = i;
+        return;
+      }
+      ++cnt;
+      first = -1;
+    }
+  }
+  I = 0;
+  J = 1;  // not reached: k < m / 2
+}
+// pairing of schedule step stp: stp >= 0 the round-robin step, stp < 0 band round
+// (d, par) with -1 - stp = 2 (d - 1) + par
+__device__ __forceinline__ void bj_pair(int k, int stp, int m, int& I, int& J) {
+  if (stp < 0) {
+    const int code = -1 - stp;
+    bj_band_pair(k, code / 2 + 1, code & 1, m, I, J);
+    return;
+  }
+  int i1 = rr_index(k, stp, m), i2 = rr_index(m - 1 - k, stp, m);
   I = min(i1, i2);
   J = max(i1, i2);
 }
@@ -410,17 +451,16 @@ __global__ void __launch_bounds__(BJ_THREADS, 3) jacobi_block_kernel(BJParams p)
     if ((int)blockIdx.x < c0) return;
     for (int j = blockIdx.x - c0; j < vt * h; j += gridDim.x - c0) item(j / vt, j / vt, j % vt, stp, par);
   };
-  int sweeps = 0;
+  int sweeps = 0, band_sweeps = 0;
   bool converged = false;
-  int gs = 0, last_step = 0;  // global step counter (rotation buffer parity), last step run
+  int gs = 0, prev_stp = 0;  // global round counter (rotation buffer parity), previous round's pairing
   unsigned long long tacc[4] = {0, 0, 0, 0}, tq = gtimer();
-  for (int sw = 0; sw < p.max_sweeps; ++sw) {
-    for (int step = 0; step < m - 1; ++step, ++gs) {
-      last_step = step;
+  // one round: the m/2 disjoint block pairs of schedule step stp (rotation count -> cnt[cslot])
+  auto do_round = [&](const int stp, const int cslot) __attribute__((always_inline)) {
       // ---------------- phase 1: diagonalise each pair block
       for (int k = blockIdx.x; k < h; k += gridDim.x) {
         int I, J;
-        bj_pair(k, step, m, I, J);
+        bj_pair(k, stp, m, I, J);
         double* const S0 = S;  // phase 1: S ping-pong between S and X (phase-2 scratch)
         double* const S1 = X;
         // S: the pair block, swizzled (jb_swz) so every half-warp access below is bank-
@@ -568,13 +608,13 @@ __global__ void __launch_bounds__(BJ_THREADS, 3) jacobi_block_kernel(BJParams p)
         }
         if (tid == 0) {
           p.rotf[(gs & 1) * h + k] = rot_total > 0;
-          if (rot_total) atomicAdd(&p.cnt[sw], rot_total);
+          if (rot_total) atomicAdd(&p.cnt[cslot], rot_total);
         }
         __syncthreads();
       }
       // the previous step's V tiles, by the CTAs without a pair block (all CTAs after their
       // pair blocks when the grid is not larger than h)
-      if (gs > 0) v_items(step > 0 ? step - 1 : m - 2, (gs - 1) & 1, (int)gridDim.x > h ? h : 0);
+      if (gs > 0) v_items(prev_stp, (gs - 1) & 1, (int)gridDim.x > h ? h : 0);
       { unsigned long long t = gtimer(); tacc[0] += t - tq; tq = t; }
       grid_barrier(p.bar);
       { unsigned long long t = gtimer(); tacc[1] += t - tq; tq = t; }
@@ -585,12 +625,51 @@ __global__ void __launch_bounds__(BJ_THREADS, 3) jacobi_block_kernel(BJParams p)
         while (l * (l - 1) / 2 > it) --l;
         while ((l + 1) * l / 2 <= it) ++l;
         const int k = it - l * (l - 1) / 2;  // k < l
-        item(k, l, -1, step, gs & 1);
+        item(k, l, -1, stp, gs & 1);
       }
       { unsigned long long t = gtimer(); tacc[2] += t - tq; tq = t; }
       grid_barrier(p.bar);
       { unsigned long long t = gtimer(); tacc[3] += t - tq; tq = t; }
+      prev_stp = stp;
+      ++gs;
+  };
+  // Banded pre-phase.  The Rayleigh-Ritz matrices this solver gets (W W^T of a block from
+  // simultaneous iteration, columns aligned with the eigenvectors except inside clusters)
+  // couple only nearby indices: on cfg 2 / 4 the relative couplings |a_ij| / sqrt(a_ii a_jj)
+  // fall below 1e-8 beyond |i - j| ~ 64 / ~128.  Sweeps over the block pairs at distance
+  // <= D (2 D rounds each, against m - 1 for a round-robin sweep) annihilate the band
+  // first; the round-robin sweeps then start from ~1e-7 instead of ~1e-1 and need 1-2
+  // instead of 4-5 (CPU simulation of this kernel's rotation sequence on emulated cfg 2 / 3 /
+  // 4 matrices: 95 -> 43, 36 -> 21, 235 -> 111 rounds).  Skipped when some coupling beyond
+  // the band exceeds 1e-3 (no band structure: e.g. random eigenvectors).  Band sweeps stop
+  // once one rotates < 30 % of the first one's count, at most band_max.
+  if (p.band_d > 0) {
+    const int D = p.band_d;
+    int far = 0;
+    for (int64_t e = gtid; e < (int64_t)b * b; e += gthreads) {
+      const int i = (int)(e % b), j = (int)(e / b);
+      if (i < j && j / BJ_W - i / BJ_W > D) {
+        const double apq = cur[(int64_t)j * ld + i];
+        const double app = cur[(int64_t)i * ld + i], aqq = cur[(int64_t)j * ld + j];
+        far |= apq * apq > 1e-6 * fabs(app * aqq);
+      }
     }
+    if (__syncthreads_or(far) && tid == 0) atomicAdd(p.cnt + 250, 1);
+    grid_barrier(p.bar);
+    if (*(volatile int*)(p.cnt + 250) == 0) {
+      int c0 = 0;
+      for (int bs = 0; bs < p.band_max && bs < 8; ++bs) {
+        for (int d = 1; d <= D; ++d)
+          for (int par = 0; par < 2; ++par) do_round(-1 - (2 * (d - 1) + par), 120 + bs);
+        ++band_sweeps;
+        const int c = *(volatile int*)(p.cnt + 120 + bs);  // after the round's last barrier
+        if (bs == 0) c0 = c;
+        if (c == 0 || (bs > 0 && 10LL * c < 3LL * c0)) break;
+      }
+    }
+  }
+  for (int sw = 0; sw < p.max_sweeps; ++sw) {
+    for (int step = 0; step < m - 1; ++step) do_round(step, sw);
     ++sweeps;
     const int rot_sw = *(volatile int*)(p.cnt + sw);  // read after the barrier: identical in every CTA
     if (rot_sw == 0) {
@@ -621,11 +700,12 @@ __global__ void __launch_bounds__(BJ_THREADS, 3) jacobi_block_kernel(BJParams p)
     }
   }
   // the last step's V tiles (its rotations are complete: phase 2 ended with a barrier)
-  if (gs > 0) v_items(last_step, (gs - 1) & 1, 0);
+  if (gs > 0) v_items(prev_stp, (gs - 1) & 1, 0);
   for (int64_t i = gtid; i < b; i += gthreads) p.lam[i] = cur[i * ld + i];
   if (gtid == 0) {
     p.info[0] = sweeps;
     p.info[2] = converged ? 0 : 1;
+    p.info[3] = band_sweeps;
     if (p.ts)
       for (int i = 0; i < 4; ++i) p.ts[i] = tacc[i];
   }
@@ -753,6 +833,24 @@ int syevj(int64_t b, const double* A, int64_t lda, double* lambda, double* Vout,
       bj.inner_sweeps = inner;
     }
     bj.bar = ws.bar; bj.cnt = ws.cnt; bj.info = ws.info;
+    // banded pre-phase (see the kernel): block distance D ~ b / 96 (the coupling band of the
+    // Rayleigh-Ritz matrices grows with the block: ~48 indices at b ~ 300, ~128 at b ~ 760),
+    // at least 2, at most m/2 - 1; off for m < 8.  RHOSVD_JAC_BAND=0 disables it,
+    // RHOSVD_JAC_BAND_D forces D.
+    {
+      static const int band_env = [] {
+        const char* e = getenv("RHOSVD_JAC_BAND");
+        return e ? atoi(e) : 1;
+      }();
+      static const int band_d_env = [] {
+        const char* e = getenv("RHOSVD_JAC_BAND_D");
+        return e ? atoi(e) : 0;
+      }();
+      int D = band_d_env > 0 ? band_d_env : (int)std::lround((double)b / 96.0);
+      D = std::max(2, std::min(D, bj.m / 2 - 1));
+      bj.band_d = (band_env && bj.m >= 8) ? D : 0;
+      bj.band_max = 6;
+    }
     const int threads = BJ_THREADS;
     const size_t smem = (size_t)(2 * BJ_P + 2 * BJ_VT) * BJ_LD * sizeof(double);
     static const cudaError_t attr_b =
@@ -789,8 +887,16 @@ int syevj(int64_t b, const double* A, int64_t lda, double* lambda, double* Vout,
       cudaStreamSynchronize(st);
       cudaMemcpy(h, tsb, sizeof(h), cudaMemcpyDeviceToHost);
       cudaMemcpy(inf, ws.info, sizeof(inf), cudaMemcpyDeviceToHost);
-      fprintf(stderr, "[jacobi ts] b=%d m=%d grid=%d sweeps=%d: phase1 %.1f bar1 %.1f phase2 %.1f bar2 %.1f us\n",
-              (int)b, bj.m, grid, inf[0], h[0] * 1e-3, h[1] * 1e-3, h[2] * 1e-3, h[3] * 1e-3);
+      fprintf(stderr,
+              "[jacobi ts] b=%d m=%d grid=%d band D=%d sweeps=%d+%d: phase1 %.1f bar1 %.1f phase2 %.1f bar2 %.1f us\n",
+              (int)b, bj.m, grid, bj.band_d, inf[3], inf[0], h[0] * 1e-3, h[1] * 1e-3, h[2] * 1e-3, h[3] * 1e-3);
+      if (inf[3] > 0) {
+        int bc[8] = {0};
+        cudaMemcpy(bc, ws.cnt + 120, sizeof(bc), cudaMemcpyDeviceToHost);
+        fprintf(stderr, "[jacobi ts] rotations per band sweep:");
+        for (int i = 0; i < std::min(inf[3], 8); ++i) fprintf(stderr, " %d", bc[i]);
+        fprintf(stderr, "\n");
+      }
       {
         int cnt[16] = {0};
         cudaMemcpy(cnt, ws.cnt, sizeof(int) * std::min(16, bj.max_sweeps), cudaMemcpyDeviceToHost);
