@@ -21,9 +21,11 @@
 #include <cstring>
 #include <map>
 #include <memory>
+#include <chrono>
 #include <condition_variable>
 #include <thread>
 #include <array>
+#include <chrono>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -370,12 +372,22 @@ struct Timeline {
   cudaEvent_t origin = nullptr;
   struct E { int mode; const char* label; cudaEvent_t ev; };
   std::vector<E> evs;
+  // host-side stamps (ms since begin): when the host got past a point
+  std::chrono::steady_clock::time_point h0;
+  std::vector<std::pair<double, std::string>> hs;
   void begin(cudaStream_t st) {
     const char* e = getenv("RHOSVD_TIMELINE");
     on = e && e[0] == '1';
     if (!on) return;
     cudaEventCreate(&origin);
     cudaEventRecord(origin, st);
+    h0 = std::chrono::steady_clock::now();
+  }
+  void hmark(int mode, const char* label) {
+    if (!on) return;
+    const double t = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - h0).count();
+    std::lock_guard<std::mutex> lk(mu);
+    hs.emplace_back(t, "mode " + std::to_string(mode) + "  " + label);
   }
   void mark(int mode, const char* label, cudaStream_t st) {
     if (!on) return;
@@ -394,6 +406,8 @@ struct Timeline {
       fprintf(stderr, "[timeline] %9.3f ms  mode %2d  %s\n", t, x.mode, x.label);
       cudaEventDestroy(x.ev);
     }
+    for (auto& x : hs) fprintf(stderr, "[timeline host] %9.3f ms  %s\n", x.first, x.second.c_str());
+    hs.clear();
     evs.clear();
     cudaEventDestroy(origin);
     on = false;
@@ -1004,6 +1018,7 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
                            scal + 24 + 4 * mode, w.inv.p, st));
     RH_CHECK(d2h_wait(sel, scal + 24 + 4 * mode, 3 * sizeof(double), st));
     RH_CHECK(d2h_wait(&rho_h, scal + 16 + mode, sizeof(double), st));
+    TL().hmark(mode, "rank selected");
   }
   int64_t r = (int64_t)sel[0];
   // full space (b = min(n, R)): the tail beyond b is zero, so r = b is the rule's answer
@@ -1035,6 +1050,7 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     if (o.flags & RHOSVD_F_SIGN_FIX) RH_CHECK(k_sign_fix(mo.Z, LDN, n, r, mo.W, Rp, Rl, w.sgn.p, st));
   }
   TL().mark(mode, "projection", st);
+  TL().hmark(mode, "projection launched");
   return RHOSVD_OK;
 }
 
@@ -1660,6 +1676,7 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
       t2.join();
     }
     if (comm_thread.joinable()) comm_thread.join();
+    TL().hmark(-1, "modes joined");
     g_launches += mlaunch[0] + mlaunch[1] + mlaunch[2];
     c.flops += mflops[0] + mflops[1] + mflops[2];
     // per-phase device times of the concurrent region, summed over the modes (ms[9..13]:
@@ -1803,8 +1820,11 @@ static int c2t_impl(const double* U_in[3], int64_t ldu, const double* xi, int64_
       RH_CHECK(w.W2x.ensure(core_ws_doubles(r2, Rl, Rp), st));
       if (dbg_on()) dt.mark(3);
       cudaEventRecord(c0, st);
+      TL().mark(-1, "core_kr start (stream reached)", st);
+      TL().hmark(-1, "core_kr entered");
       RH_CHECK(core_kr(w.W1x.p, Rp, mo[1].W, mo[2].W, Rp, r1, r2, r3, Rl, res->beta, w.W2x.p, w.corepart.p,
                        w.corepart.cap, st, &c.flops, chunks.done ? &chunks : nullptr));
+      TL().hmark(-1, "core_kr returned");
       cudaEventRecord(c1, st);
       TL().mark(-1, "core", st);
       if (dbg_on()) {

@@ -346,6 +346,10 @@ __global__ void __launch_bounds__(BJ_THREADS, 3) jacobi_block_kernel(BJParams p)
     p.V[j * ld + i] = (i == j) ? 1.0 : 0.0;
   }
   for (int64_t e = gtid; e < 256; e += gthreads) p.cnt[e] = 0;  // rotation counts [0, 128), tests [128, 256)
+  // block-pair marks of the convergence pass (A1 is not used by this kernel): marks[I m + J]
+  // = g when block pair (I, J) held an entry above the threshold after sweep g - 1
+  int* const marks = (int*)p.A1;
+  for (int64_t e = gtid; e < (int64_t)p.m * p.m; e += gthreads) marks[e] = 0;
   grid_barrier(p.bar);
 
   double* cur = p.A0;  // updated in place: blocks of unrotated pairs are never touched
@@ -668,19 +672,33 @@ __global__ void __launch_bounds__(BJ_THREADS, 3) jacobi_block_kernel(BJParams p)
       }
     }
   }
+  // Round-robin sweeps.  After every sweep one pass over the strict upper triangle applies
+  // the rotation test to the current matrix and marks the block pairs holding an entry that
+  // would rotate: none means converged (the next sweep would change nothing, bitwise); else
+  // the next sweep runs only the steps that contain a marked pair (the other steps' pair
+  // solves would all exit early).  Pairs that a later round of the same sweep pushes above
+  // the threshold are caught by the next pass.  cfg 4 after the band phase: the second
+  // sweep rotates 37-271 entries, in a handful of the 47 steps.
   for (int sw = 0; sw < p.max_sweeps; ++sw) {
-    for (int step = 0; step < m - 1; ++step) do_round(step, sw);
+    for (int step = 0; step < m - 1; ++step) {
+      if (sw > 0) {  // marks are written only between sweeps: every CTA decides alike
+        bool need = false;
+        for (int k = 0; k < h && !need; ++k) {
+          int I, J;
+          bj_pair(k, step, m, I, J);
+          need = marks[I * m + J] == sw;
+        }
+        if (!need) continue;
+      }
+      do_round(step, sw);
+    }
     ++sweeps;
     const int rot_sw = *(volatile int*)(p.cnt + sw);  // read after the barrier: identical in every CTA
     if (rot_sw == 0) {
       converged = true;
       break;
     }
-    // Near convergence (few rotations in this sweep) one pass over the strict upper
-    // triangle applies the rotation test of every pair to the current matrix: if no pair
-    // would rotate, the next sweep would change nothing (bitwise), so it is skipped.
-    // b ~ 760 on cfg 4: the last, rotation-free sweep cost ~1 ms of the ~7 ms solve.
-    if ((int64_t)rot_sw * 16 < (int64_t)b * b) {
+    {
       int* flag = p.cnt + 128 + sw;
       int any = 0;
       for (int64_t e = gtid; e < (int64_t)b * b; e += gthreads) {
@@ -688,7 +706,10 @@ __global__ void __launch_bounds__(BJ_THREADS, 3) jacobi_block_kernel(BJParams p)
         if (i < j) {
           const double apq = cur[(int64_t)j * ld + i];
           const double app = cur[(int64_t)i * ld + i], aqq = cur[(int64_t)j * ld + j];
-          any |= apq * apq > fmax(abs2, tol2 * fabs(app * aqq));
+          if (apq * apq > fmax(abs2, tol2 * fabs(app * aqq))) {
+            any = 1;
+            marks[(i / BJ_W) * m + j / BJ_W] = sw + 1;
+          }
         }
       }
       if (__syncthreads_or(any) && tid == 0) atomicAdd(flag, 1);
