@@ -14,7 +14,10 @@
 namespace rhosvd {
 
 // ---------------------------------------------------------------- K0 normalize
-// one warp per column k of one mode
+// One warp per column k of one mode.  HBM-bound: the column is read from DRAM once (the
+// scaling pass re-reads it from L2) and Uhat written once.  16-B aligned columns (U 16-B
+// aligned, ldu even - the torch layout) take double2 loads, four in flight per lane, so
+// an SM keeps ~128 KB of reads outstanding (one-double loads: 4.3 TB/s on cfg 5).
 __global__ void normalize_kernel(const double* __restrict__ U, int64_t ldu, int n, int R, int Rp,
                                  double* __restrict__ Uh, int64_t ldn, double* __restrict__ s_out,
                                  double* __restrict__ tcol, int* __restrict__ flag) {
@@ -31,13 +34,43 @@ __global__ void normalize_kernel(const double* __restrict__ U, int64_t ldu, int 
     return;
   }
   const double* src = U + (int64_t)k * ldu;
+  const bool vec = (reinterpret_cast<uintptr_t>(src) & 15) == 0;
   double ss = 0.0, mx = 0.0;
   bool bad = false;
-  for (int i = lane; i < n; i += 32) {
-    double v = src[i];
-    bad |= !isfinite(v);
-    ss = fma(v, v, ss);
-    mx = fmax(mx, fabs(v));
+  if (vec) {
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+    const int n2 = n >> 1;
+    int i = lane;
+    for (; i + 96 < n2; i += 128) {
+      const double2 v0 = __ldg(s2 + i), v1 = __ldg(s2 + i + 32), v2 = __ldg(s2 + i + 64), v3 = __ldg(s2 + i + 96);
+      const double w[8] = {v0.x, v0.y, v1.x, v1.y, v2.x, v2.y, v3.x, v3.y};
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        bad |= !isfinite(w[q]);
+        ss = fma(w[q], w[q], ss);
+        mx = fmax(mx, fabs(w[q]));
+      }
+    }
+    for (; i < n2; i += 32) {
+      const double2 v = __ldg(s2 + i);
+      bad |= !isfinite(v.x) || !isfinite(v.y);
+      ss = fma(v.x, v.x, ss);
+      ss = fma(v.y, v.y, ss);
+      mx = fmax(mx, fmax(fabs(v.x), fabs(v.y)));
+    }
+    if ((n & 1) && lane == 0) {
+      const double v = src[n - 1];
+      bad |= !isfinite(v);
+      ss = fma(v, v, ss);
+      mx = fmax(mx, fabs(v));
+    }
+  } else {
+    for (int i = lane; i < n; i += 32) {
+      double v = src[i];
+      bad |= !isfinite(v);
+      ss = fma(v, v, ss);
+      mx = fmax(mx, fabs(v));
+    }
   }
   ss = warp_sum(ss);
 #pragma unroll
@@ -64,15 +97,134 @@ __global__ void normalize_kernel(const double* __restrict__ U, int64_t ldu, int 
   }
   const double inv = s > 0.0 ? 1.0 / s : 0.0;
   double tt = 0.0;
-  for (int64_t i = lane; i < ldn; i += 32) {
-    double v = (i < n) ? src[i] * inv : 0.0;
-    dst[i] = v;
-    tt = fma(v, v, tt);
+  if (vec && (ldn & 1) == 0) {  // dst is 16-B aligned (ldn is a multiple of 16 doubles)
+    const double2* s2 = reinterpret_cast<const double2*>(src);
+    double2* d2 = reinterpret_cast<double2*>(dst);
+    for (int64_t i = lane; i < (ldn >> 1); i += 32) {
+      const int64_t e = 2 * i;
+      double2 v;
+      if (e + 1 < n) {
+        const double2 x = s2[i];
+        v = make_double2(x.x * inv, x.y * inv);
+      } else {
+        v = make_double2(e < n ? src[e] * inv : 0.0, 0.0);
+      }
+      d2[i] = v;
+      tt = fma(v.x, v.x, tt);
+      tt = fma(v.y, v.y, tt);
+    }
+  } else {
+    for (int64_t i = lane; i < ldn; i += 32) {
+      double v = (i < n) ? src[i] * inv : 0.0;
+      dst[i] = v;
+      tt = fma(v, v, tt);
+    }
   }
   tt = warp_sum(tt);
   if (lane == 0) {
     s_out[k] = s;
     tcol[k] = tt;
+  }
+}
+
+// K0 for 512 <= n <= 4096 (every BASELINE config but cfg 1): one CTA of T = 32 ceil(n / 512)
+// threads per column holds the column in registers (16 doubles per thread, eight double2
+// loads issued back to back), so the column is read from DRAM once and never re-read: norm by
+// a block reduction, then the scaled column written from registers.  The one-warp kernel
+// above re-reads each column from L2 for the scaling pass and keeps fewer loads in flight.
+// Same outputs as normalize_kernel up to the summation order of the norms.
+constexpr int NRM_PER = 16;
+__global__ void __launch_bounds__(256) normalize_col_kernel(const double* __restrict__ U, int64_t ldu, int n, int R,
+                                                            double* __restrict__ Uh, int64_t ldn,
+                                                            double* __restrict__ s_out, double* __restrict__ tcol,
+                                                            int* __restrict__ flag) {
+  __shared__ double red[3][8];
+  const int k = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const double* src = U + (int64_t)k * ldu;
+  double* dst = Uh + (int64_t)k * ldn;
+  // thread t owns elements 2 (t + T j) and 2 (t + T j) + 1, j < 8 (coalesced double2 accesses)
+  const int T = blockDim.x;
+  double2 v[NRM_PER / 2];
+#pragma unroll
+  for (int j = 0; j < NRM_PER / 2; ++j) {
+    const int e = 2 * (tid + T * j);
+    if (e + 1 < n) v[j] = __ldg(reinterpret_cast<const double2*>(src + e));
+    else v[j] = make_double2(e < n ? src[e] : 0.0, 0.0);
+  }
+  double ss = 0.0, mx = 0.0;
+  bool bad = false;
+#pragma unroll
+  for (int j = 0; j < NRM_PER / 2; ++j) {
+    bad |= !isfinite(v[j].x) || !isfinite(v[j].y);
+    ss = fma(v[j].x, v[j].x, ss);
+    ss = fma(v[j].y, v[j].y, ss);
+    mx = fmax(mx, fmax(fabs(v[j].x), fabs(v[j].y)));
+  }
+  ss = warp_sum(ss);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  bad = __syncthreads_or(bad);
+  if (lane == 0) {
+    red[0][warp] = ss;
+    red[1][warp] = mx;
+  }
+  __syncthreads();
+  ss = 0.0;
+  mx = 0.0;
+  for (int w = 0; w < nw; ++w) {  // fixed order
+    ss += red[0][w];
+    mx = fmax(mx, red[1][w]);
+  }
+  if (bad) {
+    if (tid == 0) atomicOr(flag, 1);
+    ss = 0.0;
+    mx = 0.0;
+  }
+  double s;
+  if (mx == 0.0) {
+    s = 0.0;
+  } else if (ss > 1e-280 && ss < 1e280) {
+    s = sqrt(ss);
+  } else {  // rescaled sum (underflow / overflow safe), from the registers
+    const double inv = 1.0 / mx;
+    double t = 0.0;
+#pragma unroll
+    for (int j = 0; j < NRM_PER / 2; ++j) {
+      t = fma(v[j].x * inv, v[j].x * inv, t);
+      t = fma(v[j].y * inv, v[j].y * inv, t);
+    }
+    t = warp_sum(t);
+    __syncthreads();
+    if (lane == 0) red[2][warp] = t;
+    __syncthreads();
+    t = 0.0;
+    for (int w = 0; w < nw; ++w) t += red[2][w];
+    s = mx * sqrt(t);
+  }
+  const double inv = s > 0.0 ? 1.0 / s : 0.0;
+  double tt = 0.0;
+#pragma unroll
+  for (int j = 0; j < NRM_PER / 2; ++j) {
+    const int e = 2 * (tid + T * j);
+    if (e < ldn) {  // ldn even: the pair (e, e + 1) lies inside the padded column
+      const double2 x = make_double2(v[j].x * inv, v[j].y * inv);
+      *reinterpret_cast<double2*>(dst + e) = x;
+      tt = fma(x.x, x.x, tt);
+      tt = fma(x.y, x.y, tt);
+    }
+  }
+  // padding rows beyond the registers' reach (ldn > 2 T NRM_PER / 2 cannot happen: T >= n / 16
+  // and ldn - n < 16) are zero-filled by the loop above only up to 2 T NRM_PER / 2
+  for (int64_t e = (int64_t)T * NRM_PER + tid; e < ldn; e += T) dst[e] = 0.0;
+  tt = warp_sum(tt);
+  __syncthreads();
+  if (lane == 0) red[2][warp] = tt;
+  __syncthreads();
+  if (tid == 0) {
+    double t2 = 0.0;
+    for (int w = 0; w < nw; ++w) t2 += red[2][w];
+    s_out[k] = s;
+    tcol[k] = t2;
   }
 }
 
@@ -258,6 +410,21 @@ int k_normalize(const double* U, int64_t ldu, int64_t n, int64_t R, int64_t Rp, 
                 double* s, double* tcol, int* flag, cudaStream_t st) {
   if (Rp <= 0) return RHOSVD_OK;
   const int wpb = 8;
+  // register-resident column kernel for 512 <= n <= 4096 with 16-B aligned columns; the
+  // padding columns R..Rp-1 (zero) and every other shape take the one-warp kernel
+  const bool col = n >= 512 && n <= 4096 && (ldn & 1) == 0 && (ldu & 1) == 0 &&
+                   (reinterpret_cast<uintptr_t>(U) & 15) == 0 && (reinterpret_cast<uintptr_t>(Uh) & 15) == 0;
+  if (col && R > 0) {
+    const int T = (int)(32 * cdiv(n, 32 * NRM_PER));
+    normalize_col_kernel<<<(unsigned)R, T, 0, st>>>(U, ldu, (int)n, (int)R, Uh, ldn, s, tcol, flag);
+    LAUNCH_OK();
+    if (Rp > R) {  // zero padding columns
+      normalize_kernel<<<(unsigned)cdiv(Rp - R, wpb), 32 * wpb, 0, st>>>(U, ldu, (int)n, 0, (int)(Rp - R),
+                                                                        Uh + R * ldn, ldn, s + R, tcol + R, flag);
+      LAUNCH_OK();
+    }
+    return RHOSVD_OK;
+  }
   normalize_kernel<<<(unsigned)cdiv(Rp, wpb), 32 * wpb, 0, st>>>(U, ldu, (int)n, (int)R, (int)Rp, Uh, ldn, s,
                                                                   tcol, flag);
   LAUNCH_OK();
