@@ -257,3 +257,33 @@ def test_parity_stress(rh, i, n, R, eps, ranks, wide):
     if any(o.report["near_tie"]):
         pytest.skip(f"oracle flags a near-tie at the cut: {o.report['margins']}")
     compare(g, o, sig_floor=True)
+
+
+# ------------------------------------------------------------------ K0 column kernel shapes
+@pytest.mark.parametrize("n,R", [(512, 300), (777, 260), (2048, 130), (4096, 90)])
+def test_normalize_column_kernel_edges(rh, n, R):
+    """512 <= n <= 4096 takes the register-resident column kernel of K0 (csrc/misc_kernels.cu).
+    Its special cases against the oracle (PAPER.md:252 normalisation; readings A2/A3): a zero
+    column (xi' = 0), columns scaled by 1e-145 (sum of squares below 1e-280: the rescaled
+    norm) and by 1e+145 (above 1e280) - paired within a term so xi' keeps its size -, an odd
+    n (the last double2 pair is half padding) and n = 4096 (every register slot used);
+    T_l, ||xi'||, ranks, sigma and the Tucker tensor."""
+    p = make_random_params(n, R, seed=n + R, eps=1e-6)
+    U1, U2, U3, xi = (np.array(a) for a in make_config(p))
+    U1[3] = 0.0
+    U2[5] *= 1e-145
+    U3[5] *= 1e145
+    U1[11] *= 1e145
+    U2[11] *= 1e-145
+    o = oracle_rhosvd([U1, U2, U3], xi, eps=1e-6)
+    g = run_gpu(rh, [U1, U2, U3], xi, eps=1e-6)
+    compare(g, o)
+
+
+def test_normalize_column_kernel_nonfinite(rh):
+    rng = np.random.default_rng(12)
+    Us = [rng.normal(size=(40, 1024)) for _ in range(3)]
+    Us[1][17, 1000] = np.inf
+    with pytest.raises(rh.RhosvdError) as e:
+        run_gpu(rh, Us, rng.normal(size=40), eps=1e-3)
+    assert e.value.status == -2
