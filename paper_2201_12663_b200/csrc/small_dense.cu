@@ -25,8 +25,14 @@ __device__ __forceinline__ void grid_barrier(unsigned* bar) {
   cooperative_groups::this_grid().sync();
 }
 
+// round-robin tournament position pos at step (0 <= step < m - 1, 0 <= pos < m): position 0
+// fixed, the others rotate.  pos - 1 + step < 2 (m - 1), so one conditional subtraction
+// replaces the modulo (an integer division).
 __device__ __forceinline__ int rr_index(int pos, int step, int m) {
-  return pos == 0 ? 0 : 1 + (pos - 1 + step) % (m - 1);
+  if (pos == 0) return 0;
+  int x = pos - 1 + step;
+  if (x >= m - 1) x -= m - 1;
+  return 1 + x;
 }
 
 // ------------------------------------------------------------------ Jacobi
