@@ -35,5 +35,18 @@ rhosvd.c2t([U1, U2, U3], xi, eps=p.eps, als_sweeps=1)
 F = [torch.as_tensor(rng.normal(size=(4, 100)), device=dev) for _ in range(3)]
 P = [torch.as_tensor(rng.normal(size=(2, 100)), device=dev) for _ in range(3)]
 rhosvd.conv3d(F, torch.ones(4, dtype=torch.float64, device=dev), P, torch.ones(2, dtype=torch.float64, device=dev), 0.5)
+# round-2 kernels: the Gram's diagonal-strip path and snake deal (n >= 128 tiles, K >= 2048),
+# the register-resident column normalisation (512 <= n <= 4096, odd n), the block Jacobi's
+# banded pre-phase and mark-driven sweeps (the pipeline's W W^T, b > 112)
+p2 = make_random_params(521, 2600, seed=11, eps=1e-6)
+V1, V2, V3, xi2 = make_config(p2, backend="torch", device=dev)
+g2 = rhosvd.c2t([V1, V2, V3], xi2, eps=p2.eps)
+b = 300
+Eb = rng.normal(size=(b, b)) * 0.03
+ii, jj = np.indices((b, b))
+Eb[np.abs(ii - jj) > 40] = 0.0
+Ab = np.eye(b) + np.triu(Eb, 1) + np.triu(Eb, 1).T
+db = np.logspace(0, -6, b)
+rhosvd.syevj(torch.as_tensor(db[:, None] * Ab * db[None, :], device=dev))
 torch.cuda.synchronize()
-print("ok", g.ranks, cp.R)
+print("ok", g.ranks, cp.R, g2.ranks, g2.report["block"])
