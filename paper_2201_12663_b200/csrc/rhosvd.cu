@@ -946,7 +946,17 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
       if (dbg_on())
         fprintf(stderr, "[rhosvd dbg] mode %d refine step %d: a-posteriori estimate %.3e (steps planned %d)\n", mode,
                 rs + 1, est, nref);
-      if (adapt && est <= 1e-11 && rs + 1 < nref) nref = rs + 1;
+      // the estimate is meaningful only while lambda_b / lambda_1 (here the smallest
+      // non-squared Rayleigh quotient c_jj of the block) stays above the squared floor,
+      // ~2u: below it one non-squared step can leave sigma_r off by ~1e-6 although the
+      // estimate reads 1e-12 (r2g: n = 257, R = 2300, eps = 1e-8, kappa_r 6.5e7, ratio
+      // 2.8e-17 after step 1: sigma 3e-6 off after one step, 4.5e-10 after two; the
+      // Gram-domain d_r overstates such lambda_r 5000x, so d_h cannot tell), and the planned
+      // steps run.  BJ configs after step 1: 1.7e-15 (cfg 3 / 5) ... 1.1e-13 (cfg 4).
+      double lam_ratio = 1.0;
+      for (int64_t j = 0; j < b; ++j) lam_ratio = std::min(lam_ratio, std::max(cd[j], 0.0) / std::max(cd[0], 1e-300));
+      if (dbg_on()) fprintf(stderr, "[rhosvd dbg] mode %d refine step %d: lambda_b / lambda_1 %.3e\n", mode, rs + 1, lam_ratio);
+      if (adapt && est <= 1e-11 && rs + 1 < nref && lam_ratio >= 2.0 * u) nref = rs + 1;
     }
     RH_CHECK(orth(c, n, b, LDN, w.M.p, w.Z.p, w.T1.p, ldb, ORTH_CQR2));
     TL().mark(mode, "refine CholQR2", st);
@@ -1024,6 +1034,27 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
   // full space (b = min(n, R)): the tail beyond b is zero, so r = b is the rule's answer
   // (the residual is rounding only; the oracle's rule also returns m when no r < m meets it)
   if (r < 0 && b >= m) r = b;
+  // ... but a full-rank answer is certified only if the smallest Ritz value lies above the
+  // squared Rayleigh-Ritz noise (~u lambda_1 per value): a full-space block reached because
+  // the Gram-domain estimates could not resolve an eps^2 T below that noise would otherwise
+  // return r = min(n, R) for a problem whose rank is far smaller (r2g: n = 600, R = 5000,
+  // eps = 1e-9: one mode returned 600 against the oracle's 101).  Checked when the block
+  // grew to the full space; a full space taken from the start (min(n, R) <= the first block)
+  // keeps the rule's r = min(n, R) as before.
+  if (epsmode && r == b && b >= m && b > 1 && mo.grows > 0) {
+    double lam[2] = {0.0, 0.0};
+    RH_CHECK(d2h_wait(&lam[0], w.th.p, sizeof(double), st));
+    RH_CHECK(d2h_wait(&lam[1], w.th.p + (b - 1), sizeof(double), st));
+    const double noise = 8.0 * u * std::max(lam[0], 0.0) * std::sqrt((double)b);
+    if (!(lam[1] > noise)) {
+      char msg[320];
+      snprintf(msg, sizeof msg,
+               "mode %d: eps^2 T = %.3e cannot be resolved: the block reached the full space (%lld) and its "
+               "smallest Ritz values are at the squared Rayleigh-Ritz noise (lambda_min %.3e <= %.3e)",
+               mode, epsmode ? o.eps * o.eps * T : 0.0, (long long)b, lam[1], noise);
+      return fail(RHOSVD_ENOCONV, msg);
+    }
+  }
   if (r < 0) {
     char msg[256];
     snprintf(msg, sizeof msg,

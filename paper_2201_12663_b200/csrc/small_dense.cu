@@ -217,7 +217,8 @@ struct BJParams {
   double* lam;
   double tol, abstol;
   int max_sweeps, inner_sweeps;
-  int band_d, band_max;  // banded pre-phase: block distance D (0: off), at most band_max band sweeps
+  int band_d, band_max;
+  int select;  // mark-driven selective sweeps (RHOSVD_JAC_SELECT=0: every step of every sweep)  // banded pre-phase: block distance D (0: off), at most band_max band sweeps
   unsigned* bar;
   int* cnt;     // [0, 120) rotations per sweep, [120, 128) per band sweep, [128, 256) tests
   int* info;
@@ -687,7 +688,7 @@ __global__ void __launch_bounds__(BJ_THREADS, 3) jacobi_block_kernel(BJParams p)
   // sweep rotates 37-271 entries, in a handful of the 47 steps.
   for (int sw = 0; sw < p.max_sweeps; ++sw) {
     for (int step = 0; step < m - 1; ++step) {
-      if (sw > 0) {  // marks are written only between sweeps: every CTA decides alike
+      if (sw > 0 && p.select) {  // marks are written only between sweeps: every CTA decides alike
         bool need = false;
         for (int k = 0; k < h && !need; ++k) {
           int I, J;
@@ -877,6 +878,11 @@ int syevj(int64_t b, const double* A, int64_t lda, double* lambda, double* Vout,
       D = std::max(2, std::min(D, bj.m / 2 - 1));
       bj.band_d = (band_env && bj.m >= 8) ? D : 0;
       bj.band_max = 6;
+      static const int sel_env = [] {
+        const char* e = getenv("RHOSVD_JAC_SELECT");
+        return e ? atoi(e) : 1;
+      }();
+      bj.select = sel_env;
     }
     const int threads = BJ_THREADS;
     const size_t smem = (size_t)(2 * BJ_P + 2 * BJ_VT) * BJ_LD * sizeof(double);

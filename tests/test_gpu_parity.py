@@ -82,6 +82,56 @@ def compare(g, o, check_W=True, sig_floor=False):
 
 
 # ------------------------------------------------------------------ small random cases
+# mid-size shapes for the round-2 kernel paths: the Gram's 128-tile diagonal strips and snake
+# deal (n >= 256 with K >= 2048), the register-resident column normalisation (n >= 512, odd n),
+# the block Jacobi's banded pre-phase (blocks b > 112), the one-CTA Cholesky (b <= 160)
+@pytest.mark.parametrize("n,R,eps", [
+    (257, 2300, 1e-8),
+    (520, 2100, 1e-6),
+    (777, 4100, 1e-6),
+    (1030, 3000, 1e-5),
+    (600, 5000, 1e-7),
+])
+def test_parity_mid_sizes(rh, n, R, eps):
+    p = make_random_params(n, R, seed=n + 7 * R, eps=eps)
+    U1, U2, U3, xi = make_config(p)
+    o = oracle_rhosvd([U1, U2, U3], xi, eps=eps)
+    g = run_gpu(rh, [U1, U2, U3], xi, eps=eps)
+    # eps <= 1e-8 keeps sigma_r ~ 1e-8 sigma_1: the any-fp64-SVD floor of reading A13 applies
+    compare(g, o, sig_floor=eps <= 1e-8)
+
+
+def test_full_space_noise_rank_never_silently_wrong(rh):
+    """eps = 1e-9, r (101) << min(n, R) = 600: the block of one mode grows to the full space
+    because its Gram-domain tail estimates sit at the squared floor; the smallest Ritz values
+    there are noise (~u lambda_1), so a full-rank answer r = 600 cannot be certified and the
+    call fails with ENOCONV (it returned r = 600 silently before r2g).  At this noise floor
+    the outcome is not bitwise stable from call to call (about 1 call in 40 resolves the
+    block and returns the oracle's ranks): either outcome is accepted,
+    a wrong rank is not."""
+    p = make_random_params(600, 5000, seed=600 + 7 * 5000, eps=1e-9)
+    U1, U2, U3, xi = make_config(p)
+    try:
+        g = run_gpu(rh, [U1, U2, U3], xi, eps=1e-9)
+    except rh.RhosvdError as e:
+        assert e.status == -3
+        return
+    o = oracle_rhosvd([U1, U2, U3], xi, eps=1e-9)
+    assert tuple(g.ranks) == tuple(o.ranks)
+
+
+def test_eps_below_gram_resolution_fails_loudly(rh):
+    """eps = 1e-11 with r (115) < min(n, R): the rank rule needs sigma down to ~3e-11 sigma_1,
+    below what the Gram-domain block selection resolves (its estimates sit at the squared
+    floor u lambda_1); the block comes out too small, the direct residual shows the miss, and
+    the call fails with ENOCONV instead of returning a rank that breaks the rule."""
+    p = make_random_params(600, 5000, seed=600 + 7 * 5000, eps=1e-11)
+    U1, U2, U3, xi = make_config(p)
+    with pytest.raises(rh.RhosvdError) as e:
+        run_gpu(rh, [U1, U2, U3], xi, eps=1e-11)
+    assert e.value.status == -3
+
+
 @pytest.mark.parametrize("n,R,eps,ranks", [
     (16, 40, None, (3, 4, 5)),
     (37, 200, 1e-3, None),
