@@ -1078,6 +1078,47 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     RH_CHECK(mm(c, n, r, b, w.Z.p, LDN, false, w.V.p, ldb, true, mo.Z, LDN));
     RH_CHECK(mm(c, Rl, r, b, w.W.p, Rp, false, w.V.p, ldb, true, mo.W, Rp));
     RH_CUDA(cudaMemcpyAsync(mo.sigma, w.inv.p, r * sizeof(double), cudaMemcpyDeviceToDevice, st));
+    // Retained directions at the rounding level (a fixed r above the numerical rank, or a
+    // full space taken from the start): sigma_k <= 1e-10 sigma_1 is below what the squared
+    // Rayleigh-Ritz resolves, and such frame columns come out of CholeskyQR's
+    // dependent-column rule (unit pivot, zero sub-column), i.e. not orthonormal (r2h sweep:
+    // n = 644, fixed r = 198 against a numerical rank of 131 gave |Z^T Z - I| = 1).  They are
+    // replaced by an orthonormal completion of the other columns (random columns, projected
+    // out of them twice, CholQR2) and their W rows recomputed as Z_c^T Uhat, so beta stays the
+    // projection of A onto the returned frames; the energy they carry is <= 1e-20 of sigma_1^2
+    // each, so the Tucker tensor is unchanged to rounding.  (Replacing every column that
+    // failed a 1e-13 orthogonality test instead also dropped columns that carry energy:
+    // Tucker error 0.78 on that case.)
+    {
+      double s1r[2] = {0.0, 0.0};
+      RH_CHECK(d2h_wait(&s1r[0], mo.sigma, sizeof(double), st));
+      RH_CHECK(d2h_wait(&s1r[1], mo.sigma + (r - 1), sizeof(double), st));
+      if (r > 1 && !(s1r[1] > 1e-10 * s1r[0])) {
+        std::vector<double> sg(r);
+        RH_CHECK(d2h_wait(sg.data(), mo.sigma, r * sizeof(double), st));
+        int64_t kg = 0;
+        while (kg < r && sg[kg] > 1e-10 * sg[0]) ++kg;
+        const int64_t nc = r - kg;
+        double* X = mo.Z + kg * LDN;
+        RH_CHECK(k_random(mo.Z, LDN, n, kg, r, seed ^ 0x5bd1e995ull, st));
+        if (kg > 0) {
+          const int64_t ldt = round_up(std::max<int64_t>(kg, 2), 2);
+          for (int pass = 0; pass < 2; ++pass) {  // X -= Z_g (Z_g^T X), twice
+            RH_CHECK(mm(c, kg, nc, n, mo.Z, LDN, true, X, LDN, true, w.S.p, ldt));
+            GemmArgs gp;
+            gp.M = n; gp.N = nc; gp.K = kg; gp.A = mo.Z; gp.lda = LDN; gp.a_k = false; gp.B = w.S.p; gp.ldb = ldt;
+            gp.b_k = true; gp.C = X; gp.ldc = LDN; gp.alpha = -1.0; gp.beta = 1.0;
+            RH_CHECK(gemm(gp, w.gsc, st, &c.flops));
+          }
+        }
+        RH_CHECK(orth(c, n, nc, LDN, X, w.M.p, w.T1.p, ldbs(nc), ORTH_CQR2));
+        RH_CUDA(cudaMemcpyAsync(X, w.M.p, (size_t)LDN * nc * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        if (Rl > 0) RH_CHECK(mm(c, Rl, nc, n, Uh, LDN, true, X, LDN, true, mo.W + kg * Rp, Rp));
+        if (dbg_on())
+          fprintf(stderr, "[rhosvd dbg] mode %d: %lld of %lld frame columns (sigma <= 1e-10 sigma_1) completed\n", mode,
+                  (long long)nc, (long long)r);
+      }
+    }
     if (o.flags & RHOSVD_F_SIGN_FIX) RH_CHECK(k_sign_fix(mo.Z, LDN, n, r, mo.W, Rp, Rl, w.sgn.p, st));
   }
   TL().mark(mode, "projection", st);

@@ -337,3 +337,27 @@ def test_normalize_column_kernel_nonfinite(rh):
     with pytest.raises(rh.RhosvdError) as e:
         run_gpu(rh, Us, rng.normal(size=40), eps=1e-3)
     assert e.value.status == -2
+
+
+def test_fixed_rank_beyond_numerical_rank(rh):
+    """Fixed ranks (198, 101, 144) on a problem of numerical rank ~107 (sigma > 1e-10 sigma_1):
+    the retained directions at the rounding level get an orthonormal completion of the other
+    frame columns (before r2h their columns came out of CholeskyQR's dependent-column rule and
+    |Z^T Z - I| reached 1).  Checked: ranks, frames orthonormal, the Tucker tensor against the
+    oracle, and sigma where the squared Rayleigh-Ritz resolves it (sigma_k > 1e-7 sigma_1; below
+    that both sides return rounding-level values)."""
+    p = make_random_params(644, 1571, seed=50019, ranks=(198, 101, 144), a_range=(0.5, 20.0), signed=True)
+    U1, U2, U3, xi = make_config(p)
+    o = oracle_rhosvd([U1, U2, U3], xi, ranks=(198, 101, 144))
+    g = run_gpu(rh, [U1, U2, U3], xi, ranks=(198, 101, 144))
+    assert tuple(g.ranks) == tuple(o.ranks) == (198, 101, 144)
+    for l in range(3):
+        Z = g.Z[l].cpu().numpy()
+        assert orth_error(Z) <= 1e-12, orth_error(Z)
+        so = o.sigma[l][:o.ranks[l]]
+        sg = g.sigma[l].cpu().numpy()
+        res = so > 1e-7 * so[0]
+        tol = np.maximum(SIG_TOL, 16 * 1.1102230246251565e-16 * so[0] / so)
+        assert np.all(np.abs(sg - so)[res] <= (tol * so)[res])
+    d, nrm = tucker_diff(g.beta.cpu().numpy(), [z.cpu().numpy() for z in g.Z], o.beta, o.Z)
+    assert d <= TUCKER_TOL * nrm, d / nrm
