@@ -379,6 +379,21 @@ def test_fixed_rank_beyond_numerical_rank(rh, n, R, seed, eps, ranks, wide, sign
     _sweep_case_check(g, o, ranks)
 
 
+def test_fixed_rank_subspace_angle(rh):
+    """Fixed ranks (126, 21, 5) with wide cut gaps (seed-99 sweep case 34).  With no block
+    truncation after a fixed-rank iteration, one refinement step at rate rho = 0.31 left the
+    mode-1 subspace 5e-8 from the oracle's (sigma right to 1e-15, Tucker tensor 1.6e-9 off);
+    the Gram-domain iteration now runs to sin(theta_r) ~ 1e-12 in fixed-rank mode: 6e-15."""
+    ranks = (126, 21, 5)
+    p = make_random_params(633, 3450, seed=50034, ranks=ranks, a_range=(0.05, 400.0), signed=False)
+    U1, U2, U3, xi = make_config(p)
+    o = oracle_rhosvd([U1, U2, U3], xi, ranks=ranks)
+    g = run_gpu(rh, [U1, U2, U3], xi, ranks=ranks)
+    _sweep_case_check(g, o, ranks)
+    d, nrm = tucker_diff(g.beta.cpu().numpy(), [z.cpu().numpy() for z in g.Z], o.beta, o.Z)
+    assert d <= 1e-12 * nrm, d / nrm
+
+
 def test_full_space_eps_block(rh):
     """eps = 1e-4 on n = 197 < R: the block grows to the full space (r2h sweep case 20).  The
     refined full-space block tilted the kept subspace by up to 2e-8 (Tucker tensor 3e-10 or
