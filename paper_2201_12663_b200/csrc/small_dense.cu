@@ -19,8 +19,8 @@ namespace rhosvd {
 
 // ------------------------------------------------------------------ grid barrier
 __device__ __forceinline__ void grid_barrier(unsigned* bar) {
-  // sense-free generation barrier: gpu-scope release/acquire (a .sys-scope volatile
-  // spin, as plain `volatile` compiles to, costs tens of microseconds per barrier)
+  // cooperative-groups grid sync (the kernels are launched cooperatively); `bar` is kept in
+  // the signature for the callers and is unused
   (void)bar;
   cooperative_groups::this_grid().sync();
 }
