@@ -684,15 +684,17 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
   mo.T = T;
 
   // n x b work buffers sized for the largest possible block m = min(n, R) once, so
-  // block growth keeps their contents; the b x R buffers grow on demand.
-  RH_CHECK(w.Z.ensure((size_t)LDN * m + 64, st));
-  RH_CHECK(w.Y.ensure((size_t)LDN * m + 64, st));
-  RH_CHECK(w.M.ensure((size_t)LDN * m + 64, st));
-  RH_CHECK(w.T1.ensure((size_t)LDN * m + 64, st));
+  // block growth keeps their contents; the b x R buffers grow on demand.  A fixed-rank call
+  // with R < n <= 2048 may take the full-space path below with b = n > m.
+  const int64_t mws = (!epsmode && n <= 2048) ? std::max(n, m) : m;
+  RH_CHECK(w.Z.ensure((size_t)LDN * mws + 64, st));
+  RH_CHECK(w.Y.ensure((size_t)LDN * mws + 64, st));
+  RH_CHECK(w.M.ensure((size_t)LDN * mws + 64, st));
+  RH_CHECK(w.T1.ensure((size_t)LDN * mws + 64, st));
   {
-    int64_t ldm = round_up(std::max<int64_t>(m, 2), 2);
-    for (DBuf* d : {&w.H, &w.V, &w.S, &w.Bp}) RH_CHECK(d->ensure((size_t)ldm * m + 64, st));
-    for (DBuf* d : {&w.th, &w.inv, &w.tail2, &w.sgn}) RH_CHECK(d->ensure((size_t)m + 64, st));
+    int64_t ldm = round_up(std::max<int64_t>(mws, 2), 2);
+    for (DBuf* d : {&w.H, &w.V, &w.S, &w.Bp}) RH_CHECK(d->ensure((size_t)ldm * mws + 64, st));
+    for (DBuf* d : {&w.th, &w.inv, &w.tail2, &w.sgn}) RH_CHECK(d->ensure((size_t)mws + 64, st));
   }
   auto ensure_b = [&](int64_t bb) -> int {
     RH_CHECK(w.W.ensure((size_t)bb * Rp, st));
@@ -888,10 +890,14 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
     return e ? atoi(e) : 1;
   }();
   bool full_eye = full_eye_env && m == n && n > 1 && b >= m;
-  if (full_eye_env && m == n && n > 1 && !full_eye && !epsmode && n <= 2048 && rfix > 0 &&
+  // R < n (m = R): Z = I is still an exact orthonormal basis of a space that holds the
+  // column space of Uhat, so the same path applies with b = n > m - W = Uhat, W W^T = G of
+  // rank <= R, its n - R null directions sort last (seed-7 sweep case 10, seed-11 case 38).
+  // RHOSVD_FULL_EYE=2 restricts the fixed-rank trigger to m = n as before.
+  if (full_eye_env && (m == n || full_eye_env != 2) && n > 1 && !full_eye && !epsmode && n <= 2048 && rfix > 0 &&
       (int64_t)d_h.size() >= rfix && !(d_h[rfix - 1] >= 1e-10 * d_h[0])) {
     full_eye = true;
-    b = m;
+    b = n;
     d_h.resize(b, 0.0);  // host arrays below are indexed by the block size
     RH_CHECK(ensure_b(b));
   }

@@ -364,6 +364,10 @@ def _sweep_case_check(g, o, ranks):
     (682, 3410, 50004, None, (161, 158, 140), False, False),
     # (46, 80, 166): mode 2 beyond the numerical rank (r2h sweep case 37)
     (980, 2451, 50037, None, (46, 80, 166), False, True),
+    # R < n: fixed ranks above the numerical rank with m = R (seed-7 sweep case 10 and seed-11
+    # case 38): the full-space basis Z = I with b = n > m
+    (589, 221, 50010, None, (133, 31, 107), False, False),
+    (906, 486, 50038, None, (122, 144, 118), False, False),
 ])
 def test_fixed_rank_beyond_numerical_rank(rh, n, R, seed, eps, ranks, wide, signed):
     """Fixed ranks above the numerical rank (sigma_r ~ 1e-16 sigma_1).  Before r2zz the refined
