@@ -33,6 +33,8 @@ CASES = {
     "random": dict(n=70, R=517, seed=23, eps=1e-7),
     "cfg2": dict(config=2),
     "cfg3": dict(config=3),
+    # fixed ranks above the numerical rank with R < n (seed-7 sweep case 10): full-space path, b = n > R
+    "rltn": dict(n=589, R=221, seed=50010, eps=None, ranks=(133, 31, 107), signed=False),
 }
 
 
@@ -41,7 +43,8 @@ def _params(case):
     c = CASES[case]
     if "config" in c:
         return make_params(c["config"])
-    return make_random_params(c["n"], c["R"], seed=c["seed"], eps=c["eps"])
+    return make_random_params(c["n"], c["R"], seed=c["seed"], eps=c["eps"], ranks=c.get("ranks"),
+                              signed=c.get("signed", True))
 
 
 def _worker(rank, world, port, case, q, serial=False, extra=None, env=None):
@@ -268,5 +271,33 @@ def test_r_sharded_nccl_one_rank_per_gpu(case):
     assert tuple(g0["ranks"]) == tuple(o.ranks)
     for l in range(3):
         assert sigma_rel_err(g0["sigma"][l], o.sigma[l][:o.ranks[l]]) <= 1e-10
+    d, nrm = tucker_diff(g0["beta"], g0["Z"], o.beta, o.Z)
+    assert d <= 1e-9 * nrm
+
+
+def test_r_sharded_full_space_r_lt_n():
+    """The full-space path with b = n > R (fixed ranks above the numerical rank, R < n;
+    DESIGN.md 1) under R-sharding with mode parallelism, world 2 on one GPU: both ranks hold
+    bit-identical outputs; against the CPU oracle of the full problem the sweep criteria
+    hold - ranks, sigma within max(1e-10, 16 u sigma_1 / sigma_k) at every k (reading A13),
+    frames orthonormal to 1e-13, Tucker tensor within 1e-9."""
+    from oracle import orth_error, rhosvd as oracle_rhosvd, tucker_diff
+    from workloads import make_config
+
+    out = _run_world2("rltn", {})
+    g0, g1 = out[0], out[1]
+    p = _params("rltn")
+    assert g0["ranks"] == g1["ranks"] == list(p.ranks)
+    assert np.array_equal(g0["beta"], g1["beta"])
+    for l in range(3):
+        assert np.array_equal(g0["Z"][l], g1["Z"][l])
+        assert np.array_equal(g0["sigma"][l], g1["sigma"][l])
+    U1, U2, U3, xi = make_config(p)
+    o = oracle_rhosvd([U1, U2, U3], xi, eps=p.eps, ranks=p.ranks)
+    for l in range(3):
+        assert orth_error(g0["Z"][l]) <= 1e-13
+        so, sg = o.sigma[l][:o.ranks[l]], g0["sigma"][l]
+        tol = np.maximum(1e-10, 16 * 1.1102230246251565e-16 * so[0] / so)
+        assert np.all(np.abs(sg - so) <= tol * so), np.max(np.abs(sg - so) / (tol * so))
     d, nrm = tucker_diff(g0["beta"], g0["Z"], o.beta, o.Z)
     assert d <= 1e-9 * nrm
