@@ -443,6 +443,7 @@ struct CommSched {
     int root = -1;  // -1: sum all-reduce; >= 0: broadcast from this rank
     cudaStream_t st = nullptr;
     bool posted = false, done = false, finished = false;
+    bool phase_done = false;  // this mode has posted every collective of the current phase
     int status = RHOSVD_OK;
     std::string err;
   } req[3];
@@ -462,6 +463,20 @@ struct CommSched {
     req[mode].finished = true;
     cv.notify_all();
   }
+  // Phase boundary (mode parallelism): a mode calls this once it has posted its last
+  // collective before the final Jacobi, i.e. before it waits on the rank's Jacobi latch.
+  // The comm thread skips such a mode until every mode has reached the boundary, then
+  // resumes the round robin at mode 0.  Without it, modes with different numbers of
+  // refinement all-reduces deadlock: the comm thread waits for the next post of a mode
+  // whose thread waits on the latch for an owned Jacobi whose W W^T all-reduce comes later
+  // in the round robin (r2end: fixed ranks (133, 31, 107), n = 589, R = 221, world 2).
+  // The sequence stays a function of each mode's own program order, so it is identical on
+  // all ranks.
+  void phase_end(int mode) {
+    std::lock_guard<std::mutex> lk(mu);
+    req[mode].phase_done = true;
+    cv.notify_all();
+  }
   // comm thread
   void run() {
     cudaSetDevice(dev);
@@ -471,8 +486,18 @@ struct CommSched {
       if (req[0].finished && req[1].finished && req[2].finished) break;
       Req& r = req[l];
       if (!r.finished) {
-        cv.wait(lk, [&] { return r.posted || r.finished; });
-        if (r.posted) {
+        cv.wait(lk, [&] { return r.posted || r.finished || r.phase_done; });
+        if (r.phase_done) {
+          // at the boundary: skipped until all modes are there (posts made after the
+          // boundary wait for the reset), then the round robin restarts at mode 0
+          bool all = true;
+          for (int k = 0; k < 3; ++k) all = all && (req[k].finished || req[k].phase_done);
+          if (all) {
+            for (int k = 0; k < 3; ++k) req[k].phase_done = false;
+            l = 0;
+            continue;
+          }
+        } else if (r.posted) {
           r.posted = false;
           if (comm_trace()) fprintf(stderr, "[rhosvd comm exec] rank %d mode %d count %lld\n", comm->rank, l, (long long)r.count);
           lk.unlock();
@@ -1066,6 +1091,7 @@ static int solve_mode(Ctx& c, int mode, int64_t n, int64_t LDN, int64_t Rl, int6
       // eigenvectors go out by broadcast once every Jacobi this rank owns has finished
       int st_j = RHOSVD_OK, sw = 0;
       std::string err_j;
+      if (c.sched) c.sched->phase_end(mode);  // last collective before the Jacobi latch
       if (c.mp->owner) {
         // the rank's owned Jacobis share the GPU (p >= 3: one Jacobi with every SM)
         const int cap_saved = g_coop_cap;
