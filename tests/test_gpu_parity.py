@@ -412,3 +412,16 @@ def test_full_space_eps_block(rh):
     assert torch.equal(g0.beta, g1.beta)
     for l in range(3):
         assert torch.equal(g0.Z[l], g1.Z[l])
+
+
+@pytest.mark.parametrize("n,R,seed,signed", [(1037, 238, 50016, False), (766, 253, 50023, True)])
+def test_eps_block_full_column_space_r_lt_n(rh, n, R, seed, signed):
+    """eps = 1e-7 with R < n: the block grows to the whole column space (b = m = R < n).  The
+    refined R-column block left frames off the 1e-13 orthonormality bound (sweep seeds 17 / 23,
+    cases 16 / 23; ranks, sigma and the Tucker tensor passed); the block is now the full space
+    with b = n > m (Z = I, two Rayleigh-Ritz passes)."""
+    p = make_random_params(n, R, seed=seed, eps=1e-7, a_range=(0.5, 20.0), signed=signed)
+    U1, U2, U3, xi = make_config(p)
+    o = oracle_rhosvd([U1, U2, U3], xi, eps=1e-7)
+    g = run_gpu(rh, [U1, U2, U3], xi, eps=1e-7)
+    _sweep_case_check(g, o, None)
